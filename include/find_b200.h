@@ -1,0 +1,160 @@
+/*
+ * find_b200.h — C ABI of the B200-native FIND selected-inversion path.
+ *
+ * Drop-in boundary for the reference package find_selinv 0.1.0
+ * (/root/reference/pkg/src/find_selinv).  The reference is pure Python; its
+ * "FFI" for this path is the Python call
+ *     solve(mesh, a, sigma, config) -> SelectedInverse      (solver.py:586-701)
+ * which the Python host package paper_1104_0623_b200 keeps verbatim and
+ * implements on top of the entry points below (ctypes binding, see
+ * INTEGRATION.md).  No torch types cross this boundary: plain pointers,
+ * sizes and a cudaStream_t passed as void*.
+ *
+ * Complex numbers are interleaved (re, im) doubles — the memory layout of
+ * numpy/torch complex128.
+ *
+ * Return codes: FIND_OK 0, FIND_EINVAL 1 (invalid argument, maps to
+ * ValueError, solver.py:591-608), FIND_ESINGULAR 2 (singular pivot, maps to
+ * SingularPivotError, kernels.py:237-252 / solver.py:383-389),
+ * FIND_ECUDA 3 (CUDA error), FIND_ENOMEM 4 (workspace too small).
+ */
+#ifndef FIND_B200_H
+#define FIND_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FIND_OK 0
+#define FIND_EINVAL 1
+#define FIND_ESINGULAR 2
+#define FIND_ECUDA 3
+#define FIND_ENOMEM 4
+
+typedef struct find_plan find_plan;
+
+/* Status of one find_solve call (device-side pivot test mapped back to the
+ * reference's SingularPivotError(node, cluster), errors.py:8-18). */
+typedef struct find_status {
+  int32_t code;          /* FIND_* */
+  int32_t energy_idx;    /* energy point of the failing elimination, -1 if none */
+  int64_t cluster_label; /* cluster label (negative: complement cluster), 0 if none */
+  int64_t node_id;       /* mesh node of the failing pivot, -1 if none */
+  double pivot_ratio;    /* |u_kk| / max|A(S,S)| at the failing pivot (NaN if unknown) */
+  char message[160];
+} find_status;
+
+/* ---- energy-independent plan (host only; replaces build_cluster_tree +
+ *      annotate_boundaries + complement_boundary_sets, mesh.py:176-290, and
+ *      the merge bookkeeping of solver.py:97-132, 234-243) ---- */
+
+/* Build the nested-dissection plan for an nx*ny mesh whose operator has CSR
+ * pattern (indptr[n+1], indices[nnz]); node id = x + nx*y.  The pattern
+ * must be structurally symmetric (solver.py:593-594).  leaf_max as
+ * SolverConfig.leaf_max (mesh.py:176-206). */
+int find_plan_create(int64_t nx, int64_t ny, const int64_t* indptr, const int64_t* indices,
+                     int64_t nnz, int32_t leaf_max, find_plan** out, find_status* st);
+void find_plan_destroy(find_plan* plan);
+
+/* Plan statistics: out[0..15] = {n, nnz, n_clusters, n_elims, n_levels_up,
+ * n_levels_down, up_arena_elems, down_arena_elems, ws_elems, max_n, max_s,
+ * max_b, n_launch_groups, sparse_entries, tree_depth, n_leaves}. */
+int find_plan_info(const find_plan* plan, int64_t* out16);
+
+/* Node sets of one cluster, ascending ids (for set-for-set validation
+ * against mesh.py:209-290).  which: 0 = nodes, 1 = boundary B,
+ * 2 = private inner S, 3 = complement boundary B_{-c}, 4 = complement
+ * private inner S_{-c}.  Returns the set size (writes min(size, cap)
+ * entries), or -1 if the label does not exist. */
+int64_t find_plan_cluster_set(const find_plan* plan, int64_t label, int32_t which, int64_t* out,
+                              int64_t cap);
+
+/* Per-elimination shapes in execution order: kind (0 leaf seed, 1 upward
+ * merge, 2 downward merge, 3 final leaf step), s, b, label.  Arrays of
+ * n_elims entries (find_plan_info out[3]). */
+int find_plan_elims(const find_plan* plan, int32_t* kind, int32_t* s, int32_t* b, int64_t* label);
+
+/* CSR slots of the merge-structure exception entries (kernels.py:192-202,
+ * counted into SelectedInverse.stats at solver.py:217-219) for pass 0
+ * (upward merges) or 1 (downward merges); an entry counts when its value is
+ * nonzero.  Returns the number of slots (writes min(count, cap)). */
+int64_t find_plan_exception_slots(const find_plan* plan, int32_t pass, int64_t* out, int64_t cap);
+
+/* Exact multiplication count of the reference FlopLedger (kernels.py:48-146,
+ * charged at kernels.py:379,391,436, solver.py:388,664) for one energy
+ * point.  kernel: 0 naive, 1 parallel_inverse, 2 sequential_inverse,
+ * 3 block_lu, 4 naive_lu (KERNEL_NAMES order, solver.py:49).  Writes
+ * per-ledger-key numerators over the common denominator *den (=48) into
+ * num[FIND_LEDGER_KEYS] in the key order of find_ledger_key_name(). */
+#define FIND_LEDGER_KEYS 12
+int find_plan_ledger(const find_plan* plan, int32_t kernel, int32_t compute_gless, int64_t* num,
+                     int64_t* den);
+const char* find_ledger_key_name(int32_t key);
+
+/* ---- device side ---- */
+
+/* Bytes of device workspace find_solve needs for n_energies points. */
+size_t find_solve_workspace_bytes(const find_plan* plan, int32_t n_energies, int32_t compute_gless);
+
+/* Upload the plan's index maps to the current device (idempotent). */
+int find_plan_upload(find_plan* plan, find_status* st);
+
+/* Selected inversion for n_energies operators sharing the plan's pattern.
+ *   a_vals   device, [n_energies][nnz] complex128 (values of A(E_k) on the pattern)
+ *   s_vals   device, [nnz] complex128 if s_broadcast else [n_energies][nnz]
+ *            (Sigma^< on A's pattern; zeros where Sigma^< has no entry);
+ *            may be NULL when compute_gless == 0
+ *   gr_out   device, [n_energies][n] complex128  diag(G^r)
+ *   gl_out   device, [n_energies][n] complex128  diag(G^<) (NULL if !compute_gless)
+ *   ws       device workspace of >= find_solve_workspace_bytes()
+ *   stream   cudaStream_t
+ * Stream-ordered; on return the work is enqueued.  Call find_solve_status()
+ * (synchronises the stream) to obtain the pivot status. */
+int find_solve(find_plan* plan, const void* a_vals, const void* s_vals, int32_t s_broadcast,
+               int32_t n_energies, int32_t compute_gless, double pivot_rtol, void* gr_out,
+               void* gl_out, void* ws, size_t ws_bytes, void* stream, find_status* st);
+
+/* Same as find_solve restricted to launch groups [g_begin, g_end) of the
+ * plan's schedule (upward levels deepest-first, then per level the downward
+ * merges and the final leaf steps).  The device status word is reset only
+ * when g_begin == 0.  Used for per-level timing. */
+int find_solve_groups(find_plan* plan, const void* a_vals, const void* s_vals, int32_t s_broadcast,
+                      int32_t n_energies, int32_t compute_gless, double pivot_rtol, void* gr_out,
+                      void* gl_out, void* ws, size_t ws_bytes, int64_t g_begin, int64_t g_end,
+                      void* stream, find_status* st);
+
+/* Launch-group table (find_plan_info out[12] entries): pass (0 upward,
+ * 1 downward, 2 final), tree level, path (0 warp-per-elimination, 1 CTA),
+ * number of eliminations, and the largest s+b, s, b in the group.  Any
+ * pointer may be NULL. */
+int find_plan_groups(const find_plan* plan, int32_t* pass, int32_t* level, int32_t* path, int64_t* count,
+                     int32_t* max_n, int32_t* max_s, int32_t* max_b);
+
+/* Synchronise `stream` and decode the device status of the last find_solve
+ * that used `ws`. */
+int find_solve_status(find_plan* plan, void* ws, int32_t n_energies, void* stream, find_status* st);
+
+/* Number of kernel launches one find_solve enqueues. */
+int64_t find_solve_launch_count(const find_plan* plan);
+
+/* Unit-test shim with the reference's kernel-level signature
+ * schur_update + sigma_update (kernels.py:363-392) for ONE dense
+ * elimination input: ass[s*s], asb[s*b], abs[b*s], abb[b*b], and the four
+ * Sigma blocks (may be NULL), all row-major device buffers; writes
+ * u_out[b*b], r_out[b*b], l_out[b*s] (L = A(B,S) A(S,S)^{-1}).  Runs the
+ * same device code path as find_solve (force_path: -1 auto, 0 warp path,
+ * 1 CTA path).  Returns FIND_ESINGULAR with st->node_id = position k of the
+ * failing pivot. */
+int find_schur_sigma_update(int32_t s, int32_t b, const void* ass, const void* asb, const void* abs_,
+                            const void* abb, const void* sss, const void* ssb, const void* sbs,
+                            const void* sbb, double pivot_rtol, void* u_out, void* r_out, void* l_out,
+                            int32_t force_path, void* stream, find_status* st);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FIND_B200_H */

@@ -1,0 +1,549 @@
+// Host plan builder: nested-dissection tree, node sets, elimination schedule.
+//
+// Restates (from scratch, O(nnz * depth) instead of the reference's
+// O(n * #clusters) sparse mat-vec per cluster):
+//   build_cluster_tree        mesh.py:176-206
+//   boundary_nodes            mesh.py:209-221
+//   adjacent_nodes            mesh.py:224-232
+//   private_inner_nodes       mesh.py:235-252
+//   annotate_boundaries       mesh.py:255-264
+//   complement_boundary_sets  mesh.py:267-290
+//   _merge_permutation        solver.py:111-132   ([S_l, S_r, B_l, B_r])
+//   _Engine.store             solver.py:234-243   (U/R re-sorted to ascending B)
+//   FlopLedger charges        kernels.py:88-146, 379, 391, 436; solver.py:388, 664
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+
+#include "../../include/find_b200.h"
+#include "plan.h"
+
+using namespace findb200;
+
+namespace {
+
+void set_status(find_status* st, int code, const char* msg) {
+  if (!st) return;
+  st->code = code;
+  st->energy_idx = -1;
+  st->cluster_label = 0;
+  st->node_id = -1;
+  st->pivot_ratio = NAN;
+  std::snprintf(st->message, sizeof(st->message), "%s", msg);
+}
+
+// Scratch (complex elements) of one CTA-path elimination: M, MS, inverse
+// diagonal blocks (nb <= 32), pivots/permutation (int32, 4 per complex slot).
+int64_t scratch_elems(int64_t n, int64_t s) {
+  int64_t e = 2 * n * n + ((s + 31) / 32) * 1024 + 1024 + (3 * n + 3) / 4 + 2;
+  return (e + 1) & ~int64_t(1);
+}
+
+constexpr int32_t kSmallMaxN = 32;  // warp-per-elimination path up to this merged size
+
+struct Builder {
+  find_plan* P;
+  std::vector<int32_t> mark;  // generation marks over nodes
+  std::vector<int32_t> posv;  // position lookup over nodes
+  int32_t gen = 0;
+
+  explicit Builder(find_plan* p) : P(p), mark(p->n, 0), posv(p->n, -1) {}
+
+  void build_tree() {
+    // mesh.py:176-206: bisect the longer side (ties -> x), ceil half first.
+    struct Item { int64_t label; int32_t x0, y0, w, h, level, parent; int32_t slot_child; };
+    std::vector<Item> stack;
+    stack.push_back({1, 0, 0, (int32_t)P->nx, (int32_t)P->ny, 0, -1, -1});
+    while (!stack.empty()) {
+      Item it = stack.back();
+      stack.pop_back();
+      Cluster c;
+      c.label = it.label;
+      c.x0 = it.x0; c.y0 = it.y0; c.w = it.w; c.h = it.h; c.level = it.level;
+      c.parent = it.parent;
+      c.child0 = c.child1 = -1;
+      int32_t idx = (int32_t)P->clusters.size();
+      P->clusters.push_back(c);
+      if (it.parent >= 0) {
+        if (it.slot_child == 0) P->clusters[it.parent].child0 = idx;
+        else P->clusters[it.parent].child1 = idx;
+      }
+      P->depth = std::max(P->depth, it.level);
+      if (it.w <= P->leaf_max && it.h <= P->leaf_max) {
+        P->n_leaves++;
+        continue;
+      }
+      Item l = it, r = it;
+      l.label = 2 * it.label; r.label = 2 * it.label + 1;
+      l.level = r.level = it.level + 1;
+      l.parent = r.parent = idx;
+      l.slot_child = 0; r.slot_child = 1;
+      if (it.w >= it.h) {
+        int32_t wl = (it.w + 1) / 2;
+        l.w = wl; r.x0 = it.x0 + wl; r.w = it.w - wl;
+      } else {
+        int32_t hl = (it.h + 1) / 2;
+        l.h = hl; r.y0 = it.y0 + hl; r.h = it.h - hl;
+      }
+      stack.push_back(r);  // preorder: left popped first
+      stack.push_back(l);
+    }
+    std::vector<std::pair<int64_t, int32_t>> kv;
+    kv.reserve(P->clusters.size());
+    for (int32_t i = 0; i < (int32_t)P->clusters.size(); ++i) kv.push_back({P->clusters[i].label, i});
+    std::sort(kv.begin(), kv.end());
+    for (auto& e : kv) { P->label_keys.push_back(e.first); P->label_index.push_back(e.second); }
+  }
+
+  inline bool in_rect(const Cluster& c, int64_t v) const {
+    int64_t x = v % P->nx, y = v / P->nx;
+    return x >= c.x0 && x < c.x0 + c.w && y >= c.y0 && y < c.y0 + c.h;
+  }
+
+  // mesh.py:209-221 (B) and mesh.py:224-232 (complement boundary).
+  void boundary_sets(Cluster& c) {
+    c.B.clear();
+    c.CB.clear();
+    for (int32_t y = c.y0; y < c.y0 + c.h; ++y) {
+      for (int32_t x = c.x0; x < c.x0 + c.w; ++x) {
+        int64_t v = x + P->nx * (int64_t)y;
+        bool outside = false;
+        for (int64_t k = P->indptr[v]; k < P->indptr[v + 1]; ++k) {
+          int64_t u = P->indices[k];
+          if (u == v) continue;
+          if (!in_rect(c, u)) {
+            outside = true;
+            c.CB.push_back(u);
+          }
+        }
+        if (outside) c.B.push_back(v);
+      }
+    }
+    // rect iteration is ascending in id (row-major)
+    std::sort(c.CB.begin(), c.CB.end());
+    c.CB.erase(std::unique(c.CB.begin(), c.CB.end()), c.CB.end());
+  }
+
+  static std::vector<int64_t> set_union(const std::vector<int64_t>& a, const std::vector<int64_t>& b) {
+    std::vector<int64_t> out;
+    out.reserve(a.size() + b.size());
+    std::set_union(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(out));
+    return out;
+  }
+  static std::vector<int64_t> set_diff(const std::vector<int64_t>& a, const std::vector<int64_t>& b) {
+    std::vector<int64_t> out;
+    out.reserve(a.size());
+    std::set_difference(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(out));
+    return out;
+  }
+
+  void annotate() {
+    auto& C = P->clusters;
+    for (auto& c : C) boundary_sets(c);
+    // S: leaves = C \ B (mesh.py:259-261); internal = (B_l u B_r) \ B (mesh.py:249-251)
+    for (auto& c : C) {
+      if (c.leaf()) {
+        std::vector<int64_t> nodes;
+        nodes.reserve((size_t)c.w * c.h);
+        for (int32_t y = c.y0; y < c.y0 + c.h; ++y)
+          for (int32_t x = c.x0; x < c.x0 + c.w; ++x) nodes.push_back(x + P->nx * (int64_t)y);
+        c.S = set_diff(nodes, c.B);
+      } else {
+        c.S = set_diff(set_union(C[c.child0].B, C[c.child1].B), c.B);
+      }
+    }
+    // complement private inner (mesh.py:280-289), preorder so parents come first
+    for (auto& c : C) {
+      if (c.parent < 0) {
+        c.CB.clear();
+        c.CS.clear();
+        continue;
+      }
+      const Cluster& par = C[c.parent];
+      int32_t me = (int32_t)(&c - &C[0]);
+      const Cluster& sib = C[par.child0 == me ? par.child1 : par.child0];
+      c.CS = set_diff(set_union(par.CB, sib.B), c.CB);
+    }
+  }
+
+  // ---- elimination descriptors ----
+  int32_t next_gen() {
+    if (++gen == INT32_MAX) { std::fill(mark.begin(), mark.end(), 0); gen = 1; }
+    return gen;
+  }
+
+  // Build one elimination: merged order [S_l, S_r, B_l, B_r] (solver.py:111-132).
+  // left/right are ascending label lists (the stored blocks' order); `lblock`
+  // / `rblock` tell whether a stored (U, R) block exists for that side; sparse
+  // entries are generated for every (i, j) not covered by a block and present
+  // in the CSR pattern.
+  void add_elim(int32_t kind, int64_t label, const std::vector<int64_t>& left,
+                const std::vector<int64_t>& right, const std::vector<int64_t>& S,
+                const std::vector<int64_t>& Bsorted, int32_t left_arena, int64_t left_off,
+                int32_t right_arena, int64_t right_off, int32_t out_arena, int64_t out_off,
+                const std::vector<int64_t>* final_nodes, bool order_is_leaf_seed) {
+    ElimDesc d;
+    std::memset(&d, 0, sizeof(d));
+    const int32_t p = (int32_t)left.size(), q = (int32_t)right.size();
+    d.p = p;
+    d.kind = kind;
+    d.label = label;
+    d.left_arena = left_arena;
+    d.right_arena = right_arena;
+    d.left_off = left_off;
+    d.right_off = right_off;
+    d.out_arena = out_arena;
+    d.out_off = out_off;
+    // membership of S
+    int32_t g = next_gen();
+    for (int64_t v : S) mark[v] = g;
+    std::vector<int32_t> perm;
+    perm.reserve(p + q);
+    for (int32_t i = 0; i < p; ++i) if (mark[left[i]] == g) perm.push_back(i);
+    for (int32_t i = 0; i < q; ++i) if (mark[right[i]] == g) perm.push_back(p + i);
+    int32_t s = (int32_t)perm.size();
+    for (int32_t i = 0; i < p; ++i) if (mark[left[i]] != g) perm.push_back(i);
+    for (int32_t i = 0; i < q; ++i) if (mark[right[i]] != g) perm.push_back(p + i);
+    int32_t n = p + q, b = n - s;
+    if ((size_t)s != S.size() || (size_t)b != Bsorted.size()) {
+      std::fprintf(stderr, "find_b200: merge labels do not split into S and B (label %lld)\n", (long long)label);
+      throw std::runtime_error("merge labels do not split into the given S and B sets");
+    }
+    d.s = s; d.b = b; d.n = n;
+    auto lab = [&](int32_t k) { return k < p ? left[k] : right[k - p]; };
+    d.map_off = (int64_t)P->i32.size();
+    for (int32_t k = 0; k < n; ++k) P->i32.push_back(perm[k]);
+    d.rank_off = (int64_t)P->i32.size();
+    if (final_nodes) {
+      for (int32_t k = s; k < n; ++k) P->i32.push_back((int32_t)lab(perm[k]));
+    } else {
+      int32_t gb = next_gen();
+      for (size_t r = 0; r < Bsorted.size(); ++r) { mark[Bsorted[r]] = gb; posv[Bsorted[r]] = (int32_t)r; }
+      for (int32_t k = s; k < n; ++k) P->i32.push_back(posv[lab(perm[k])]);
+    }
+    d.slabel_off = (int64_t)P->slabels.size();
+    for (int32_t k = 0; k < s; ++k) P->slabels.push_back(lab(perm[k]));
+    // merged position of every label
+    int32_t gm = next_gen();
+    for (int32_t k = 0; k < n; ++k) { int64_t v = lab(perm[k]); mark[v] = gm; posv[v] = k; }
+    // side of every merged position
+    d.sparse_off = (int64_t)P->sparse.size();
+    const bool lb = left_arena != kArenaNone && !order_is_leaf_seed;
+    const bool rb = right_arena != kArenaNone;
+    for (int32_t k = 0; k < n; ++k) {
+      int32_t src = perm[k];
+      bool from_left = src < p;
+      int64_t v = lab(src);
+      for (int64_t e = P->indptr[v]; e < P->indptr[v + 1]; ++e) {
+        int64_t u = P->indices[e];
+        if (mark[u] != gm) continue;
+        int32_t j = posv[u];
+        bool u_left = perm[j] < p;
+        bool covered = (from_left == u_left) && (from_left ? lb : rb);
+        if (covered) continue;
+        P->sparse.push_back({k, j, e});
+      }
+    }
+    d.nsparse = (int32_t)((int64_t)P->sparse.size() - d.sparse_off);
+    if (kind == kUpMerge || kind == kDownMerge) {
+      // structure exceptions (kernels.py:192-202): off-diagonal entries of the
+      // S_l x S_r / S_r x S_l blocks and any entry of X, Y, Q, R.  All of them
+      // are cross entries, i.e. CSR-sourced.
+      int32_t ml = 0, nl = 0;
+      for (int32_t k = 0; k < s; ++k) ml += perm[k] < p;
+      for (int32_t k = s; k < n; ++k) nl += perm[k] < p;
+      auto& out = P->exc_slots[kind == kUpMerge ? 0 : 1];
+      for (int64_t t = d.sparse_off; t < (int64_t)P->sparse.size(); ++t) {
+        const int32_t i = P->sparse[t].i, j = P->sparse[t].j;
+        bool exc = false;
+        if (i < ml && j >= ml && j < s) exc = (i != j - ml);                   // B12 off-diagonal
+        else if (i >= ml && i < s && j < ml) exc = (i - ml != j);              // C21 off-diagonal
+        else if (i < ml && j >= s + nl) exc = true;                            // X
+        else if (i >= ml && i < s && j >= s && j < s + nl) exc = true;         // Y
+        else if (i >= s && i < s + nl && j >= ml && j < s) exc = true;         // Q
+        else if (i >= s + nl && j < ml) exc = true;                            // R
+        if (exc) out.push_back(P->sparse[t].csr);
+      }
+    }
+    P->elims.push_back(d);
+  }
+
+  void schedule() {
+    auto& C = P->clusters;
+    const int32_t D = P->depth;
+    std::vector<std::vector<int32_t>> by_level(D + 1);
+    for (int32_t i = 0; i < (int32_t)C.size(); ++i) by_level[C[i].level].push_back(i);
+    for (auto& v : by_level)
+      std::sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return C[a].label < C[b].label; });
+    std::vector<int64_t> up_off(C.size(), -1), down_off(C.size(), -1);
+    // upward arena: every non-root cluster, 2*b^2 (U then R)
+    int64_t acc = 0;
+    for (int32_t L = D; L >= 1; --L)
+      for (int32_t i : by_level[L]) { up_off[i] = acc; acc += 2 * (int64_t)C[i].B.size() * C[i].B.size(); }
+    P->arena_elems[kArenaUp] = acc;
+    int64_t down_max = 0;
+    for (int32_t L = 1; L <= D; ++L) {
+      int64_t a = 0;
+      for (int32_t i : by_level[L]) { down_off[i] = a; a += 2 * (int64_t)C[i].CB.size() * C[i].CB.size(); }
+      down_max = std::max(down_max, a);
+    }
+    P->arena_elems[kArenaDown0] = P->arena_elems[kArenaDown1] = down_max;
+    const std::vector<int64_t> empty;
+
+    auto emit_groups = [&](int64_t begin, int32_t pass, int32_t level) {
+      // sort the level's eliminations by merged size, split into paths
+      int64_t end = (int64_t)P->elims.size();
+      if (end == begin) return;
+      std::stable_sort(P->elims.begin() + begin, P->elims.end(),
+                       [](const ElimDesc& a, const ElimDesc& b) { return a.n < b.n; });
+      int64_t split = begin;
+      while (split < end && P->elims[split].n <= kSmallMaxN) ++split;
+      for (int path = 0; path < 2; ++path) {
+        int64_t gb = path == 0 ? begin : split, ge = path == 0 ? split : end;
+        if (gb == ge) continue;
+        LaunchGroup G;
+        G.begin = gb; G.end = ge; G.path = path; G.pass = pass; G.level = level;
+        G.max_n = G.max_s = G.max_b = 0;
+        int64_t ws = 0;
+        for (int64_t k = gb; k < ge; ++k) {
+          ElimDesc& d = P->elims[k];
+          G.max_n = std::max(G.max_n, d.n); G.max_s = std::max(G.max_s, d.s); G.max_b = std::max(G.max_b, d.b);
+          d.ws_off = ws;
+          if (path == 1) ws += scratch_elems(d.n, d.s);
+        }
+        G.ws_elems = ws;
+        P->ws_elems = std::max(P->ws_elems, ws);
+        P->groups.push_back(G);
+        P->max_n = std::max(P->max_n, G.max_n);
+        P->max_s = std::max(P->max_s, G.max_s);
+        P->max_b = std::max(P->max_b, G.max_b);
+      }
+    };
+
+    // ---- upward pass (solver.py:256-308), deepest level first ----
+    for (int32_t L = D; L >= 1; --L) {
+      int64_t begin = (int64_t)P->elims.size();
+      for (int32_t i : by_level[L]) {
+        const Cluster& c = C[i];
+        if (c.leaf()) {
+          std::vector<int64_t> order(c.S);
+          order.insert(order.end(), c.B.begin(), c.B.end());
+          add_elim(kLeafSeed, c.label, order, empty, c.S, c.B, kArenaNone, -1, kArenaNone, -1, kArenaUp, up_off[i],
+                   nullptr, true);
+        } else {
+          const Cluster& l = C[c.child0];
+          const Cluster& r = C[c.child1];
+          add_elim(kUpMerge, c.label, l.B, r.B, c.S, c.B, kArenaUp, up_off[c.child0], kArenaUp, up_off[c.child1],
+                   kArenaUp, up_off[i], nullptr, false);
+        }
+      }
+      if ((int64_t)P->elims.size() > begin) P->n_levels_up++;
+      emit_groups(begin, 0, L);
+    }
+    // ---- downward pass (solver.py:311-375) level by level, finals right after ----
+    for (int32_t L = 1; L <= D; ++L) {
+      int64_t begin = (int64_t)P->elims.size();
+      int32_t arena = (L % 2 == 1) ? kArenaDown1 : kArenaDown0;
+      int32_t parena = (L % 2 == 1) ? kArenaDown0 : kArenaDown1;
+      for (int32_t i : by_level[L]) {
+        const Cluster& c = C[i];
+        const Cluster& par = C[c.parent];
+        int32_t sib = par.child0 == i ? par.child1 : par.child0;
+        bool par_root = par.parent < 0;
+        add_elim(kDownMerge, -c.label, par.CB, C[sib].B, c.CS, c.CB, par_root ? kArenaNone : parena,
+                 par_root ? -1 : down_off[c.parent], kArenaUp, up_off[sib], arena, down_off[i], nullptr, false);
+      }
+      if ((int64_t)P->elims.size() > begin) P->n_levels_down++;
+      emit_groups(begin, 1, L);
+      begin = (int64_t)P->elims.size();
+      for (int32_t i : by_level[L]) {
+        const Cluster& c = C[i];
+        if (!c.leaf()) continue;
+        std::vector<int64_t> nodes;
+        for (int32_t y = c.y0; y < c.y0 + c.h; ++y)
+          for (int32_t x = c.x0; x < c.x0 + c.w; ++x) nodes.push_back(x + P->nx * (int64_t)y);
+        add_elim(kFinal, c.label, c.CB, nodes, c.CB, nodes, arena, down_off[i], kArenaNone, -1, kArenaNone, -1,
+                 &nodes, false);
+      }
+      emit_groups(begin, 2, L);
+    }
+    if (C[0].leaf()) {  // single-cluster mesh: only the final step of the root
+      int64_t begin = (int64_t)P->elims.size();
+      const Cluster& c = C[0];
+      std::vector<int64_t> nodes;
+      for (int32_t y = c.y0; y < c.y0 + c.h; ++y)
+        for (int32_t x = c.x0; x < c.x0 + c.w; ++x) nodes.push_back(x + P->nx * (int64_t)y);
+      add_elim(kFinal, c.label, empty, nodes, empty, nodes, kArenaNone, -1, kArenaNone, -1, kArenaNone, -1, &nodes,
+               false);
+      emit_groups(begin, 2, 0);
+    }
+  }
+};
+
+// ---- ledger (kernels.py:88-146) over a common denominator of 48 ----
+enum LedgerKey {
+  kNaiveDense = 0, kSigmaNaive, kDenseInverse, kGlessSandwich, kParallel, kSequential, kBlockLU, kNaiveLU,
+  kSigmaSparse, kKeyPad1, kKeyPad2, kKeyPad3
+};
+const char* kKeyNames[FIND_LEDGER_KEYS] = {"naive_dense", "sigma_naive", "dense_inverse", "gless_sandwich",
+                                            "parallel_inverse", "sequential_inverse", "block_lu", "naive_lu",
+                                            "sigma_sparse", "", "", ""};
+
+typedef __int128 i128;
+// 48 * polynomial, exact
+i128 p48_naive_dense(i128 s, i128 b) { return 16 * s * s * s + 48 * s * s * b + 48 * s * b * b; }
+i128 p48_sigma_naive(i128 s, i128 b) { return 48 * s * s * b + 144 * s * b * b; }
+i128 p48_sigma_sparse(i128 s, i128 b) { return 24 * s * s * b + 96 * s * b * b; }
+// m = s/2, n = b/2: c3*m^3 + c21*m^2 n + c12*m n^2 -> over 48: 48*c3/8 s^3 + 48*c21/8 s^2 b + 48*c12/8 s b^2
+i128 p48_mn(i128 s, i128 b, i128 c3_num, i128 c3_den, i128 c21_num, i128 c21_den, i128 c12_num, i128 c12_den) {
+  return (6 * c3_num / c3_den) * s * s * s + (6 * c21_num / c21_den) * s * s * b + (6 * c12_num / c12_den) * s * b * b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int find_plan_create(int64_t nx, int64_t ny, const int64_t* indptr, const int64_t* indices, int64_t nnz,
+                     int32_t leaf_max, find_plan** out, find_status* st) {
+  set_status(st, FIND_OK, "ok");
+  if (!out) { set_status(st, FIND_EINVAL, "out is NULL"); return FIND_EINVAL; }
+  *out = nullptr;
+  if (nx < 1 || ny < 1) { set_status(st, FIND_EINVAL, "mesh dimensions must be positive"); return FIND_EINVAL; }
+  if (leaf_max < 1) { set_status(st, FIND_EINVAL, "leaf_max must be >= 1"); return FIND_EINVAL; }
+  if (nx * ny > (int64_t)INT32_MAX) { set_status(st, FIND_EINVAL, "mesh too large"); return FIND_EINVAL; }
+  const int64_t n = nx * ny;
+  if (!indptr || (nnz > 0 && !indices) || indptr[0] != 0 || indptr[n] != nnz) {
+    set_status(st, FIND_EINVAL, "invalid CSR pattern");
+    return FIND_EINVAL;
+  }
+  for (int64_t v = 0; v < n; ++v)
+    if (indptr[v + 1] < indptr[v]) { set_status(st, FIND_EINVAL, "indptr not monotone"); return FIND_EINVAL; }
+  for (int64_t k = 0; k < nnz; ++k)
+    if (indices[k] < 0 || indices[k] >= n) { set_status(st, FIND_EINVAL, "entry index out of range"); return FIND_EINVAL; }
+  find_plan* P = new (std::nothrow) find_plan();
+  if (!P) { set_status(st, FIND_ENOMEM, "out of host memory"); return FIND_ENOMEM; }
+  try {
+    P->nx = nx; P->ny = ny; P->n = n; P->nnz = nnz; P->leaf_max = leaf_max;
+    P->indptr.assign(indptr, indptr + n + 1);
+    P->indices.assign(indices, indices + nnz);
+    Builder B(P);
+    B.build_tree();
+    B.annotate();
+    B.schedule();
+  } catch (const std::exception& e) {
+    set_status(st, FIND_EINVAL, e.what());
+    delete P;
+    return FIND_EINVAL;
+  }
+  *out = P;
+  return FIND_OK;
+}
+
+int find_plan_info(const find_plan* P, int64_t* o) {
+  if (!P || !o) return FIND_EINVAL;
+  int64_t sp = (int64_t)P->sparse.size();
+  int64_t v[16] = {P->n, P->nnz, (int64_t)P->clusters.size(), (int64_t)P->elims.size(), P->n_levels_up,
+                   P->n_levels_down, P->arena_elems[0], P->arena_elems[1], P->ws_elems, P->max_n, P->max_s,
+                   P->max_b, (int64_t)P->groups.size(), sp, P->depth, P->n_leaves};
+  std::memcpy(o, v, sizeof(v));
+  return FIND_OK;
+}
+
+int64_t find_plan_cluster_set(const find_plan* P, int64_t label, int32_t which, int64_t* out, int64_t cap) {
+  if (!P) return -1;
+  auto it = std::lower_bound(P->label_keys.begin(), P->label_keys.end(), label);
+  if (it == P->label_keys.end() || *it != label) return -1;
+  const Cluster& c = P->clusters[P->label_index[it - P->label_keys.begin()]];
+  std::vector<int64_t> nodes;
+  const std::vector<int64_t>* src = nullptr;
+  switch (which) {
+    case 0:
+      for (int32_t y = c.y0; y < c.y0 + c.h; ++y)
+        for (int32_t x = c.x0; x < c.x0 + c.w; ++x) nodes.push_back(x + P->nx * (int64_t)y);
+      src = &nodes;
+      break;
+    case 1: src = &c.B; break;
+    case 2: src = &c.S; break;
+    case 3: src = &c.CB; break;
+    case 4: src = &c.CS; break;
+    default: return -1;
+  }
+  int64_t sz = (int64_t)src->size();
+  if (out) for (int64_t k = 0; k < std::min(sz, cap); ++k) out[k] = (*src)[k];
+  return sz;
+}
+
+int find_plan_elims(const find_plan* P, int32_t* kind, int32_t* s, int32_t* b, int64_t* label) {
+  if (!P) return FIND_EINVAL;
+  for (size_t k = 0; k < P->elims.size(); ++k) {
+    if (kind) kind[k] = P->elims[k].kind;
+    if (s) s[k] = P->elims[k].s;
+    if (b) b[k] = P->elims[k].b;
+    if (label) label[k] = P->elims[k].label;
+  }
+  return FIND_OK;
+}
+
+int64_t find_plan_exception_slots(const find_plan* P, int32_t pass, int64_t* out, int64_t cap) {
+  if (!P || pass < 0 || pass > 1) return -1;
+  const auto& v = P->exc_slots[pass];
+  if (out) for (int64_t k = 0; k < std::min<int64_t>((int64_t)v.size(), cap); ++k) out[k] = v[k];
+  return (int64_t)v.size();
+}
+
+const char* find_ledger_key_name(int32_t key) {
+  if (key < 0 || key >= FIND_LEDGER_KEYS) return "";
+  return kKeyNames[key];
+}
+
+int find_plan_ledger(const find_plan* P, int32_t kernel, int32_t compute_gless, int64_t* num, int64_t* den) {
+  if (!P || !num || !den || kernel < 0 || kernel > 4) return FIND_EINVAL;
+  i128 acc[FIND_LEDGER_KEYS] = {0};
+  for (const ElimDesc& d : P->elims) {
+    i128 s = d.s, b = d.b;
+    const bool split = d.kind == kUpMerge || d.kind == kDownMerge;
+    if (d.kind == kFinal) {
+      // solver.py:404 naive schur, 410 sigma, 388 inverse c^3, 664 sandwich 2c^3
+      if (s > 0) {
+        acc[kNaiveDense] += p48_naive_dense(s, b);
+        if (compute_gless) acc[kSigmaNaive] += p48_sigma_naive(s, b);
+      }
+      acc[kDenseInverse] += 48 * b * b * b;
+      if (compute_gless) acc[kGlessSandwich] += 96 * b * b * b;
+      continue;
+    }
+    if (s == 0) continue;  // kernels.py:372-375 / 387-388 / 423-427: no charge
+    if (!split || kernel == 0) {
+      acc[kNaiveDense] += p48_naive_dense(s, b);
+      if (compute_gless) acc[kSigmaNaive] += p48_sigma_naive(s, b);
+      continue;
+    }
+    // block kernels (kernels.py:100-111), *_with_factor when G^< is requested
+    i128 v = 0;
+    const bool wf = compute_gless != 0;
+    switch (kernel) {
+      case 1: v = wf ? p48_mn(s, b, 8, 3, 6, 1, 4, 1) : p48_mn(s, b, 8, 3, 4, 1, 4, 1); break;
+      case 2: v = p48_mn(s, b, 4, 3, 5, 1, 4, 1); break;
+      case 3: v = wf ? p48_mn(s, b, 4, 3, 5, 1, 4, 1) : p48_mn(s, b, 4, 3, 4, 1, 5, 1); break;
+      case 4: v = wf ? p48_mn(s, b, 8, 3, 15, 2, 4, 1) : p48_mn(s, b, 8, 3, 13, 2, 4, 1); break;
+    }
+    acc[3 + kernel] += v;
+    if (compute_gless) acc[kSigmaSparse] += p48_sigma_sparse(s, b);
+  }
+  for (int k = 0; k < FIND_LEDGER_KEYS; ++k) num[k] = (int64_t)acc[k];
+  *den = 48;
+  return FIND_OK;
+}
+
+void find_plan_free_device(find_plan* P);  // find_solve.cu
+
+void find_plan_destroy(find_plan* P) {
+  if (!P) return;
+  find_plan_free_device(P);
+  delete P;
+}
+
+}  // extern "C"

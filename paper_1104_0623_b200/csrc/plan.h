@@ -1,0 +1,85 @@
+// Internal plan structures shared by the host plan builder (plan.cpp) and the
+// device driver (find_solve.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace findb200 {
+
+// Elimination kinds (execution semantics of solver.py):
+enum ElimKind : int32_t {
+  kLeafSeed = 0,   // upward leaf: order = S u B seeded from A (solver.py:276-291)
+  kUpMerge = 1,    // upward internal merge of the two children (solver.py:293-307)
+  kDownMerge = 2,  // complement of c = parent complement (+) sibling (solver.py:339-364)
+  kFinal = 3,      // final leaf step S = ring, B = leaf nodes (solver.py:392-418, 644-669)
+};
+
+// Arenas that hold per-cluster (U, R) blocks, one copy per energy point.
+enum Arena : int32_t { kArenaNone = -1, kArenaUp = 0, kArenaDown0 = 1, kArenaDown1 = 2 };
+
+// One elimination (one merge + Schur/Sigma update), POD, device-visible.
+struct alignas(16) ElimDesc {
+  int32_t s, b, n, p;        // |S|, |B|, s+b, |left|
+  int32_t kind, nsparse;     // ElimKind, number of sparse (CSR-sourced) entries
+  int32_t left_arena, right_arena;
+  int32_t out_arena, pad0;
+  int64_t label;             // cluster label (negative = complement); final: leaf label
+  int64_t left_off, right_off;  // complex-element offsets of child U blocks in their arena (R follows at +sz*sz)
+  int64_t out_off;           // offset of the output U block (R at +b*b); final: unused
+  int64_t map_off;           // int32[n]: merged position -> index into [left ++ right]
+  int64_t rank_off;          // int32[b]: merged B position -> sorted rank (final: mesh node id)
+  int64_t sparse_off;        // sparse entries [sparse_off, sparse_off+nsparse)
+  int64_t ws_off;            // complex-element offset of this elimination's scratch (per energy)
+  int64_t slabel_off;        // int64 host-only array: S labels in merged order (error reporting)
+};
+
+struct LaunchGroup {
+  int64_t begin, end;  // ElimDesc range
+  int32_t path;        // 0 = warp-per-elimination small path, 1 = CTA blocked path
+  int32_t pass;        // 0 up, 1 down, 2 final
+  int32_t level;
+  int32_t max_n, max_s, max_b;
+  int64_t ws_elems;    // scratch per energy used by this group
+};
+
+struct SparseEntry {  // merged (row, col) <- csr value slot
+  int32_t i, j;
+  int64_t csr;
+};
+
+struct Cluster {
+  int64_t label;
+  int32_t x0, y0, w, h, level;
+  int32_t parent;   // index, -1 for root
+  int32_t child0, child1;  // indices, -1 if leaf
+  std::vector<int64_t> B, S, CB, CS;
+  bool leaf() const { return child0 < 0; }
+};
+
+}  // namespace findb200
+
+struct find_plan {
+  int64_t nx = 0, ny = 0, n = 0, nnz = 0;
+  int32_t leaf_max = 2;
+  std::vector<int64_t> indptr, indices;
+  std::vector<findb200::Cluster> clusters;  // preorder
+  std::vector<int64_t> label_keys;          // sorted labels for lookup
+  std::vector<int32_t> label_index;         // parallel to label_keys
+  std::vector<findb200::ElimDesc> elims;
+  std::vector<findb200::LaunchGroup> groups;
+  std::vector<int32_t> i32;                 // maps and ranks
+  std::vector<int64_t> slabels;             // S labels (merged order) per elimination
+  std::vector<findb200::SparseEntry> sparse;
+  std::vector<int64_t> exc_slots[2];         // CSR slots of structure-exception entries (up, down)
+  int64_t arena_elems[3] = {0, 0, 0};
+  int64_t ws_elems = 0;
+  int32_t max_n = 0, max_s = 0, max_b = 0, depth = 0, n_leaves = 0;
+  int32_t n_levels_up = 0, n_levels_down = 0;
+  // device copies (owned), set by find_plan_upload
+  int device = -1;
+  void* d_elims = nullptr;
+  void* d_i32 = nullptr;
+  void* d_sparse = nullptr;
+};

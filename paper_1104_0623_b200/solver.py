@@ -1,0 +1,209 @@
+"""Drop-in ``solve`` on the B200 path (mirror of find_selinv/solver.py:53-89, 586-701).
+
+Same signature, validation, error types and result fields as the reference;
+the arithmetic runs in the sm_100a kernels behind the C ABI (include/find_b200.h).
+There is no CPU fallback: without a CUDA device the call raises.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+from .errors import NativeLibraryError
+from .ledger import BLOCK_KERNELS, HERMITIAN_KERNELS, KERNEL_NAMES, FlopLedger
+from .operators import check_pattern_subset, check_structural_symmetry, is_hermitian
+from .plan import Plan, plan_for
+
+
+@dataclass
+class SolverConfig:
+    """solver.py:53-71 (same fields, defaults and validation)."""
+
+    kernel: str = "naive"
+    use_symmetry: bool = False
+    compute_gless: bool = True
+    compute_offdiag: bool = False
+    tiling: str = "full-leaves"
+    leaf_max: int = 2
+    pivot_rtol: float = 1e-12
+    sigma_mode: str = "auto"
+    debug_checks: bool = False
+
+    def __post_init__(self):
+        if self.kernel not in KERNEL_NAMES:
+            raise ValueError(f"unknown kernel {self.kernel!r}; choose from {KERNEL_NAMES}")
+        if self.tiling not in ("full-leaves", "half-leaves"):
+            raise ValueError(f"unknown tiling {self.tiling!r}")
+        if self.kernel in HERMITIAN_KERNELS:
+            self.use_symmetry = True
+
+
+@dataclass
+class SelectedInverse:
+    """solver.py:82-89."""
+
+    gr_diag: np.ndarray
+    gless_diag: np.ndarray | None
+    offdiag: dict | None
+    ledger: FlopLedger
+    timings: dict = field(default_factory=dict)
+    stats: dict = field(default_factory=dict)
+
+
+@dataclass
+class SelectedInverseBatch:
+    """Result of :func:`solve_batch`: one row per energy point."""
+
+    gr_diag: np.ndarray  # [nE, n]
+    gless_diag: np.ndarray | None
+    ledger: FlopLedger  # per energy point
+    timings: dict = field(default_factory=dict)
+    stats: dict = field(default_factory=dict)
+
+
+def _csr_sorted(m) -> sp.csr_matrix:
+    m = m.tocsr()
+    if not m.has_sorted_indices:
+        m = m.copy()
+        m.sort_indices()
+    return m
+
+
+def sigma_on_pattern(a: sp.csr_matrix, sigma: sp.csr_matrix) -> np.ndarray:
+    """Sigma values scattered onto A's CSR slots (zeros where Sigma has no entry)."""
+    n = a.shape[0]
+    rows_a = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.indptr))
+    keys = rows_a * n + a.indices.astype(np.int64)
+    s = sigma.tocoo()
+    skeys = s.row.astype(np.int64) * n + s.col.astype(np.int64)
+    pos = np.searchsorted(keys, skeys)
+    ok = (pos < keys.size) & (keys[np.minimum(pos, keys.size - 1)] == skeys)
+    if not ok.all():
+        raise ValueError("scattering pattern exceeds the operator pattern")
+    out = np.zeros(a.nnz, np.complex128)
+    np.add.at(out, pos, s.data.astype(np.complex128))
+    return out
+
+
+def _validate(mesh, a, sigma, config):
+    """solver.py:591-608."""
+    if a.n != mesh.n:
+        raise ValueError(f"operator size {a.n} does not match mesh with {mesh.n} nodes")
+    if not check_structural_symmetry(a):
+        raise ValueError("operator pattern is not structurally symmetric")
+    if config.compute_gless:
+        if sigma is None:
+            raise ValueError("compute_gless requires a scattering matrix")
+        if sigma.n != a.n:
+            raise ValueError("scattering matrix size mismatch")
+        if not check_pattern_subset(sigma, a):
+            raise ValueError("scattering pattern exceeds the operator pattern")
+    if config.kernel == "ldlt":
+        d = a.matrix - a.matrix.T
+        scale = max(np.abs(a.matrix.data).max() if a.matrix.nnz else 1.0, 1.0)
+        if d.nnz and np.abs(d.data).max() > 1e-10 * scale:
+            raise ValueError("ldlt kernel requires a (complex-)symmetric operator")
+    elif config.use_symmetry and not is_hermitian(a.matrix):
+        raise ValueError("use_symmetry requires a Hermitian operator")
+    if config.compute_offdiag or config.tiling != "full-leaves":
+        raise NotImplementedError(
+            "off-diagonal extraction and half-leaves tiling are not in this build (SURVEY.md §8(f) row 1)")
+
+
+def _device():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("the FIND B200 path needs a CUDA device (there is no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, compute_gless=True, pivot_rtol=1e-12):
+    """Run the plan on host value arrays a_vals [nE, nnz], s_vals [nnz] or [nE, nnz].
+
+    Host -> device copies, the level-batched kernels, status check and the
+    device -> host copy of the diagonals.  Returns (gr, gl, device_seconds_up, device_seconds_down)."""
+    import torch
+
+    dev = _device()
+    a_vals = np.ascontiguousarray(np.atleast_2d(a_vals), dtype=np.complex128)
+    n_e = a_vals.shape[0]
+    stream = torch.cuda.current_stream(dev)
+    a_d = torch.from_numpy(a_vals).to(dev, non_blocking=False)
+    s_d = None
+    s_b = True
+    if compute_gless:
+        s_vals = np.ascontiguousarray(s_vals, dtype=np.complex128)
+        s_b = s_vals.ndim == 1
+        s_d = torch.from_numpy(s_vals).to(dev)
+    gr_d = torch.empty((n_e, plan.n), dtype=torch.complex128, device=dev)
+    gl_d = torch.empty((n_e, plan.n), dtype=torch.complex128, device=dev) if compute_gless else None
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record(stream)
+    ws = plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, stream=stream, groups=(0, plan.first_down_group))
+    ev[1].record(stream)
+    plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, ws=ws, stream=stream,
+             groups=(plan.first_down_group, -1))
+    ev[2].record(stream)
+    plan.check_status(ws, n_e, stream)
+    gr = gr_d.cpu().numpy()
+    gl = gl_d.cpu().numpy() if gl_d is not None else None
+    return gr, gl, ev[0].elapsed_time(ev[1]) * 1e-3, ev[1].elapsed_time(ev[2]) * 1e-3
+
+
+def _stats(plan: Plan, a_data: np.ndarray) -> dict:
+    return {
+        "upward_exception_entries": int(np.count_nonzero(a_data[plan.exception_slots(0)])),
+        "downward_exception_entries": int(np.count_nonzero(a_data[plan.exception_slots(1)])),
+    }
+
+
+def solve(mesh, a, sigma, config: SolverConfig) -> SelectedInverse:
+    """Run the full selected inversion on one operator (solver.py:586-701)."""
+    t0 = time.perf_counter()
+    _validate(mesh, a, sigma, config)
+    am = _csr_sorted(a.matrix)
+    plan, _ = plan_for(mesh.nx, mesh.ny, am.indptr, am.indices, config.leaf_max)
+    s_vals = sigma_on_pattern(am, _csr_sorted(sigma.matrix)) if config.compute_gless else None
+    sigma_herm = is_hermitian(sigma.matrix) if sigma is not None else False
+    t1 = time.perf_counter()
+    gr, gl, t_up, t_down = solve_values(plan, am.data[None, :], s_vals, config.compute_gless, config.pivot_rtol)
+    t3 = time.perf_counter()
+    ledger = plan.ledger(config.kernel, config.compute_gless, sigma_herm, config.sigma_mode)
+    return SelectedInverse(
+        gr_diag=gr[0],
+        gless_diag=gl[0] if gl is not None else None,
+        offdiag=None,
+        ledger=ledger,
+        timings={"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},
+        stats=_stats(plan, am.data),
+    )
+
+
+def solve_batch(mesh, a_list, sigma, config: SolverConfig) -> SelectedInverseBatch:
+    """Energy-batched solve: every operator shares A's pattern; one launch per
+    (tree level, size class) covers all energy points."""
+    t0 = time.perf_counter()
+    if not a_list:
+        raise ValueError("a_list is empty")
+    _validate(mesh, a_list[0], sigma, config)
+    am0 = _csr_sorted(a_list[0].matrix)
+    vals = np.empty((len(a_list), am0.nnz), np.complex128)
+    for k, a in enumerate(a_list):
+        am = _csr_sorted(a.matrix)
+        if am.nnz != am0.nnz or not (np.array_equal(am.indptr, am0.indptr) and np.array_equal(am.indices, am0.indices)):
+            raise ValueError("all operators of a batch must share one sparsity pattern")
+        vals[k] = am.data
+    plan, _ = plan_for(mesh.nx, mesh.ny, am0.indptr, am0.indices, config.leaf_max)
+    s_vals = sigma_on_pattern(am0, _csr_sorted(sigma.matrix)) if config.compute_gless else None
+    sigma_herm = is_hermitian(sigma.matrix) if sigma is not None else False
+    t1 = time.perf_counter()
+    gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol)
+    t3 = time.perf_counter()
+    return SelectedInverseBatch(gr, gl, plan.ledger(config.kernel, config.compute_gless, sigma_herm, config.sigma_mode),
+                                {"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},
+                                _stats(plan, am0.data))

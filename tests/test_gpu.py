@@ -1,0 +1,253 @@
+"""GPU parity tests: the sm_100a path (through the C ABI) against the reference's
+golden outputs, the CPU oracle and dense inversion.  Tolerance: BASELINE.json
+north star, max|Δ|/max|ref| <= 1e-10 for diag(G^r) and diag(G^<)."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import golden_frac, load_golden, problem_from_golden, stencil_operator, stencil_ops, stencil_sigma
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(x, ref):
+    return float(np.max(np.abs(np.asarray(x) - np.asarray(ref))) / np.max(np.abs(ref)))
+
+
+# ---------------------------------------------------------------- kernel shim
+def shim(ass, asb, abs_, abb, sss=None, ssb=None, sbs=None, sbb=None, path=-1, rtol=1e-12):
+    import torch
+
+    from paper_1104_0623_b200 import _native
+
+    s, b = ass.shape[0], abb.shape[0]
+    dev = torch.device("cuda", 0)
+    t = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex128)).to(dev)
+    ins = [t(x) for x in (ass, asb, abs_, abb)]
+    gl = sss is not None
+    sig = [t(x) for x in (sss, ssb, sbs, sbb)] if gl else [None] * 4
+    u = torch.zeros((b, b), dtype=torch.complex128, device=dev)
+    r = torch.zeros((b, b), dtype=torch.complex128, device=dev)
+    l = torch.zeros((b, s), dtype=torch.complex128, device=dev)
+    st = _native.FindStatus()
+    ptr = lambda x: C.c_void_p(x.data_ptr()) if x is not None and x.numel() else C.c_void_p(0)
+    rc = _native.lib().find_schur_sigma_update(
+        s, b, *[ptr(x) for x in ins], *[ptr(x) for x in sig], rtol, ptr(u), ptr(r) if gl else C.c_void_p(0), ptr(l),
+        path, C.c_void_p(torch.cuda.current_stream().cuda_stream), C.byref(st))
+    return rc, st, u.cpu().numpy(), r.cpu().numpy(), l.cpu().numpy()
+
+
+def dense_input(s, b, seed, shift=None):
+    rng = np.random.default_rng(seed)
+    rnd = lambda p, q: rng.standard_normal((p, q)) + 1j * rng.standard_normal((p, q))
+    shift = shift if shift is not None else 3 * max(s, b, 1)
+    return rnd(s, s) + shift * np.eye(s), rnd(s, b), rnd(b, s), rnd(b, b) + shift * np.eye(b)
+
+
+def ref_update(ass, asb, abs_, abb, sss, ssb, sbs, sbb):
+    """kernels.py:363-392 in numpy (explicit L)."""
+    l = abs_ @ np.linalg.inv(ass)
+    u = abb - l @ asb
+    lh = l.conj().T
+    r = sbb - l @ ssb - sbs @ lh + (l @ sss) @ lh
+    return u, r, l
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_shim_scalar_case(cuda, path):
+    # test_kernels.py:51-60: U = 2.5, L = 0.5 exactly
+    rc, st, u, r, l = shim(np.array([[2.0]]), np.array([[1.0]]), np.array([[1.0]]), np.array([[3.0]]), path=path)
+    assert rc == 0
+    assert u[0, 0] == 2.5 and l[0, 0] == 0.5
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_shim_identity_pivot(cuda, path):
+    # test_kernels.py:39-48
+    abs_ = np.random.default_rng(0).standard_normal((3, 2)).astype(complex)
+    abb = np.arange(9, dtype=complex).reshape(3, 3)
+    rc, st, u, r, l = shim(np.eye(2), np.zeros((2, 3)), abs_, abb, path=path)
+    assert rc == 0
+    assert np.array_equal(u, abb) and np.array_equal(l, abs_)
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_shim_singular_pivot_position(cuda, path):
+    # test_kernels.py:80-91: zero A(S,S) fails at position 0 (node = s_labels[0])
+    rc, st, *_ = shim(np.zeros((2, 2)), np.zeros((2, 1)), np.zeros((1, 2)), np.eye(1), path=path)
+    assert rc == 2 and st.node_id == 0
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_shim_sigma_scalar_expansion(cuda, path):
+    # test_kernels.py:102-106: R = 1 + |l|^2 for S = I, L = l
+    lv = 0.5 + 0.5j
+    rc, st, u, r, l = shim(np.eye(1), np.zeros((1, 1)), np.array([[lv]]), np.eye(1), np.eye(1), np.zeros((1, 1)),
+                           np.zeros((1, 1)), np.eye(1), path=path)
+    assert rc == 0 and np.isclose(r[0, 0], 1 + abs(lv) ** 2)
+
+
+@pytest.mark.parametrize("s,b,path", [(2, 4, 0), (7, 3, 0), (16, 16, 0), (20, 12, 0), (7, 3, 1), (30, 40, 1),
+                                      (64, 33, 1), (100, 90, 1), (257, 194, 1), (300, 5, 1), (0, 9, 1), (9, 0, 1),
+                                      (500, 120, 1), (33, 1, 1)])
+def test_shim_dense_vs_numpy(cuda, s, b, path):
+    ass, asb, abs_, abb = dense_input(s, b, seed=s * 131 + b)
+    rng = np.random.default_rng(s + 7 * b)
+    n = s + b
+    sm = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    sss, ssb, sbs, sbb = sm[:s, :s], sm[:s, s:], sm[s:, :s], sm[s:, s:]
+    rc, st, u, r, l = shim(ass, asb, abs_, abb, sss, ssb, sbs, sbb, path=path)
+    assert rc == 0, st.text
+    if s == 0:
+        assert np.array_equal(u, abb) and np.array_equal(r, sbb)
+        return
+    ue, re_, le = ref_update(ass, asb, abs_, abb, sss, ssb, sbs, sbb)
+    if b:
+        assert rel(u, ue) < 1e-12 and rel(r, re_) < 1e-12 and rel(l, le) < 1e-12
+
+
+def test_shim_pivoting_needed(cuda):
+    # zero leading diagonal forces row interchanges inside the panel
+    s, b = 70, 20
+    ass, asb, abs_, abb = dense_input(s, b, seed=5, shift=0.0)
+    ass[np.arange(s), np.arange(s)] = 0.0
+    for path in (1,):
+        rc, st, u, r, l = shim(ass, asb, abs_, abb, path=path)
+        assert rc == 0
+        ue, _, le = ref_update(ass, asb, abs_, abb, np.eye(s), np.zeros((s, b)), np.zeros((b, s)), np.eye(b))
+        assert rel(u, ue) < 1e-10 and rel(l, le) < 1e-10
+    ass2, asb2, abs2, abb2 = dense_input(12, 6, seed=6, shift=0.0)
+    ass2[np.arange(12), np.arange(12)] = 0.0
+    rc, st, u, r, l = shim(ass2, asb2, abs2, abb2, path=0)
+    ue, _, le = ref_update(ass2, asb2, abs2, abb2, np.eye(12), np.zeros((12, 6)), np.zeros((6, 12)), np.eye(6))
+    assert rc == 0 and rel(u, ue) < 1e-10
+
+
+# ---------------------------------------------------------------- full solves
+@pytest.mark.parametrize("name", ["cfg0", "c5_16x12", "c9_20x20", "c5_8x30"])
+def test_solve_matches_reference_golden(cuda, name):
+    from paper_1104_0623_b200 import Mesh, SolverConfig, SparseOperator, solve, solve_batch
+
+    g = load_golden(name)
+    p = problem_from_golden(g)
+    mesh = Mesh(p.nx, p.ny)
+    sig = SparseOperator(p.sigma_csr())
+    ops = [SparseOperator(p.a_csr(k)) for k in range(p.energies.size)]
+    res = solve(mesh, ops[0], sig, SolverConfig())
+    assert rel(res.gr_diag, g["gr"][0]) < TOL
+    assert rel(res.gless_diag, g["gl"][0]) < TOL
+    assert res.ledger.multiplications == golden_frac(g["W"])
+    batch = solve_batch(mesh, ops, sig, SolverConfig())
+    for k in range(p.energies.size):
+        assert rel(batch.gr_diag[k], g["gr"][k]) < TOL
+        assert rel(batch.gless_diag[k], g["gl"][k]) < TOL
+
+
+@pytest.mark.parametrize("name", ["stencil_6x4", "stencil_4x4", "stencil_3x5", "stencil_5x7", "stencil_8x8",
+                                  "stencil_16x16"])
+@pytest.mark.parametrize("leaf_max", [1, 2, 3])
+def test_solve_matches_reference_stencil(cuda, name, leaf_max):
+    from paper_1104_0623_b200 import SolverConfig, solve
+
+    g = load_golden(name)
+    if f"gr_{leaf_max}" not in g.files:
+        pytest.skip("no golden")
+    mesh, a, s = stencil_ops(g)
+    res = solve(mesh, a, s, SolverConfig(leaf_max=leaf_max))
+    assert rel(res.gr_diag, g[f"gr_{leaf_max}"]) < TOL
+    assert rel(res.gless_diag, g[f"gl_{leaf_max}"]) < TOL
+    # exact check against dense inversion at small N (north star)
+    assert np.max(np.abs(res.gr_diag - g["dense_gr"]) / np.abs(g["dense_gr"])) < TOL
+    assert np.max(np.abs(res.gless_diag - g["dense_gl"]) / np.abs(g["dense_gl"])) < TOL
+
+
+def test_solve_identity(cuda):
+    from paper_1104_0623_b200 import SolverConfig, SparseOperator, assemble_sigma, build_mesh, solve
+
+    mesh = build_mesh(3, 4)
+    ids = np.arange(12)
+    a = SparseOperator.from_coo(12, ids, ids, np.ones(12))
+    res = solve(mesh, a, assemble_sigma(mesh, "diagonal", np.ones(12)), SolverConfig())
+    assert np.allclose(res.gr_diag, 1.0) and np.allclose(res.gless_diag, 1.0)
+
+
+def test_diagonal_operator(cuda):
+    from paper_1104_0623_b200 import SolverConfig, SparseOperator, build_mesh, solve
+
+    mesh = build_mesh(3, 3)
+    ids = np.arange(9)
+    a = SparseOperator.from_coo(9, ids, ids, 2.0 * np.ones(9))
+    res = solve(mesh, a, None, SolverConfig(compute_gless=False))
+    assert np.allclose(res.gr_diag, 0.5) and res.gless_diag is None
+
+
+@pytest.mark.parametrize("nx,ny", [(1, 1), (2, 2), (1, 7), (5, 1), (2, 9), (11, 3)])
+def test_degenerate_meshes_vs_dense(cuda, nx, ny):
+    from paper_1104_0623_b200 import SolverConfig, solve
+
+    mesh, a = stencil_operator(nx, ny, seed=nx * 10 + ny)
+    s = stencil_sigma(mesh, seed=3, mode="stencil")
+    res = solve(mesh, a, s, SolverConfig())
+    d = a.to_dense()
+    g = np.linalg.inv(d)
+    gl = g @ s.to_dense() @ g.conj().T
+    assert rel(res.gr_diag, np.diagonal(g)) < TOL
+    assert rel(res.gless_diag, np.diagonal(gl)) < TOL
+
+
+def test_singular_pivot_reports_cluster(cuda):
+    # test_solver.py:331-341
+    from paper_1104_0623_b200 import SingularPivotError, SolverConfig, SparseOperator, build_mesh, solve
+
+    mesh = build_mesh(4, 4)
+    ids = np.arange(16)
+    adj = mesh.adjacency().tocoo()
+    vals = np.concatenate([np.zeros(16), np.ones(adj.nnz)])
+    a = SparseOperator.from_coo(16, np.concatenate([ids, adj.row]), np.concatenate([ids, adj.col]), vals)
+    with pytest.raises(SingularPivotError) as err:
+        solve(mesh, a, None, SolverConfig(compute_gless=False))
+    assert err.value.node is not None and err.value.cluster is not None
+
+
+def test_determinism_bit_identical(cuda):
+    from paper_1104_0623_b200 import SolverConfig, solve
+
+    g = load_golden("c9_20x20")
+    p = problem_from_golden(g)
+    from paper_1104_0623_b200 import Mesh, SparseOperator
+
+    args = (Mesh(p.nx, p.ny), SparseOperator(p.a_csr(0)), SparseOperator(p.sigma_csr()), SolverConfig())
+    r1, r2 = solve(*args), solve(*args)
+    assert np.array_equal(r1.gr_diag, r2.gr_diag) and np.array_equal(r1.gless_diag, r2.gless_diag)
+
+
+def test_cfg1_full_scale_properties(cuda):
+    """BASELINE cfg1 (130x130, 16 energies) at full size: independent sparse-LU
+    spot checks (A^H x = e_i) and the sign structure of G^r / G^<."""
+    import scipy.sparse.linalg as spla
+
+    from paper_1104_0623_b200.configs import config_problem
+    from paper_1104_0623_b200.plan import plan_for
+    from paper_1104_0623_b200.solver import solve_values
+
+    p = config_problem(1)
+    plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
+    gr, gl, _, _ = solve_values(plan, p.a_vals_all(), p.s_vals)
+    assert np.all(gr.imag < 0)  # retarded: Im G^r_ii < 0
+    assert np.max(np.abs(gl.real)) < 1e-10 * np.max(np.abs(gl))  # G^< = i G Gamma G^H
+    assert np.all(gl.imag > -1e-12 * np.max(np.abs(gl)))
+    rng = np.random.default_rng(0)
+    sig = p.sigma_csr()
+    for k in (0, 7, 15):
+        lu = spla.splu(p.a_csr(k).conj().T.tocsc())
+        nodes = rng.choice(p.n, 8, replace=False)
+        nodes[:2] = [0, p.n - 1]
+        for i in nodes:
+            e = np.zeros(p.n, complex)
+            e[i] = 1.0
+            x = lu.solve(e)  # x = A^{-H} e_i  ->  G^r_ii = conj(x_i), G^<_ii = x^H Sigma x
+            assert abs(gr[k, i] - np.conj(x[i])) < 1e-10 * np.max(np.abs(gr[k]))
+            assert abs(gl[k, i] - np.vdot(x, sig @ x)) < 1e-10 * np.max(np.abs(gl[k]))

@@ -1,0 +1,42 @@
+"""Pin the CPU oracle (oracle/find_oracle.py) against the reference's own outputs."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_frac, load_golden, problem_from_golden, stencil_ops
+from oracle.find_oracle import FindOracle, dense_gless_diag, dense_gr_diag, work_naive
+
+
+@pytest.mark.parametrize("name", ["c5_16x12", "c9_20x20", "c5_8x30", "cfg0"])
+def test_oracle_matches_reference_contacts(name):
+    g = load_golden(name)
+    p = problem_from_golden(g)
+    o = FindOracle(p.nx, p.ny, p.a_csr(0))
+    energies = range(p.energies.size) if name != "cfg0" else [0]
+    for k in energies:
+        r = o.solve(p.a_csr(k), p.sigma_csr())
+        assert np.abs(r.gr_diag - g["gr"][k]).max() / np.abs(g["gr"][k]).max() < 1e-13
+        assert np.abs(r.gless_diag - g["gl"][k]).max() / np.abs(g["gl"][k]).max() < 1e-13
+        assert r.ledger.multiplications == golden_frac(g["W"])
+    assert work_naive(o) == golden_frac(g["W"])
+
+
+@pytest.mark.parametrize("name", ["stencil_6x4", "stencil_4x4", "stencil_3x5", "stencil_5x7", "stencil_8x8"])
+@pytest.mark.parametrize("leaf_max", [1, 2, 3])
+def test_oracle_matches_reference_stencil(name, leaf_max):
+    g = load_golden(name)
+    mesh, a, s = stencil_ops(g)
+    o = FindOracle(mesh.nx, mesh.ny, a.matrix, leaf_max)
+    r = o.solve(a.matrix, s.matrix)
+    np.testing.assert_allclose(r.gr_diag, g[f"gr_{leaf_max}"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(r.gless_diag, g[f"gl_{leaf_max}"], rtol=1e-12, atol=1e-14)
+    assert r.ledger.multiplications == golden_frac(g[f"W_{leaf_max}"])
+
+
+def test_oracle_matches_dense_small():
+    g = load_golden("stencil_6x4")
+    mesh, a, s = stencil_ops(g)
+    o = FindOracle(mesh.nx, mesh.ny, a.matrix)
+    r = o.solve(a.matrix, s.matrix)
+    assert np.max(np.abs(r.gr_diag - dense_gr_diag(a.to_dense())) / np.abs(g["dense_gr"])) < 1e-10
+    assert np.max(np.abs(r.gless_diag - dense_gless_diag(a.to_dense(), s.to_dense())) / np.abs(g["dense_gl"])) < 1e-10
