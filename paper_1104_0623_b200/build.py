@@ -41,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         obj = OUT.parent / (Path(src).stem + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
         if src.endswith(".cpp"):
-            cmd = [NVCC, *FLAGS, "-x", "c++", "-c", str(CSRC / src), "-o", str(obj)]
+            cmd = [NVCC, *FLAGS, "-Wno-deprecated-gpu-targets", "-x", "c++", "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

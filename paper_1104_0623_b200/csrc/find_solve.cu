@@ -33,6 +33,9 @@
 
 using namespace findb200;
 
+int64_t find_scratch_elems(int64_t n, int64_t s, int nb);
+void find_build_tasks(find_plan* P);
+
 namespace {
 
 // ------------------------------------------------------------------ complex
@@ -194,7 +197,12 @@ __device__ void final_epilogue_warp(const SolveParams& P, const ElimDesc& d, int
   }
 }
 
-__global__ void __launch_bounds__(kSmallWarps * 32) small_elim_kernel(SolveParams P, int64_t count, int nmax, int ld) {
+// Per-warp shared memory (complex elements): M [nmax][ld] (A, later Sigma),
+// XC [xcap] (X = Y L11^-1, and U_f for final steps), 3 x 32 ints.
+__host__ __device__ constexpr int small_warp_elems(int nmax, int ld, int xcap) { return nmax * ld + xcap + 24; }
+
+__global__ void __launch_bounds__(kSmallWarps * 32) small_elim_kernel(SolveParams P, int64_t count, int nmax, int ld,
+                                                                      int xcap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t idx = (int64_t)blockIdx.x * kSmallWarps + warp;
@@ -203,15 +211,17 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_elim_kernel(SolveParam
   const ElimDesc d = P.elims[idx];
   const int64_t elim_global = P.elim_base + idx;
   const int n = d.n, s = d.s, b = d.b;
-  double2* MA = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * (2 * nmax * ld + 64);
-  double2* MS = MA + nmax * ld;
-  int* piv = reinterpret_cast<int*>(MS + nmax * ld);  // piv, sig, isg: 3 x 32 ints
+  double2* MA = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * small_warp_elems(nmax, ld, xcap);
+  double2* XC = MA + nmax * ld;
+  int* piv = reinterpret_cast<int*>(XC + xcap);  // piv, sig, isg: 3 x 32 ints
   int* sig = piv + 32;
+  int* isg = sig + 32;
   const int32_t* map = P.i32 + d.map_off;
   const int32_t* rank = P.i32 + d.rank_off;
   const double2* lblk = d.left_arena >= 0 ? P.arena[d.left_arena] + (int64_t)e * P.arena_elems[d.left_arena] + d.left_off : nullptr;
   const double2* rblk = d.right_arena >= 0 ? P.arena[d.right_arena] + (int64_t)e * P.arena_elems[d.right_arena] + d.right_off : nullptr;
   const double2* av = P.a_vals + (int64_t)e * P.nnz;
+  const SparseEntry* sp = P.sparse + d.sparse_off;
 
   // ---- gather A (solver.py:203-205) ----
   const int mj = lane < n ? map[lane] : 0;
@@ -220,85 +230,83 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_elim_kernel(SolveParam
     if (lane < n) MA[i * ld + lane] = block_entry(d, lblk, rblk, mi, mj);
   }
   __syncwarp();
-  const SparseEntry* sp = P.sparse + d.sparse_off;
   for (int t = lane; t < d.nsparse; t += 32) {
-    SparseEntry en = sp[t];
+    const SparseEntry en = sp[t];
     MA[en.i * ld + en.j] = ldg2(av + en.csr);
   }
   __syncwarp();
 
-  // ---- partial LU, pivoting among S rows (kernels.py:237-252, 376) ----
+  // ---- partial LU, pivoting among S rows (kernels.py:237-252, 376); lane = row ----
   double scale = 0.0;
-  for (int i = 0; i < s; ++i)
-    if (lane < s) scale = fmax(scale, cabs(MA[i * ld + lane]));
+  if (lane < s)
+    for (int j = 0; j < s; ++j) scale = fmax(scale, cabs(MA[lane * ld + j]));
   for (int o = 16; o; o >>= 1) scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
   int bad = (s > 0 && scale == 0.0) ? 0 : INT32_MAX;
   for (int k = 0; k < s; ++k) {
     double v = (lane >= k && lane < s) ? cabs1(MA[lane * ld + k]) : -1.0;
     int vi = lane;
     for (int o = 16; o; o >>= 1) {
-      double ov = __shfl_xor_sync(0xffffffffu, v, o);
-      int oi = __shfl_xor_sync(0xffffffffu, vi, o);
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
       if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
     }
     const int pr = vi;
     if (lane == 0) piv[k] = pr;
-    if (pr != k && lane < n) {
-      double2 t = MA[k * ld + lane];
+    if (pr != k && lane < n) {  // lane = column for the interchange
+      const double2 tmp = MA[k * ld + lane];
       MA[k * ld + lane] = MA[pr * ld + lane];
-      MA[pr * ld + lane] = t;
+      MA[pr * ld + lane] = tmp;
     }
     __syncwarp();
     const double2 ukk = MA[k * ld + k];
     if (cabs(ukk) < P.rtol * scale && bad == INT32_MAX) bad = k;
     const double2 uinv = cinv(ukk);
-    // column below the pivot (S and B rows), then rank-1 update (lane = column)
-    double2 urow = lane < n ? MA[k * ld + lane] : cz();
-    __syncwarp();
-    for (int i = k + 1; i < n; ++i) {
-      double2 l = cmul(MA[i * ld + k], uinv);
-      __syncwarp();
-      if (lane == k) MA[i * ld + k] = l;
-      else if (lane > k && lane < n) MA[i * ld + lane] = cfms(MA[i * ld + lane], l, urow);
+    if (lane > k && lane < n) {  // lane = row: multiplier and rank-1 update of its own row
+      double2* rw = MA + lane * ld;
+      const double2 l = cmul(rw[k], uinv);
+      rw[k] = l;
+      for (int j = k + 1; j < n; ++j) rw[j] = cfms(rw[j], l, MA[k * ld + j]);
     }
     __syncwarp();
   }
   if (bad != INT32_MAX && lane == 0) report_bad(P, elim_global, e, bad);
 
-  // ---- X = Y L11^-1 (row per lane) ----
+  // ---- X = Y L11^-1 (row per lane), stashed in XC [b][s] ----
   if (lane < b) {
-    double2* row = MA + (s + lane) * ld;
+    double2* rw = MA + (s + lane) * ld;
     for (int k = s - 1; k >= 0; --k) {
-      double2 acc = row[k];
-      for (int m = k + 1; m < s; ++m) acc = cfms(acc, row[m], MA[m * ld + k]);
-      row[k] = acc;
+      double2 acc = rw[k];
+      for (int m = k + 1; m < s; ++m) acc = cfms(acc, rw[m], MA[m * ld + k]);
+      rw[k] = acc;
     }
+    for (int k = 0; k < s; ++k) XC[lane * s + k] = rw[k];
+  }
+  // permutation sigma from the pivot sequence: pivoted row k = merged row sig[k]
+  if (lane == 0) {
+    for (int k = 0; k < s; ++k) sig[k] = k;
+    for (int k = 0; k < s; ++k) { const int tmp = sig[k]; sig[k] = sig[piv[k]]; sig[piv[k]] = tmp; }
   }
   __syncwarp();
-
-  if (d.kind != kFinal && d.out_arena >= 0) {  // store U sorted (solver.py:234-243)
+  if (P.dbg_l && idx == 0 && e == 0 && lane < b)
+    for (int k = 0; k < s; ++k) P.dbg_l[(int64_t)lane * s + sig[k]] = XC[lane * s + k];
+  double2* UF = XC + b * s;  // final step: U_f kept for the epilogue
+  if (d.kind == kFinal) {
+    if (lane < b)
+      for (int j = 0; j < b; ++j) UF[lane * b + j] = MA[(s + lane) * ld + s + j];
+  } else if (d.out_arena >= 0) {  // store U sorted (solver.py:234-243)
     double2* out = P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off;
     const int rj = lane < b ? rank[lane] : 0;
     for (int i = 0; i < b; ++i)
       if (lane < b) out[(int64_t)rank[i] * b + rj] = MA[(s + i) * ld + s + lane];
   }
-  // permutation sigma from the pivot sequence: pivoted row k = merged row sig[k]
-  if (lane == 0) {
-    for (int k = 0; k < s; ++k) sig[k] = k;
-    for (int k = 0; k < s; ++k) { int t = sig[k]; sig[k] = sig[piv[k]]; sig[piv[k]] = t; }
-  }
   __syncwarp();
-  if (P.dbg_l && idx == 0 && e == 0 && lane < b)
-    for (int k = 0; k < s; ++k) P.dbg_l[(int64_t)lane * s + sig[k]] = MA[(s + lane) * ld + k];
+  double2* MS = MA;  // Sigma reuses the A buffer
   if (P.compute_gless) {
     const double2* lr = lblk ? lblk + (int64_t)d.p * d.p : nullptr;
     const int q = n - d.p;
     const double2* rr = rblk ? rblk + (int64_t)q * q : nullptr;
     const double2* sv = P.s_vals + (P.s_broadcast ? 0 : (int64_t)e * P.nnz);
-    // inverse permutation for the sparse scatter: merged pos -> pivoted pos
-    int* isg = sig + 32;
-    if (lane < n && lane >= s) isg[lane] = lane;  // B part: identity
-    __syncwarp();
+    if (lane < n && lane >= s) isg[lane] = lane;
     if (lane < s) isg[sig[lane]] = lane;
     __syncwarp();
     const int pj = lane < n ? map[lane < s ? sig[lane] : lane] : 0;
@@ -308,7 +316,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_elim_kernel(SolveParam
     }
     __syncwarp();
     for (int t = lane; t < d.nsparse; t += 32) {
-      SparseEntry en = sp[t];
+      const SparseEntry en = sp[t];
       MS[isg[en.i] * ld + isg[en.j]] = ldg2(sv + en.csr);
     }
     __syncwarp();
@@ -316,7 +324,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_elim_kernel(SolveParam
     if (lane < n)
       for (int i = 0; i < b; ++i) {
         double2 acc = MS[(s + i) * ld + lane];
-        for (int k = 0; k < s; ++k) acc = cfms(acc, MA[(s + i) * ld + k], MS[k * ld + lane]);
+        for (int k = 0; k < s; ++k) acc = cfms(acc, XC[i * s + k], MS[k * ld + lane]);
         MS[(s + i) * ld + lane] = acc;
       }
     __syncwarp();
@@ -324,7 +332,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_elim_kernel(SolveParam
     if (lane < b)
       for (int i = 0; i < b; ++i) {
         double2 acc = MS[(s + i) * ld + s + lane];
-        for (int k = 0; k < s; ++k) acc = cfms(acc, MS[(s + i) * ld + k], cconj(MA[(s + lane) * ld + k]));
+        for (int k = 0; k < s; ++k) acc = cfms(acc, MS[(s + i) * ld + k], cconj(XC[lane * s + k]));
         MS[(s + i) * ld + s + lane] = acc;
       }
     __syncwarp();
@@ -337,82 +345,170 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_elim_kernel(SolveParam
   }
   if (d.kind == kFinal) {
     __syncwarp();
-    final_epilogue_warp(P, d, elim_global, e, MA + s * ld + s, ld, MS + s * ld + s, ld, lane);
+    final_epilogue_warp(P, d, elim_global, e, UF, b, MS + s * ld + s, ld, lane);
   }
 }
 
-// ================================================================== blocked path
+// ================================================================== CTA path: phase launches
+// Every phase of the blocked elimination is one launch over a flattened task
+// list covering all eliminations of the level and (grid.y) all energy points,
+// so the trailing updates and the T / R products of a level spread over all
+// 148 SMs and many CTAs per SM hide the latency of the sequential panel steps.
 constexpr int kThreads = 256;
-constexpr int kTM = 64, kTN = 64, kKC = 16, kSK = kKC + 4;  // smem row stride 20 complex = 320 B
+constexpr int kKC = 16, kSK = kKC + 4;  // K chunk; smem row stride 20 complex = 320 B (conflict-free frags)
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// C[M x N] (-)= A[M x K] * op(B).  op(B)[k][n] = B[k*ldb + n] (CONJT = false) or
-// conj(B[n*ldb + k]) (CONJT = true).  SUB: C -= AB, else C = AB.  Whole CTA.
-// In-place use is safe when each output tile's K-range of its own rows/cols
-// is the only aliased region (the LU/TRSM uses below).
-template <bool CONJT, bool SUB>
-__device__ void cta_gemm(double2* C, int64_t ldc, const double2* A, int64_t lda, const double2* B, int64_t ldb, int M,
-                         int N, int K, double2* smem) {
-  if (M <= 0 || N <= 0) return;
-  double2* As = smem;
-  double2* Bs = smem + kTM * kSK;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
-  const int tiles_m = (M + kTM - 1) / kTM, tiles_n = (N + kTN - 1) / kTN;
-  const int fr = lane >> 2, fc = lane & 3;
-  for (int tile = 0; tile < tiles_m * tiles_n; ++tile) {
-    const int m0 = (tile / tiles_n) * kTM, n0 = (tile % tiles_n) * kTN;
-    double acc[4][2][2][2];
+template <int NT = 256>
+__device__ void block_argmax(double& v, int& vi, double* cv, int* ci) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+  for (int o = 16; o; o >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oi = __shfl_xor_sync(0xffffffffu, vi, o);
+    if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
+  }
+  if (lane == 0) { cv[warp] = v; ci[warp] = vi; }
+  __syncthreads();
+  v = cv[0]; vi = ci[0];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) { acc[a][c][0][0] = acc[a][c][0][1] = acc[a][c][1][0] = acc[a][c][1][1] = 0.0; }
-    for (int k0 = 0; k0 < K; k0 += kKC) {
+  for (int w = 1; w < NT / 32; ++w) {
+    double ov = cv[w];
+    int oi = ci[w];
+    if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
+  }
+}
+
+struct Scr {
+  double2* M;   // merged A, then L\U, Y/X, U               [n][n]
+  double2* MS;  // merged, pivot-permuted Sigma, then T, R  [n][n]
+  int* PIV;     // pivot rows (global S index)              [s]
+  int* SIG;     // pivoted position -> merged position      [s]
+  int* ISG;     // merged position -> pivoted position      [s]
+  int* PERM;    // current panel's net row interchange: {nd, src[64], dst[64]}
+  double* scale;
+  double* pmax;   // per gather row chunk: max |A(S,S)| over its rows   [ceil(n/16)]
+  double2* LINV;  // per panel j: L_jj^-1  [NB][NB]   (valid when nb > 0)
+  double2* UINV;  // per panel j: U_jj^-1  [NB][NB]
+};
+// Layout must match find_scratch_elems() in plan.cpp.
+__device__ __forceinline__ Scr scratch_of(const SolveParams& P, const ElimDesc& d, int e, int nb = 0) {
+  Scr r;
+  r.M = P.scratch + (int64_t)e * P.scratch_elems + d.ws_off;
+  const int64_t nn = (int64_t)d.n * d.n;
+  r.MS = r.M + nn;
+  r.PIV = reinterpret_cast<int*>(r.M + 2 * nn);
+  r.SIG = r.PIV + d.s;
+  r.ISG = r.SIG + d.s;
+  r.PERM = r.ISG + d.s;
+  const int64_t ints = (3 * d.s + 132 + 3) / 4;
+  r.scale = reinterpret_cast<double*>(r.M + 2 * nn + ints);
+  r.pmax = r.scale + 2;
+  r.LINV = r.M + 2 * nn + ints + 1 + (d.n + 31) / 32;
+  r.UINV = nb ? r.LINV + (int64_t)((d.s + nb - 1) / nb) * nb * nb : r.LINV;
+  return r;
+}
+
+// One DMMA output tile: acc[BM x BN] = A[BM x K] * op(B)[K x BN], operands
+// streamed global -> shared memory with a 2-stage cp.async pipeline.
+// op(B)[k][c] = B[k*ldb + c] (BT = false) or conj(B[c*ldb + k]) (BT = true).
+template <int WM, int WN, int MT, int NT, bool BT>
+struct Tile {
+  static constexpr int BM = WM * MT * 8, BN = WN * NT * 8;
+  static constexpr int STAGE = (BM + BN) * kSK;
+  static constexpr size_t SMEM = 2 * STAGE * sizeof(double2);
+  double acc[MT][NT][2][2];
+
+  __device__ __forceinline__ void zero() {
 #pragma unroll
-      for (int r = 0; r < (kTM * kKC) / kThreads; ++r) {
-        const int q = tid + r * kThreads;
-        const int row = q >> 4, kk = q & 15;
-        double2 v = cz();
-        if (m0 + row < M && k0 + kk < K) v = A[(int64_t)(m0 + row) * lda + k0 + kk];
-        As[row * kSK + kk] = v;
+    for (int a = 0; a < MT; ++a)
+#pragma unroll
+      for (int c = 0; c < NT; ++c) acc[a][c][0][0] = acc[a][c][0][1] = acc[a][c][1][0] = acc[a][c][1][1] = 0.0;
+  }
+
+  __device__ __forceinline__ void load(const double2* A, int64_t lda, const double2* B, int64_t ldb, int Mv, int Nv,
+                                       int K, int kc, double2* st) {
+    const int tid = threadIdx.x;
+    double2* As = st;
+    double2* Bs = st + BM * kSK;
+    const int k0 = kc * kKC;
+#pragma unroll
+    for (int q = tid; q < BM * kKC; q += kThreads) {
+      const int row = q / kKC, kk = q % kKC;
+      const bool ok = row < Mv && k0 + kk < K;
+      cp_async16(As + row * kSK + kk, ok ? A + (int64_t)row * lda + k0 + kk : A, ok);
+    }
+    if (BT) {
+#pragma unroll
+      for (int q = tid; q < BN * kKC; q += kThreads) {
+        const int col = q / kKC, kk = q % kKC;
+        const bool ok = col < Nv && k0 + kk < K;
+        cp_async16(Bs + col * kSK + kk, ok ? B + (int64_t)col * ldb + k0 + kk : B, ok);
       }
-      if (!CONJT) {
+    } else {
 #pragma unroll
-        for (int r = 0; r < (kTN * kKC) / kThreads; ++r) {
-          const int q = tid + r * kThreads;
-          const int kk = q >> 6, col = q & 63;
-          double2 v = cz();
-          if (k0 + kk < K && n0 + col < N) v = B[(int64_t)(k0 + kk) * ldb + n0 + col];
-          Bs[col * kSK + kk] = v;
-        }
+      for (int q = tid; q < BN * kKC; q += kThreads) {
+        const int kk = q / BN, col = q % BN;
+        const bool ok = col < Nv && k0 + kk < K;
+        cp_async16(Bs + col * kSK + kk, ok ? B + (int64_t)(k0 + kk) * ldb + col : B, ok);
+      }
+    }
+    cp_async_commit();
+  }
+
+  __device__ __forceinline__ void mma(const double2* A, int64_t lda, const double2* B, int64_t ldb, int Mv, int Nv,
+                                      int K, double2* smem) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp % WM, wn = warp / WM;
+    const int fr = lane >> 2, fc = lane & 3;
+    const int nk = (K + kKC - 1) / kKC;
+    if (nk <= 0) return;
+    // fragments of this warp that hold valid rows / cols (warp-uniform); the
+    // zero padding of partial tiles is not multiplied
+    const int mtv = min(MT, max(0, (Mv - wm * MT * 8 + 7) / 8));
+    const int ntv = min(NT, max(0, (Nv - wn * NT * 8 + 7) / 8));
+    load(A, lda, B, ldb, Mv, Nv, K, 0, smem);
+    for (int kc = 0; kc < nk; ++kc) {
+      if (kc + 1 < nk) {
+        load(A, lda, B, ldb, Mv, Nv, K, kc + 1, smem + ((kc + 1) & 1) * STAGE);
+        cp_async_wait<1>();
       } else {
-#pragma unroll
-        for (int r = 0; r < (kTN * kKC) / kThreads; ++r) {
-          const int q = tid + r * kThreads;
-          const int col = q >> 4, kk = q & 15;
-          double2 v = cz();
-          if (k0 + kk < K && n0 + col < N) v = cconj(B[(int64_t)(n0 + col) * ldb + k0 + kk]);
-          Bs[col * kSK + kk] = v;
-        }
+        cp_async_wait<0>();
       }
       __syncthreads();
+      const double2* As = smem + (kc & 1) * STAGE;
+      const double2* Bs = As + BM * kSK;
+      const int kv = K - kc * kKC;
 #pragma unroll
       for (int kk = 0; kk < kKC; kk += 4) {
-        double2 a[4], b[2];
+        if (kk >= kv || mtv == 0 || ntv == 0) break;
+        double2 a[MT], b[NT];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) a[mt] = As[(wm * 32 + mt * 8 + fr) * kSK + kk + fc];
+        for (int mt = 0; mt < MT; ++mt) a[mt] = As[(wm * MT * 8 + mt * 8 + fr) * kSK + kk + fc];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) b[nt] = Bs[(wn * 16 + nt * 8 + fr) * kSK + kk + fc];
+        for (int nt = 0; nt < NT; ++nt) {
+          b[nt] = Bs[(wn * NT * 8 + nt * 8 + fr) * kSK + kk + fc];
+          if (BT) b[nt].y = -b[nt].y;
+        }
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
+        for (int mt = 0; mt < MT; ++mt) {
+          if (mt >= mtv) break;
           const double nai = -a[mt].y;
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
+          for (int nt = 0; nt < NT; ++nt) {
+            if (nt >= ntv) break;
             dmma(acc[mt][nt][0][0], acc[mt][nt][0][1], a[mt].x, b[nt].x);
             dmma(acc[mt][nt][0][0], acc[mt][nt][0][1], nai, b[nt].y);
             dmma(acc[mt][nt][1][0], acc[mt][nt][1][1], a[mt].x, b[nt].y);
@@ -422,284 +518,647 @@ __device__ void cta_gemm(double2* C, int64_t ldc, const double2* A, int64_t lda,
       }
       __syncthreads();
     }
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int r = m0 + wm * 32 + mt * 8 + fr;
-          const int c = n0 + wn * 16 + nt * 8 + 2 * fc + i;
-          if (r < M && c < N) {
-            double2* p = C + (int64_t)r * ldc + c;
-            double2 v = make_double2(acc[mt][nt][0][i], acc[mt][nt][1][i]);
-            *p = SUB ? csub(*p, v) : v;
-          }
-        }
   }
-  __syncthreads();
+
+  template <class F>
+  __device__ __forceinline__ void for_each(F f) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp % WM, wn = warp / WM;
+    const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          f(wm * MT * 8 + mt * 8 + fr, wn * NT * 8 + nt * 8 + 2 * fc + i,
+            make_double2(acc[mt][nt][0][i], acc[mt][nt][1][i]));
+  }
+};
+using Tile64 = Tile<2, 4, 4, 2, false>;
+using Tile64H = Tile<2, 4, 4, 2, true>;
+template <int NB>
+struct XTileSel;
+template <>
+struct XTileSel<32> { using T = Tile<4, 2, 2, 2, false>; };
+template <>
+struct XTileSel<16> { using T = Tile<4, 2, 2, 1, false>; };
+template <>
+struct XTileSel<8> { using T = Tile<8, 1, 1, 1, false>; };
+
+__device__ __forceinline__ const double2* child_block(const SolveParams& P, const ElimDesc& d, int e, bool left,
+                                                      bool sigma) {
+  const int a = left ? d.left_arena : d.right_arena;
+  if (a < 0) return nullptr;
+  const int sz = left ? d.p : d.n - d.p;
+  const double2* base = P.arena[a] + (int64_t)e * P.arena_elems[a] + (left ? d.left_off : d.right_off);
+  return sigma ? base + (int64_t)sz * sz : base;
 }
 
-__device__ void block_argmax(double& v, int& vi, double* cv, int* ci) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = 16; o; o >>= 1) {
-    double ov = __shfl_xor_sync(0xffffffffu, v, o);
-    int oi = __shfl_xor_sync(0xffffffffu, vi, o);
-    if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
+// ---- merged A / pivot-permuted Sigma into scratch (solver.py:97-132, 203-205, 227-228)
+template <bool SIGMA>
+__global__ void __launch_bounds__(kThreads) gather_kernel(SolveParams P, const Task* tasks) {
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s;
+  const Scr S = scratch_of(P, d, e);
+  double2* dst = SIGMA ? S.MS : S.M;
+  const int32_t* map = P.i32 + d.map_off;
+  const int32_t* rowoff = P.i32 + d.sprow_off;
+  const double2* lb = child_block(P, d, e, true, SIGMA);
+  const double2* rb = child_block(P, d, e, false, SIGMA);
+  const double2* vals = SIGMA ? P.s_vals + (P.s_broadcast ? 0 : (int64_t)e * P.nnz) : P.a_vals + (int64_t)e * P.nnz;
+  const int r0 = t.a, nr = t.b;
+  for (int q = threadIdx.x; q < nr * n; q += kThreads) {
+    const int i = r0 + q / n, j = q % n;
+    const int mi = map[(SIGMA && i < s) ? S.SIG[i] : i];
+    const int mj = map[(SIGMA && j < s) ? S.SIG[j] : j];
+    dst[(int64_t)i * n + j] = block_entry(d, lb, rb, mi, mj);
   }
-  if (lane == 0) { cv[warp] = v; ci[warp] = vi; }
   __syncthreads();
-  v = cv[0]; vi = ci[0];
-  for (int w = 1; w < kThreads / 32; ++w) {
-    double ov = cv[w];
-    int oi = ci[w];
-    if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
+  const SparseEntry* sp = P.sparse + d.sparse_off;
+  for (int ri = 0; ri < nr; ++ri) {
+    const int i = r0 + ri;
+    const int mr = (SIGMA && i < s) ? S.SIG[i] : i;
+    for (int q = rowoff[mr] + threadIdx.x; q < rowoff[mr + 1]; q += kThreads) {
+      const SparseEntry en = sp[q];
+      const int j = (SIGMA && en.j < s) ? S.ISG[en.j] : en.j;
+      dst[(int64_t)i * n + j] = ldg2(vals + en.csr);
+    }
+  }
+  if (!SIGMA) {  // partial pivot scale max |A(S,S)| of these rows (kernels.py:241)
+    __shared__ double cv[kThreads / 32];
+    __shared__ int ci[kThreads / 32];
+    __syncthreads();
+    double mx = 0.0;
+    const int rs = min(nr, max(0, s - r0));
+    for (int q = threadIdx.x; q < rs * s; q += kThreads) mx = fmax(mx, cabs(dst[(int64_t)(r0 + q / s) * n + q % s]));
+    int dummy = 0;
+    block_argmax<kThreads>(mx, dummy, cv, ci);
+    if (threadIdx.x == 0) S.pmax[r0 / kRowChunk] = mx;
   }
 }
 
-// Triangular inverse of the jb x jb diagonal block T (shared, ld ldt) into
-// `out` (shared, ld ldo).  lower: unit lower L; else upper U.  One warp,
-// lane = column.
-__device__ void warp_tri_inverse(const double2* T, int ldt, int jb, bool lower, double2* out, int ldo, int lane) {
-  if (lane >= jb) return;
-  const int c = lane;
-  if (lower) {
-    for (int r = 0; r < jb; ++r) {
-      double2 x = cz();
-      if (r == c) x = make_double2(1.0, 0.0);
-      else if (r > c)
-        for (int m = c; m < r; ++m) x = cfms(x, T[r * ldt + m], out[m * ldo + c]);
-      out[r * ldo + c] = x;
+// ---- panel LU of the S rows [j0, s) x [j0, j1) with partial pivoting (kernels.py:237-252)
+// 128-thread CTAs (several per SM); rows live in registers (row r = tid + 128 k);
+// per column one pivot search + one broadcast barrier; the owner of the pivot
+// row publishes it with its reciprocal.  Also writes L_jj^-1 / U_jj^-1.
+template <int NB, int T>
+__global__ void __launch_bounds__(T) panel_kernel(SolveParams P, const Task* tasks) {
+  constexpr int RPT = 1;
+  __shared__ double cand_v[2][T / 32];
+  __shared__ int cand_i[2][T / 32];
+  __shared__ double2 prow[2][NB + 1], orow[2][NB];
+  __shared__ double2 tri[NB][NB + 1];
+  __shared__ int s_bad, s_nd;
+  __shared__ int lpiv[NB], dsrc[2 * NB], ddst[2 * NB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s;
+  const int j = t.a, j0 = j * NB, jb = min(NB, s - j0), j1 = j0 + jb, R = s - j0;
+  const Scr S = scratch_of(P, d, e, NB);
+  double2* M = S.M;
+  if (tid == 0) s_bad = INT32_MAX;
+  double2 row[RPT][NB];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int r = tid + k * T;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) row[k][c] = (r < R && c < jb) ? M[(int64_t)(j0 + r) * n + j0 + c] : cz();
+  }
+  double scale;
+  if (j == 0) {
+    scale = 0.0;
+    for (int q = tid; q < (s + kRowChunk - 1) / kRowChunk; q += T) scale = fmax(scale, S.pmax[q]);
+    int dummy = 0;
+    block_argmax<T>(scale, dummy, cand_v[1], cand_i[1]);
+    if (tid == 0) {
+      *S.scale = scale;
+      if (scale == 0.0) s_bad = 0;
     }
   } else {
-    for (int r = jb - 1; r > c; --r) out[r * ldo + c] = cz();
-    out[c * ldo + c] = cinv(T[c * ldt + c]);
-    for (int r = c - 1; r >= 0; --r) {
-      double2 acc = cz();
-      for (int m = r + 1; m <= c; ++m) acc = cfms(acc, T[r * ldt + m], out[m * ldo + c]);
-      out[r * ldo + c] = cmul(acc, cinv(T[r * ldt + r]));
-    }
+    scale = *reinterpret_cast<volatile double*>(S.scale);
   }
-}
-
-template <int NB>
-__host__ __device__ constexpr size_t cta_panel_smem(int max_s) {
-  return (size_t)max_s * (NB + 1) * sizeof(double2) + 2 * NB * NB * sizeof(double2);
-}
-constexpr size_t kGemmSmem = 2 * kTM * kSK * sizeof(double2);
-
-template <int NB>
-__global__ void __launch_bounds__(kThreads, 1) cta_elim_kernel(SolveParams P, int64_t count) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* smem = reinterpret_cast<double2*>(smem_raw);
-  __shared__ double cand_v[2][kThreads / 32];
-  __shared__ int cand_i[2][kThreads / 32];
-  __shared__ int s_bad;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t idx = blockIdx.x;
-  const int e = blockIdx.y;
-  const ElimDesc d = P.elims[idx];
-  const int64_t elim_global = P.elim_base + idx;
-  const int n = d.n, s = d.s, b = d.b;
-  double2* M = P.scratch + (int64_t)e * P.scratch_elems + d.ws_off;
-  double2* MS = M + (int64_t)n * n;
-  double2* LINV = MS + (int64_t)n * n;  // block j at j*NB*NB (ld NB); U^-1 of the current panel after them
-  const int nblk = (s + NB - 1) / NB;
-  double2* UINV = LINV + (int64_t)nblk * NB * NB;
-  int* PIV = reinterpret_cast<int*>(UINV + NB * NB);
-  int* SIG = PIV + n;
-  const int32_t* map = P.i32 + d.map_off;
-  const int32_t* rank = P.i32 + d.rank_off;
-  const double2* lblk = d.left_arena >= 0 ? P.arena[d.left_arena] + (int64_t)e * P.arena_elems[d.left_arena] + d.left_off : nullptr;
-  const double2* rblk = d.right_arena >= 0 ? P.arena[d.right_arena] + (int64_t)e * P.arena_elems[d.right_arena] + d.right_off : nullptr;
-  const SparseEntry* sp = P.sparse + d.sparse_off;
-  const double2* av = P.a_vals + (int64_t)e * P.nnz;
-  if (tid == 0) s_bad = INT32_MAX;
-
-  // ---- gather A (solver.py:203-205) ----
-  for (int64_t q = tid; q < (int64_t)n * n; q += kThreads) {
-    const int i = (int)(q / n), j = (int)(q % n);
-    M[q] = block_entry(d, lblk, rblk, map[i], map[j]);
-  }
-  __syncthreads();
-  for (int t = tid; t < d.nsparse; t += kThreads) {
-    SparseEntry en = sp[t];
-    M[(int64_t)en.i * n + en.j] = ldg2(av + en.csr);
-  }
-  __syncthreads();
-  // pivot scale = max |A(S,S)| (kernels.py:241)
-  double scale = 0.0;
-  for (int64_t q = tid; q < (int64_t)s * s; q += kThreads) scale = fmax(scale, cabs(M[(q / s) * n + q % s]));
-  {
-    int dummy = 0;
-    block_argmax(scale, dummy, cand_v[0], cand_i[0]);
-  }
-  if (tid == 0 && s > 0 && scale == 0.0) s_bad = 0;
-  __syncthreads();
-
-  // ---- blocked right-looking partial LU; pivot search among S rows only ----
-  constexpr int PS = NB + 1;
-  for (int j0 = 0; j0 < s; j0 += NB) {
-    const int jb = min(NB, s - j0), j1 = j0 + jb, R = s - j0;
-    double2* panel = smem;                      // [R][PS]
-    double2* tinv = smem + (size_t)R * PS;      // [2][NB*NB]: L^-1, U^-1 of the diagonal block
-    for (int q = tid; q < R * jb; q += kThreads) {
-      const int r = q / jb, c = q % jb;
-      panel[r * PS + c] = M[(int64_t)(j0 + r) * n + j0 + c];
-    }
-    __syncthreads();
-    for (int jj = 0; jj < jb; ++jj) {
-      double v = -1.0;
-      int vi = INT32_MAX;
-      for (int r = jj + tid; r < R; r += kThreads) {
-        const double a = cabs1(panel[r * PS + jj]);
+#pragma unroll
+  for (int jj = 0; jj < NB; ++jj) {
+    if (jj >= jb) break;
+    const int buf = jj & 1;
+    double v = -1.0;
+    int vi = INT32_MAX;
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int r = tid + k * T;
+      if (r >= jj && r < R) {
+        const double a = cabs1(row[k][jj]);
         if (a > v) { v = a; vi = r; }
       }
-      block_argmax(v, vi, cand_v[jj & 1], cand_i[jj & 1]);
-      const int pr = vi;
-      if (tid == 0) PIV[j0 + jj] = j0 + pr;
-      if (pr != jj && tid < jb) {
-        double2 t = panel[jj * PS + tid];
-        panel[jj * PS + tid] = panel[pr * PS + tid];
-        panel[pr * PS + tid] = t;
-      }
-      __syncthreads();
-      const double2 ukk = panel[jj * PS + jj];
-      if (tid == 0 && cabs(ukk) < P.rtol * scale) atomicMin(&s_bad, j0 + jj);
-      const double2 uinv = cinv(ukk);
-      for (int r = jj + 1 + tid; r < R; r += kThreads) {
-        double2* row = panel + r * PS;
-        const double2 l = cmul(row[jj], uinv);
-        row[jj] = l;
-        for (int c = jj + 1; c < jb; ++c) row[c] = cfms(row[c], l, panel[jj * PS + c]);
-      }
-      __syncthreads();
     }
-    // inverses of the diagonal block (warp 0: unit-lower L, warp 1: upper U)
-    if (warp == 0) warp_tri_inverse(panel, PS, jb, true, tinv, NB, lane);
-    if (warp == 1) warp_tri_inverse(panel, PS, jb, false, tinv + NB * NB, NB, lane);
-    for (int q = tid; q < R * jb; q += kThreads) {
-      const int r = q / jb, c = q % jb;
-      M[(int64_t)(j0 + r) * n + j0 + c] = panel[r * PS + c];
-    }
-    // row interchanges of this panel on the other columns of the S rows
-    for (int c = tid; c < n; c += kThreads) {
-      if (c >= j0 && c < j1) continue;
-      for (int jj = 0; jj < jb; ++jj) {
-        const int pr = PIV[j0 + jj];
-        if (pr != j0 + jj) {
-          double2* pa = M + (int64_t)(j0 + jj) * n + c;
-          double2* pb = M + (int64_t)pr * n + c;
-          const double2 t = *pa;
-          *pa = *pb;
-          *pb = t;
-        }
+    block_argmax<T>(v, vi, cand_v[buf], cand_i[buf]);
+    const int pr = vi;
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int r = tid + k * T;
+      if (r == pr) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) prow[buf][c] = row[k][c];
+        prow[buf][NB] = cinv(row[k][jj]);
+      }
+      if (r == jj) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) orow[buf][c] = row[k][c];
       }
     }
+    if (tid == 0) { lpiv[jj] = pr; S.PIV[j0 + jj] = j0 + pr; }
     __syncthreads();
-    double2* linv = LINV + (int64_t)(j0 / NB) * NB * NB;
-    for (int q = tid; q < NB * NB; q += kThreads) {
-      linv[q] = tinv[q];
-      UINV[q] = tinv[NB * NB + q];
-    }
-    __syncthreads();
-    // U12 = L_jj^-1 A(j0:j1, j1:n)         (in place)
-    cta_gemm<false, false>(M + (int64_t)j0 * n + j1, n, linv, NB, M + (int64_t)j0 * n + j1, n, jb, n - j1, jb, smem);
-    // L21 (B rows) = A(s:n, j0:j1) U_jj^-1 (in place; S rows below came out of the panel)
-    cta_gemm<false, false>(M + (int64_t)s * n + j0, n, M + (int64_t)s * n + j0, n, UINV, NB, b, jb, jb, smem);
-    // trailing update over all remaining rows/cols (S and B)
-    cta_gemm<false, true>(M + (int64_t)j1 * n + j1, n, M + (int64_t)j1 * n + j0, n, M + (int64_t)j0 * n + j1, n,
-                          n - j1, n - j1, jb, smem);
-  }
-  if (tid == 0 && s_bad != INT32_MAX) report_bad(P, elim_global, e, s_bad);
-
-  // ---- X = Y L11^-1, block columns right to left ----
-  for (int j = nblk - 1; j >= 0; --j) {
-    const int j0 = j * NB, jb = min(NB, s - j0), j1 = j0 + jb;
-    if (j1 < s)
-      cta_gemm<false, true>(M + (int64_t)s * n + j0, n, M + (int64_t)s * n + j1, n, M + (int64_t)j1 * n + j0, n, b,
-                            jb, s - j1, smem);
-    cta_gemm<false, false>(M + (int64_t)s * n + j0, n, M + (int64_t)s * n + j0, n, LINV + (int64_t)j * NB * NB, NB,
-                           b, jb, jb, smem);
-  }
-
-  // ---- store U sorted (solver.py:234-243) ----
-  if (d.kind != kFinal && d.out_arena >= 0) {
-    double2* out = P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off;
-    for (int64_t q = tid; q < (int64_t)b * b; q += kThreads) {
-      const int i = (int)(q / b), j = (int)(q % b);
-      out[(int64_t)rank[i] * b + rank[j]] = M[(int64_t)(s + i) * n + s + j];
+    const double2 uinv = prow[buf][NB];
+    if (tid == 0 && cabs(prow[buf][jj]) < P.rtol * scale) atomicMin(&s_bad, j0 + jj);
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int r = tid + k * T;
+      if (r == jj) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) row[k][c] = prow[buf][c];
+      } else if (r == pr) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) row[k][c] = orow[buf][c];
+      }
+      if (r > jj && r < R) {
+        const double2 l = cmul(row[k][jj], uinv);
+        row[k][jj] = l;
+#pragma unroll
+        for (int c = jj + 1; c < NB; ++c) row[k][c] = cfms(row[k][c], l, prow[buf][c]);
+      }
     }
   }
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int r = tid + k * T;
+    if (r < R) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c < jb) M[(int64_t)(j0 + r) * n + j0 + c] = row[k][c];
+    }
+    if (r < jb) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) tri[r][c] = row[k][c];
+    }
+  }
+  // net row permutation of this panel's interchanges (rows that moved: <= 2 NB)
   if (tid == 0) {
-    for (int k = 0; k < s; ++k) SIG[k] = k;
-    for (int k = 0; k < s; ++k) {
-      const int pk = PIV[k];
-      const int t = SIG[k];
-      SIG[k] = SIG[pk];
-      SIG[pk] = t;
+    int key[2 * NB], val[2 * NB], cnt = 0;
+    for (int jj = 0; jj < jb; ++jj) {
+      if (lpiv[jj] == jj) continue;
+      int ia = -1, ib = -1;
+      for (int k = 0; k < cnt; ++k) {
+        if (key[k] == jj) ia = k;
+        if (key[k] == lpiv[jj]) ib = k;
+      }
+      if (ia < 0) { key[cnt] = jj; val[cnt] = jj; ia = cnt++; }
+      if (ib < 0) { key[cnt] = lpiv[jj]; val[cnt] = lpiv[jj]; ib = cnt++; }
+      const int tmp = val[ia];
+      val[ia] = val[ib];
+      val[ib] = tmp;
+    }
+    int nd = 0;
+    for (int k = 0; k < cnt; ++k)
+      if (key[k] != val[k]) { ddst[nd] = key[k]; dsrc[nd] = val[k]; ++nd; }
+    s_nd = nd;
+  }
+  __syncthreads();
+  // publish the net permutation for the TRSM launch, which applies it to the
+  // columns outside the panel
+  {
+    const int nd = s_nd;
+    if (tid == 0) S.PERM[0] = nd;
+    for (int k = tid; k < nd; k += T) {
+      S.PERM[1 + k] = dsrc[k];
+      S.PERM[1 + 2 * NB + k] = ddst[k];
+    }
+  }
+  // L_jj^-1 (warp 0) and U_jj^-1 (warp 1), lane = column, right-looking in registers
+  if (warp < 2 && lane < jb) {
+    const int c = lane;
+    double2 x[NB];
+    double2* out = (warp == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
+    if (warp == 0) {
+#pragma unroll
+      for (int r = 0; r < NB; ++r) x[r] = (r == c) ? make_double2(1.0, 0.0) : cz();
+#pragma unroll
+      for (int m = 0; m < NB; ++m)
+        if (m >= c && m < jb)
+#pragma unroll
+          for (int r = m + 1; r < NB; ++r)
+            if (r < jb) x[r] = cfms(x[r], tri[r][m], x[m]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < NB; ++r) x[r] = (r == c) ? make_double2(1.0, 0.0) : cz();
+#pragma unroll
+      for (int m = NB - 1; m >= 0; --m)
+        if (m < jb && m <= c) {
+          x[m] = cmul(x[m], cinv(tri[m][m]));
+#pragma unroll
+          for (int r = 0; r < NB; ++r)
+            if (r < m) x[r] = cfms(x[r], tri[r][m], x[m]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < NB; ++r) out[r * NB + c] = (r < jb) ? x[r] : cz();
+  }
+  if (warp < 2 && lane >= jb && lane < NB) {  // zero padding columns of the inverse blocks
+    double2* out = (warp == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
+    for (int r = 0; r < NB; ++r) out[r * NB + lane] = cz();
+  }
+  if (tid == 0 && s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
+}
+
+// ---- same panel step with the S-row panel in shared memory (R > 256 rows):
+// 256 threads, row per thread in a strided loop, 2 barriers per column.
+template <int NB>
+__global__ void __launch_bounds__(kThreads) panel_smem_kernel(SolveParams P, const Task* tasks) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* panel = reinterpret_cast<double2*>(smem_raw);  // [R][NB+1]
+  constexpr int PS = NB + 1;
+  __shared__ double cand_v[2][kThreads / 32];
+  __shared__ int cand_i[2][kThreads / 32];
+  __shared__ double2 s_uinv;
+  __shared__ int s_bad, s_nd;
+  __shared__ int lpiv[NB], dsrc[2 * NB], ddst[2 * NB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s;
+  const int j = t.a, j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
+  const Scr S = scratch_of(P, d, e, NB);
+  double2* M = S.M;
+  if (tid == 0) s_bad = INT32_MAX;
+  for (int q = tid; q < R * jb; q += kThreads) {
+    const int r = q / jb, c = q % jb;
+    panel[r * PS + c] = M[(int64_t)(j0 + r) * n + j0 + c];
+  }
+  double scale;
+  if (j == 0) {
+    scale = 0.0;
+    for (int q = tid; q < (s + kRowChunk - 1) / kRowChunk; q += kThreads) scale = fmax(scale, S.pmax[q]);
+    int dummy = 0;
+    block_argmax<kThreads>(scale, dummy, cand_v[1], cand_i[1]);
+    if (tid == 0) {
+      *S.scale = scale;
+      if (scale == 0.0) s_bad = 0;
+    }
+  } else {
+    scale = *reinterpret_cast<volatile double*>(S.scale);
+  }
+  __syncthreads();
+  for (int jj = 0; jj < jb; ++jj) {
+    double v = -1.0;
+    int vi = INT32_MAX;
+    for (int r = tid; r < R; r += kThreads) {  // fixed row ownership: r = tid (mod 256)
+      if (r < jj) continue;
+      const double a = cabs1(panel[r * PS + jj]);
+      if (a > v) { v = a; vi = r; }
+    }
+    block_argmax<kThreads>(v, vi, cand_v[jj & 1], cand_i[jj & 1]);
+    const int pr = vi;
+    if (tid == 0) {
+      lpiv[jj] = pr;
+      S.PIV[j0 + jj] = j0 + pr;
+      s_uinv = cinv(panel[pr * PS + jj]);
+      if (cabs(panel[pr * PS + jj]) < P.rtol * scale) atomicMin(&s_bad, j0 + jj);
+    }
+    if (pr != jj && tid < jb) {
+      const double2 tmp = panel[jj * PS + tid];
+      panel[jj * PS + tid] = panel[pr * PS + tid];
+      panel[pr * PS + tid] = tmp;
+    }
+    __syncthreads();
+    const double2 uinv = s_uinv;
+    for (int r = tid; r < R; r += kThreads) {
+      if (r <= jj) continue;
+      double2* rw = panel + r * PS;
+      const double2 l = cmul(rw[jj], uinv);
+      rw[jj] = l;
+#pragma unroll
+      for (int c = 1; c < NB; ++c)
+        if (c > jj && c < jb) rw[c] = cfms(rw[c], l, panel[jj * PS + c]);
     }
   }
   __syncthreads();
-  if (P.dbg_l && idx == 0 && e == 0)
-    for (int64_t q = tid; q < (int64_t)b * s; q += kThreads)
-      P.dbg_l[(q / s) * s + SIG[q % s]] = M[(int64_t)(s + q / s) * n + q % s];
-  if (P.compute_gless) {
-    int* ISG = SIG + s;  // merged position -> pivoted position (S part)
-    for (int k = tid; k < s; k += kThreads) ISG[SIG[k]] = k;
-    __syncthreads();
-    const double2* lr = lblk ? lblk + (int64_t)d.p * d.p : nullptr;
-    const int q = n - d.p;
-    const double2* rr = rblk ? rblk + (int64_t)q * q : nullptr;
-    const double2* sv = P.s_vals + (P.s_broadcast ? 0 : (int64_t)e * P.nnz);
-    for (int64_t t = tid; t < (int64_t)n * n; t += kThreads) {
-      const int i = (int)(t / n), j = (int)(t % n);
-      MS[t] = block_entry(d, lr, rr, map[i < s ? SIG[i] : i], map[j < s ? SIG[j] : j]);
+  for (int q = tid; q < R * jb; q += kThreads) {
+    const int r = q / jb, c = q % jb;
+    M[(int64_t)(j0 + r) * n + j0 + c] = panel[r * PS + c];
+  }
+  if (tid == 0) {
+    int key[2 * NB], val[2 * NB], cnt = 0;
+    for (int jj = 0; jj < jb; ++jj) {
+      if (lpiv[jj] == jj) continue;
+      int ia = -1, ib = -1;
+      for (int k = 0; k < cnt; ++k) {
+        if (key[k] == jj) ia = k;
+        if (key[k] == lpiv[jj]) ib = k;
+      }
+      if (ia < 0) { key[cnt] = jj; val[cnt] = jj; ia = cnt++; }
+      if (ib < 0) { key[cnt] = lpiv[jj]; val[cnt] = lpiv[jj]; ib = cnt++; }
+      const int tmp = val[ia];
+      val[ia] = val[ib];
+      val[ib] = tmp;
     }
-    __syncthreads();
-    for (int t = tid; t < d.nsparse; t += kThreads) {
-      SparseEntry en = sp[t];
-      const int i = en.i < s ? ISG[en.i] : en.i, j = en.j < s ? ISG[en.j] : en.j;
-      MS[(int64_t)i * n + j] = ldg2(sv + en.csr);
+    int nd = 0;
+    for (int k = 0; k < cnt; ++k)
+      if (key[k] != val[k]) { ddst[nd] = key[k]; dsrc[nd] = val[k]; ++nd; }
+    s_nd = nd;
+  }
+  __syncthreads();
+  {
+    const int nd = s_nd;
+    if (tid == 0) S.PERM[0] = nd;
+    for (int k = tid; k < nd; k += kThreads) {
+      S.PERM[1 + k] = dsrc[k];
+      S.PERM[1 + 2 * NB + k] = ddst[k];
     }
-    __syncthreads();
-    // T = MS[s:, :] - X MS[:s, :]
-    cta_gemm<false, true>(MS + (int64_t)s * n, n, M + (int64_t)s * n, n, MS, n, b, n, s, smem);
-    // R = T[:, s:] - T[:, :s] X^H
-    cta_gemm<true, true>(MS + (int64_t)s * n + s, n, MS + (int64_t)s * n, n, M + (int64_t)s * n, n, b, b, s, smem);
-    if (d.kind != kFinal && d.out_arena >= 0) {
-      double2* out = P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off + (int64_t)b * b;
-      for (int64_t t = tid; t < (int64_t)b * b; t += kThreads) {
-        const int i = (int)(t / b), j = (int)(t % b);
-        out[(int64_t)rank[i] * b + rank[j]] = MS[(int64_t)(s + i) * n + s + j];
+  }
+  if (warp < 2 && lane < NB) {
+    const int c = lane;
+    double2 x[NB];
+    double2* out = (warp == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
+#pragma unroll
+    for (int r = 0; r < NB; ++r) x[r] = (r == c) ? make_double2(1.0, 0.0) : cz();
+    if (c < jb) {
+      if (warp == 0) {
+#pragma unroll
+        for (int m = 0; m < NB; ++m)
+          if (m >= c && m < jb)
+#pragma unroll
+            for (int r = m + 1; r < NB; ++r)
+              if (r < jb) x[r] = cfms(x[r], panel[r * PS + m], x[m]);
+      } else {
+#pragma unroll
+        for (int m = NB - 1; m >= 0; --m)
+          if (m < jb && m <= c) {
+            x[m] = cmul(x[m], cinv(panel[m * PS + m]));
+#pragma unroll
+            for (int r = 0; r < NB; ++r)
+              if (r < m) x[r] = cfms(x[r], panel[r * PS + m], x[m]);
+          }
       }
     }
+#pragma unroll
+    for (int r = 0; r < NB; ++r) out[r * NB + c] = (r < jb && c < jb) ? x[r] : cz();
   }
-  if (d.kind == kFinal) {
-    // U_f, R_f (c x c) to shared memory, then the warp epilogue
-    const int c = b;
-    double2* uf = smem;
-    double2* rf = smem + c * c;
-    for (int t = tid; t < c * c; t += kThreads) {
-      uf[t] = M[(int64_t)(s + t / c) * n + s + t % c];
-      rf[t] = P.compute_gless ? MS[(int64_t)(s + t / c) * n + s + t % c] : cz();
+  if (tid == 0 && s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
+}
+
+// ---- U12 = L_jj^-1 A12 (type 0, 64-column tiles) and L21 = A21 U_jj^-1 (type 1, 64-row tiles), DMMA
+template <int NB>
+struct TrsmTiles;
+template <>
+struct TrsmTiles<32> { using U = Tile<4, 2, 1, 4, false>; using L = Tile<4, 2, 2, 2, false>; };
+template <>
+struct TrsmTiles<16> { using U = Tile<2, 4, 1, 2, false>; using L = Tile<4, 2, 2, 1, false>; };
+template <>
+struct TrsmTiles<8> { using U = Tile<1, 8, 1, 1, false>; using L = Tile<8, 1, 1, 1, false>; };
+
+template <int NB>
+__global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Task* tasks, int j) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s;
+  const int j0 = j * NB, jb = min(NB, s - j0);
+  const Scr S = scratch_of(P, d, e, NB);
+  double2* M = S.M;
+  if (t.a != 1) {
+    // this panel's row interchanges on columns [c0, c0+64) (solver-side zgetrf laswp):
+    // all moved rows are read before any is written
+    const int c0 = t.b, cn = min(kTile, (t.a == 2 ? j0 : n) - c0);
+    const int nd = S.PERM[0];
+    double2* st = smem;  // [2 NB][64]
+    for (int q = threadIdx.x; q < nd * kTile; q += kThreads) {
+      const int k = q / kTile, c = q % kTile;
+      if (c < cn) st[q] = M[(int64_t)(j0 + S.PERM[1 + k]) * n + c0 + c];
     }
     __syncthreads();
-    if (warp == 0) final_epilogue_warp(P, d, elim_global, e, uf, c, rf, c, lane);
+    for (int q = threadIdx.x; q < nd * kTile; q += kThreads) {
+      const int k = q / kTile, c = q % kTile;
+      if (c < cn) M[(int64_t)(j0 + S.PERM[1 + 2 * NB + k]) * n + c0 + c] = st[q];
+    }
+    __syncthreads();
+    if (t.a == 2) return;
   }
+  if (t.a == 0) {
+    using TT = typename TrsmTiles<NB>::U;
+    const int c0 = t.b;
+    double2* B = M + (int64_t)j0 * n + c0;
+    TT T;
+    T.zero();
+    T.mma(S.LINV + (int64_t)j * NB * NB, NB, B, n, jb, min(kTile, n - c0), jb, smem);
+    T.for_each([&](int r, int c, double2 v) {
+      if (r < jb && c0 + c < n) B[(int64_t)r * n + c] = v;
+    });
+  } else {
+    using TT = typename TrsmTiles<NB>::L;
+    const int r0 = s + t.b;
+    double2* A = M + (int64_t)r0 * n + j0;
+    TT T;
+    T.zero();
+    T.mma(A, n, S.UINV + (int64_t)j * NB * NB, NB, min(kTile, n - r0), jb, jb, smem);
+    T.for_each([&](int r, int c, double2 v) {
+      if (r0 + r < n && c < jb) A[(int64_t)r * n + c] = v;
+    });
+  }
+}
+
+// ---- trailing update M[j1:, j1:] -= M[j1:, j0:j1] M[j0:j1, j1:]
+__global__ void __launch_bounds__(kThreads, 2) trail_kernel(SolveParams P, const Task* tasks, int j, int nb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s;
+  const int j0 = j * nb, jb = min(nb, s - j0), j1 = j0 + jb;
+  double2* M = scratch_of(P, d, e).M;
+  const int r0 = j1 + t.a * kTile, c0 = j1 + t.b * kTile;
+  Tile64 T;
+  T.zero();
+  T.mma(M + (int64_t)r0 * n + j0, n, M + (int64_t)j0 * n + c0, n, min(kTile, n - r0), min(kTile, n - c0), jb, smem);
+  T.for_each([&](int r, int c, double2 v) {
+    if (r0 + r < n && c0 + c < n) {
+      double2* p = M + (int64_t)(r0 + r) * n + c0 + c;
+      *p = csub(*p, v);
+    }
+  });
+}
+
+// ---- X_j = (Y_j - X_{>j} L11[>j, j]) L_jj^-1 for 64 B rows
+template <int NB>
+__global__ void __launch_bounds__(kThreads) xsolve_kernel(SolveParams P, const Task* tasks, int j) {
+  using TT = typename XTileSel<NB>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  double2* Z = smem + 2 * TT::STAGE;    // [64][NB+1]
+  double2* D = Z + kTile * (NB + 1);     // [NB][NB+1]
+  const int tid = threadIdx.x;
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s;
+  const int j0 = j * NB, jb = min(NB, s - j0), j1 = j0 + jb;
+  double2* M = scratch_of(P, d, e).M;
+  const int r0 = s + t.a * kTile, nr = min(kTile, n - r0);
+  TT T;
+  T.zero();
+  if (s > j1) T.mma(M + (int64_t)r0 * n + j1, n, M + (int64_t)j1 * n + j0, n, nr, jb, s - j1, smem);
+  for (int q = tid; q < kTile * jb; q += kThreads) {
+    const int r = q / jb, c = q % jb;
+    Z[r * (NB + 1) + c] = r < nr ? M[(int64_t)(r0 + r) * n + j0 + c] : cz();
+  }
+  for (int q = tid; q < jb * jb; q += kThreads) D[(q / jb) * (NB + 1) + q % jb] = M[(int64_t)(j0 + q / jb) * n + j0 + q % jb];
+  __syncthreads();
+  T.for_each([&](int r, int c, double2 v) {
+    if (c < jb) Z[r * (NB + 1) + c] = csub(Z[r * (NB + 1) + c], v);
+  });
+  __syncthreads();
+  if (tid < nr) {
+    double2* z = Z + tid * (NB + 1);
+    for (int m = jb - 1; m > 0; --m) {
+      const double2 xm = z[m];
+      for (int c = 0; c < m; ++c) z[c] = cfms(z[c], xm, D[m * (NB + 1) + c]);
+    }
+  }
+  __syncthreads();
+  for (int q = tid; q < nr * jb; q += kThreads) {
+    const int r = q / jb, c = q % jb;
+    M[(int64_t)(r0 + r) * n + j0 + c] = Z[r * (NB + 1) + c];
+  }
+}
+
+// ---- pivot permutation (sigma), optional L (unit-test shim), store U sorted (solver.py:234-243)
+__global__ void __launch_bounds__(kThreads) finish_kernel(SolveParams P, const Task* tasks) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int* sig = reinterpret_cast<int*>(smem_raw);
+  const int tid = threadIdx.x;
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, b = d.b;
+  const Scr S = scratch_of(P, d, e);
+  for (int k = tid; k < s; k += kThreads) sig[k] = k;
+  __syncthreads();
+  if (tid == 0)
+    for (int k = 0; k < s; ++k) {
+      const int pk = S.PIV[k];
+      const int tmp = sig[k];
+      sig[k] = sig[pk];
+      sig[pk] = tmp;
+    }
+  __syncthreads();
+  for (int k = tid; k < s; k += kThreads) {
+    S.SIG[k] = sig[k];
+    S.ISG[sig[k]] = k;
+  }
+  if (P.dbg_l && t.e == 0 && e == 0)
+    for (int64_t q = tid; q < (int64_t)b * s; q += kThreads)
+      P.dbg_l[(q / s) * s + sig[q % s]] = S.M[(int64_t)(s + q / s) * n + q % s];
+  if (d.kind != kFinal && d.out_arena >= 0) {
+    double2* out = P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off;
+    const int32_t* rank = P.i32 + d.rank_off;
+    for (int64_t q = tid; q < (int64_t)b * b; q += kThreads) {
+      const int i = (int)(q / b), jj = (int)(q % b);
+      out[(int64_t)rank[i] * b + rank[jj]] = S.M[(int64_t)(s + i) * n + s + jj];
+    }
+  }
+}
+
+// ---- T = MS[s:, :] - X MS[:s, :]
+__global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const Task* tasks) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, b = d.b;
+  const Scr S = scratch_of(P, d, e);
+  const int i0 = t.a * kTile, c0 = t.b * kTile;
+  Tile64 T;
+  T.zero();
+  T.mma(S.M + (int64_t)(s + i0) * n, n, S.MS + c0, n, min(kTile, b - i0), min(kTile, n - c0), s, smem);
+  T.for_each([&](int r, int c, double2 v) {
+    if (i0 + r < b && c0 + c < n) {
+      double2* p = S.MS + (int64_t)(s + i0 + r) * n + c0 + c;
+      *p = csub(*p, v);
+    }
+  });
+}
+
+// ---- R = T[:, s:] - T[:, :s] X^H, stored sorted (or kept for the final step)
+__global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const Task* tasks) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, b = d.b;
+  const Scr S = scratch_of(P, d, e);
+  const int i0 = t.a * kTile, c0 = t.b * kTile;
+  Tile64H T;
+  T.zero();
+  T.mma(S.MS + (int64_t)(s + i0) * n, n, S.M + (int64_t)(s + c0) * n, n, min(kTile, b - i0), min(kTile, b - c0), s,
+        smem);
+  const bool store = d.kind != kFinal && d.out_arena >= 0;
+  double2* out = store ? P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off + (int64_t)b * b
+                       : nullptr;
+  const int32_t* rank = P.i32 + d.rank_off;
+  T.for_each([&](int r, int c, double2 v) {
+    const int i = i0 + r, jj = c0 + c;
+    if (i < b && jj < b) {
+      double2* p = S.MS + (int64_t)(s + i) * n + s + jj;
+      const double2 val = csub(*p, v);
+      if (store) out[(int64_t)rank[i] * b + rank[jj]] = val;
+      else *p = val;
+    }
+  });
+}
+
+// ---- final leaf step epilogue, warp per (leaf, energy)
+__global__ void __launch_bounds__(kSmallWarps * 32) final_kernel(SolveParams P, const Task* tasks, int64_t count,
+                                                                 int cmax) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t idx = (int64_t)blockIdx.x * kSmallWarps + warp;
+  if (idx >= count) return;
+  const Task t = tasks[idx];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, c = d.b;
+  const int ld = cmax + 1;
+  double2* uf = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * 2 * cmax * ld;
+  double2* rf = uf + cmax * ld;
+  const Scr S = scratch_of(P, d, e);
+  for (int q = lane; q < c * c; q += 32) {
+    uf[(q / c) * ld + q % c] = S.M[(int64_t)(s + q / c) * n + s + q % c];
+    rf[(q / c) * ld + q % c] = P.compute_gless ? S.MS[(int64_t)(s + q / c) * n + s + q % c] : cz();
+  }
+  __syncwarp();
+  final_epilogue_warp(P, d, t.e, e, uf, ld, rf, ld, lane);
 }
 
 // ================================================================== host side
-#define CUDA_TRY(x)                                                                        \
-  do {                                                                                     \
-    cudaError_t err__ = (x);                                                               \
-    if (err__ != cudaSuccess) {                                                            \
-      if (st) {                                                                            \
-        st->code = FIND_ECUDA;                                                             \
-        std::snprintf(st->message, sizeof(st->message), "%s: %s", #x, cudaGetErrorString(err__)); \
-      }                                                                                    \
-      return FIND_ECUDA;                                                                   \
-    }                                                                                      \
+#define CUDA_TRY(x)                                                                                   \
+  do {                                                                                                \
+    cudaError_t err__ = (x);                                                                          \
+    if (err__ != cudaSuccess) {                                                                       \
+      if (st) {                                                                                       \
+        st->code = FIND_ECUDA;                                                                        \
+        std::snprintf(st->message, sizeof(st->message), "%s: %s", #x, cudaGetErrorString(err__));    \
+      }                                                                                               \
+      return FIND_ECUDA;                                                                              \
+    }                                                                                                 \
   } while (0)
 
 void status_ok(find_status* st) {
@@ -712,18 +1171,140 @@ void status_ok(find_status* st) {
   std::snprintf(st->message, sizeof(st->message), "ok");
 }
 
-constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // dynamic budget (static smem of the kernels < 1 KB)
-
-int pick_nb(int max_s) {
-  if (cta_panel_smem<32>(max_s) <= kMaxSmem) return 32;
-  if (cta_panel_smem<16>(max_s) <= kMaxSmem) return 16;
-  if (cta_panel_smem<8>(max_s) <= kMaxSmem) return 8;
-  return 0;
+int fail_status(find_status* st, int code, const char* msg) {
+  if (st) {
+    st->code = code;
+    std::snprintf(st->message, sizeof(st->message), "%s", msg);
+  }
+  return code;
 }
 
+constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // dynamic budget (static smem of the kernels < 1 KB)
 size_t ws_header_bytes() { return 256; }
 
-int64_t group_launches(const find_plan* P) { return (int64_t)P->groups.size(); }
+template <int NB>
+size_t xsolve_smem() {
+  using TT = typename XTileSel<NB>::T;
+  return TT::SMEM + (size_t)(kTile * (NB + 1) + NB * (NB + 1)) * sizeof(double2);
+}
+
+template <int NB>
+size_t trsm_smem() {
+  return std::max(std::max(TrsmTiles<NB>::U::SMEM, TrsmTiles<NB>::L::SMEM), (size_t)2 * NB * kTile * sizeof(double2));
+}
+
+int set_attrs(find_status* st) {
+  static bool done = false;
+  if (done) return FIND_OK;
+  const int mx = (int)kMaxSmem;
+  CUDA_TRY(cudaFuncSetAttribute(small_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<32>()));
+  CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<16>()));
+  CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<8>()));
+  CUDA_TRY(cudaFuncSetAttribute(trail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(tgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(rgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64H::SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<32>()));
+  CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<16>()));
+  CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<8>()));
+  CUDA_TRY(cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  done = true;
+  return FIND_OK;
+}
+
+// Enqueue the launches of groups [g_begin, g_end).
+int run_groups(const find_plan* P, const SolveParams& prm, int64_t g_begin, int64_t g_end, int nE,
+               cudaStream_t stream, find_status* st) {
+  int rc = set_attrs(st);
+  if (rc) return rc;
+  const Task* dtasks = (const Task*)P->d_tasks;
+  for (int64_t gi = g_begin; gi < g_end; ++gi) {
+    const LaunchGroup& G = P->groups[gi];
+    if (G.path == 1 && G.nb == 0) return fail_status(st, FIND_EINVAL, "elimination block too large for this build");
+    for (int64_t si = G.spec_begin; si < G.spec_end; ++si) {
+      const LaunchSpec& L = P->specs[si];
+      if (!prm.compute_gless && (L.kind == kLGatherS || L.kind == kLTGemm)) continue;
+      const Task* tk = dtasks + L.task_off;
+      const unsigned cnt = (unsigned)L.task_count;
+      const dim3 grid(cnt, (unsigned)nE);
+      switch (L.kind) {
+        case kLSmall: {
+          SolveParams p = prm;
+          p.elims = prm.elims + L.task_off;
+          p.elim_base = L.task_off;
+          const int nmax = std::max(1, G.max_n), ld = nmax + 1;
+          const int xcap = G.max_b * G.max_s + G.max_b * G.max_b;
+          const size_t smem = (size_t)kSmallWarps * small_warp_elems(nmax, ld, xcap) * sizeof(double2);
+          small_elim_kernel<<<dim3((unsigned)((L.task_count + kSmallWarps - 1) / kSmallWarps), (unsigned)nE),
+                              kSmallWarps * 32, smem, stream>>>(p, L.task_count, nmax, ld, xcap);
+          break;
+        }
+        case kLGatherA: gather_kernel<false><<<grid, kThreads, 0, stream>>>(prm, tk); break;
+        case kLGatherS: gather_kernel<true><<<grid, kThreads, 0, stream>>>(prm, tk); break;
+        case kLPanel: {
+          const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
+          if (L.nb == 32 && rmax <= 64) panel_kernel<32, 64><<<grid, 64, 0, stream>>>(prm, tk);
+          else if (L.nb == 32 && rmax <= 128) panel_kernel<32, 128><<<grid, 128, 0, stream>>>(prm, tk);
+          else if (L.nb == 32) panel_kernel<32, 256><<<grid, 256, 0, stream>>>(prm, tk);
+          else if (L.nb == 16)
+            panel_smem_kernel<16><<<grid, kThreads, (size_t)G.max_s * 17 * sizeof(double2), stream>>>(prm, tk);
+          else panel_smem_kernel<8><<<grid, kThreads, (size_t)G.max_s * 9 * sizeof(double2), stream>>>(prm, tk);
+          break;
+        }
+        case kLTrsm:
+          if (L.nb == 32) trsm_kernel<32><<<grid, kThreads, trsm_smem<32>(), stream>>>(prm, tk, L.step);
+          else if (L.nb == 16) trsm_kernel<16><<<grid, kThreads, trsm_smem<16>(), stream>>>(prm, tk, L.step);
+          else trsm_kernel<8><<<grid, kThreads, trsm_smem<8>(), stream>>>(prm, tk, L.step);
+          break;
+        case kLTrail: trail_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk, L.step, L.nb); break;
+        case kLXSolve:
+          if (L.nb == 32) xsolve_kernel<32><<<grid, kThreads, xsolve_smem<32>(), stream>>>(prm, tk, L.step);
+          else if (L.nb == 16) xsolve_kernel<16><<<grid, kThreads, xsolve_smem<16>(), stream>>>(prm, tk, L.step);
+          else xsolve_kernel<8><<<grid, kThreads, xsolve_smem<8>(), stream>>>(prm, tk, L.step);
+          break;
+        case kLFinish:
+          finish_kernel<<<grid, kThreads, std::max<size_t>((size_t)G.max_s * sizeof(int), 16), stream>>>(prm, tk);
+          break;
+        case kLTGemm: tgemm_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk); break;
+        case kLRGemm: rgemm_kernel<<<grid, kThreads, Tile64H::SMEM, stream>>>(prm, tk); break;
+        case kLFinal: {
+          const int cmax = std::max(1, G.max_b);
+          const size_t smem = (size_t)kSmallWarps * 2 * cmax * (cmax + 1) * sizeof(double2);
+          final_kernel<<<dim3((cnt + kSmallWarps - 1) / kSmallWarps, (unsigned)nE), kSmallWarps * 32, smem, stream>>>(
+              prm, tk, L.task_count, cmax);
+          break;
+        }
+        default: return fail_status(st, FIND_EINVAL, "unknown launch kind");
+      }
+      CUDA_TRY(cudaGetLastError());
+    }
+  }
+  return FIND_OK;
+}
+
+SolveParams make_params(const find_plan* P, void* ws, int nE) {
+  SolveParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  unsigned char* base = (unsigned char*)ws;
+  prm.elims = (const ElimDesc*)P->d_elims;
+  prm.i32 = (const int32_t*)P->d_i32;
+  prm.sparse = (const SparseEntry*)P->d_sparse;
+  prm.nnz = P->nnz;
+  prm.status = (unsigned long long*)base;
+  size_t off = ws_header_bytes();
+  for (int a = 0; a < 3; ++a) {
+    prm.arena[a] = (double2*)(base + off);
+    prm.arena_elems[a] = P->arena_elems[a];
+    off += (size_t)nE * P->arena_elems[a] * sizeof(double2);
+  }
+  prm.scratch = (double2*)(base + off);
+  prm.scratch_elems = P->ws_elems;
+  prm.n_nodes = P->n;
+  return prm;
+}
 
 }  // namespace
 
@@ -734,7 +1315,8 @@ void find_plan_free_device(find_plan* P) {
   if (P->d_elims) cudaFree(P->d_elims);
   if (P->d_i32) cudaFree(P->d_i32);
   if (P->d_sparse) cudaFree(P->d_sparse);
-  P->d_elims = P->d_i32 = P->d_sparse = nullptr;
+  if (P->d_tasks) cudaFree(P->d_tasks);
+  P->d_elims = P->d_i32 = P->d_sparse = P->d_tasks = nullptr;
   P->device = -1;
 }
 
@@ -754,6 +1336,7 @@ int find_plan_upload(find_plan* P, find_status* st) {
   CUDA_TRY(up(&P->d_elims, P->elims.data(), P->elims.size() * sizeof(ElimDesc)));
   CUDA_TRY(up(&P->d_i32, P->i32.data(), P->i32.size() * sizeof(int32_t)));
   CUDA_TRY(up(&P->d_sparse, P->sparse.data(), P->sparse.size() * sizeof(SparseEntry)));
+  CUDA_TRY(up(&P->d_tasks, P->tasks.data(), P->tasks.size() * sizeof(Task)));
   P->device = dev;
   return FIND_OK;
 }
@@ -767,88 +1350,31 @@ size_t find_solve_workspace_bytes(const find_plan* P, int32_t nE, int32_t comput
   return b;
 }
 
-int64_t find_solve_launch_count(const find_plan* P) { return P ? group_launches(P) : 0; }
+int64_t find_solve_launch_count(const find_plan* P) { return P ? (int64_t)P->specs.size() : 0; }
 
 int find_solve_groups(find_plan* P, const void* a_vals, const void* s_vals, int32_t s_broadcast, int32_t nE,
                       int32_t compute_gless, double rtol, void* gr_out, void* gl_out, void* ws, size_t ws_bytes,
                       int64_t g_begin, int64_t g_end, void* stream_, find_status* st) {
   status_ok(st);
-  auto fail = [&](int code, const char* msg) {
-    if (st) { st->code = code; std::snprintf(st->message, sizeof(st->message), "%s", msg); }
-    return code;
-  };
-  if (!P || !a_vals || !gr_out || !ws || nE < 1) return fail(FIND_EINVAL, "invalid argument");
-  if (compute_gless && (!s_vals || !gl_out)) return fail(FIND_EINVAL, "compute_gless needs s_vals and gl_out");
-  if (nE > 0xffff) return fail(FIND_EINVAL, "too many energy points in one call");
-  if (ws_bytes < find_solve_workspace_bytes(P, nE, compute_gless)) return fail(FIND_ENOMEM, "workspace too small");
+  if (!P || !a_vals || !gr_out || !ws || nE < 1) return fail_status(st, FIND_EINVAL, "invalid argument");
+  if (compute_gless && (!s_vals || !gl_out)) return fail_status(st, FIND_EINVAL, "compute_gless needs s_vals and gl_out");
+  if (nE > 0xffff) return fail_status(st, FIND_EINVAL, "too many energy points in one call");
+  if (ws_bytes < find_solve_workspace_bytes(P, nE, compute_gless)) return fail_status(st, FIND_ENOMEM, "workspace too small");
   int rc = find_plan_upload(P, st);
   if (rc) return rc;
   cudaStream_t stream = (cudaStream_t)stream_;
-  unsigned char* base = (unsigned char*)ws;
-  SolveParams prm;
-  std::memset(&prm, 0, sizeof(prm));
-  prm.elims = (const ElimDesc*)P->d_elims;
-  prm.i32 = (const int32_t*)P->d_i32;
-  prm.sparse = (const SparseEntry*)P->d_sparse;
+  SolveParams prm = make_params(P, ws, nE);
   prm.a_vals = (const double2*)a_vals;
   prm.s_vals = (const double2*)s_vals;
-  prm.nnz = P->nnz;
   prm.s_broadcast = s_broadcast;
   prm.compute_gless = compute_gless;
   prm.rtol = rtol;
-  prm.status = (unsigned long long*)base;
-  size_t off = ws_header_bytes();
-  for (int a = 0; a < 3; ++a) {
-    prm.arena[a] = (double2*)(base + off);
-    prm.arena_elems[a] = P->arena_elems[a];
-    off += (size_t)nE * P->arena_elems[a] * sizeof(double2);
-  }
-  prm.scratch = (double2*)(base + off);
-  prm.scratch_elems = P->ws_elems;
   prm.gr_out = (double2*)gr_out;
   prm.gl_out = (double2*)gl_out;
-  prm.n_nodes = P->n;
   if (g_begin < 0) g_begin = 0;
   if (g_end < 0 || g_end > (int64_t)P->groups.size()) g_end = (int64_t)P->groups.size();
-  if (g_begin == 0) CUDA_TRY(cudaMemsetAsync(base, 0xff, 8, stream));
-  static bool attr_done = false;
-  if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(cta_elim_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
-    CUDA_TRY(cudaFuncSetAttribute(cta_elim_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
-    CUDA_TRY(cudaFuncSetAttribute(cta_elim_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
-    CUDA_TRY(cudaFuncSetAttribute(small_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
-    attr_done = true;
-  }
-  for (int64_t gi = g_begin; gi < g_end; ++gi) {
-    const LaunchGroup& G = P->groups[gi];
-    const int64_t count = G.end - G.begin;
-    SolveParams p = prm;
-    p.elims = prm.elims + G.begin;
-    p.elim_base = G.begin;
-    if (G.path == 0) {
-      const int nmax = std::max(1, G.max_n), ld = nmax + 1;
-      const size_t smem = (size_t)kSmallWarps * (2 * nmax * ld + 64) * sizeof(double2);
-      dim3 grid((unsigned)((count + kSmallWarps - 1) / kSmallWarps), (unsigned)nE);
-      small_elim_kernel<<<grid, kSmallWarps * 32, smem, stream>>>(p, count, nmax, ld);
-    } else {
-      const int nb = pick_nb(G.max_s);
-      if (nb == 0) return fail(FIND_EINVAL, "elimination block too large for the single-CTA path");
-      dim3 grid((unsigned)count, (unsigned)nE);
-      size_t smem = kGemmSmem;
-      if (nb == 32) {
-        smem = std::max(smem, cta_panel_smem<32>(G.max_s));
-        cta_elim_kernel<32><<<grid, kThreads, smem, stream>>>(p, count);
-      } else if (nb == 16) {
-        smem = std::max(smem, cta_panel_smem<16>(G.max_s));
-        cta_elim_kernel<16><<<grid, kThreads, smem, stream>>>(p, count);
-      } else {
-        smem = std::max(smem, cta_panel_smem<8>(G.max_s));
-        cta_elim_kernel<8><<<grid, kThreads, smem, stream>>>(p, count);
-      }
-    }
-    CUDA_TRY(cudaGetLastError());
-  }
-  return FIND_OK;
+  if (g_begin == 0) CUDA_TRY(cudaMemsetAsync(ws, 0xff, 8, stream));
+  return run_groups(P, prm, g_begin, g_end, nE, stream, st);
 }
 
 int find_solve(find_plan* P, const void* a_vals, const void* s_vals, int32_t s_broadcast, int32_t nE,
@@ -898,129 +1424,113 @@ int find_solve_status(find_plan* P, void* ws, int32_t nE, void* stream_, find_st
       } else {
         const int k = std::min(pos, std::max(d.s - 1, 0));
         st->node_id = d.s > 0 ? P->slabels[d.slabel_off + k] : -1;
-        std::snprintf(st->message, sizeof(st->message), "singular pivot at elimination position %d (cluster %lld, energy %d)",
-                      pos, (long long)d.label, e);
+        std::snprintf(st->message, sizeof(st->message),
+                      "singular pivot at elimination position %d (cluster %lld, energy %d)", pos, (long long)d.label, e);
       }
     }
   }
   return FIND_ESINGULAR;
 }
 
-}  // extern "C"
-
-extern "C" int find_schur_sigma_update(int32_t s, int32_t b, const void* ass, const void* asb, const void* abs_,
-                                       const void* abb, const void* sss, const void* ssb, const void* sbs,
-                                       const void* sbb, double rtol, void* u_out, void* r_out, void* l_out,
-                                       int32_t force_path, void* stream_, find_status* st) {
+int find_schur_sigma_update(int32_t s, int32_t b, const void* ass, const void* asb, const void* abs_, const void* abb,
+                            const void* sss, const void* ssb, const void* sbs, const void* sbb, double rtol,
+                            void* u_out, void* r_out, void* l_out, int32_t force_path, void* stream_,
+                            find_status* st) {
   status_ok(st);
-  if (s < 0 || b < 0 || s + b < 1 || (b > 0 && !u_out)) {
-    if (st) { st->code = FIND_EINVAL; std::snprintf(st->message, sizeof(st->message), "invalid sizes"); }
-    return FIND_EINVAL;
-  }
+  if (s < 0 || b < 0 || s + b < 1 || (b > 0 && !u_out)) return fail_status(st, FIND_EINVAL, "invalid sizes");
   cudaStream_t stream = (cudaStream_t)stream_;
   const int n = s + b;
   const bool gless = (r_out != nullptr || b == 0) && (s == 0 || sss) && (s == 0 || b == 0 || (ssb && sbs)) &&
                      (b == 0 || sbb);
   int path = force_path >= 0 ? force_path : (n <= 32 ? 0 : 1);
   if (path == 0 && n > 32) path = 1;
-  // one elimination: left block = [[ass, asb], [abs, abb]] (+ Sigma block), map = identity
+  // a one-elimination plan: left block = [[ass, asb], [abs, abb]] (+ Sigma), identity maps
+  find_plan Q;
+  Q.n = n;
+  Q.nnz = 0;
   ElimDesc d;
   std::memset(&d, 0, sizeof(d));
   d.s = s; d.b = b; d.n = n; d.p = n; d.kind = kUpMerge; d.label = 1;
   d.left_arena = kArenaUp; d.left_off = 0; d.right_arena = kArenaNone; d.right_off = -1;
   d.out_arena = kArenaDown0; d.out_off = 0;
-  d.map_off = 0; d.rank_off = n; d.sparse_off = 0; d.nsparse = 0; d.ws_off = 0;
-  std::vector<int32_t> i32(n + b);
-  for (int k = 0; k < n; ++k) i32[k] = k;
-  for (int k = 0; k < b; ++k) i32[n + k] = k;
-  const int64_t up_elems = 2 * (int64_t)n * n, out_elems = 2 * (int64_t)b * b;
-  const int64_t scr = 2 * (int64_t)n * n + ((s + 31) / 32) * 1024 + 1024 + (3 * n + 3) / 4 + 2;
-  void *d_desc = nullptr, *d_i32 = nullptr, *d_up = nullptr, *d_out = nullptr, *d_scr = nullptr, *d_stat = nullptr;
-  CUDA_TRY(cudaMalloc(&d_desc, sizeof(ElimDesc)));
-  CUDA_TRY(cudaMalloc(&d_i32, i32.size() * 4));
-  CUDA_TRY(cudaMalloc(&d_up, up_elems * 16));
-  CUDA_TRY(cudaMalloc(&d_out, (out_elems + 2) * 16));
-  CUDA_TRY(cudaMalloc(&d_scr, scr * 16));
-  CUDA_TRY(cudaMalloc(&d_stat, 16));
-  CUDA_TRY(cudaMemcpyAsync(d_desc, &d, sizeof(d), cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemcpyAsync(d_i32, i32.data(), i32.size() * 4, cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemsetAsync(d_up, 0, up_elems * 16, stream));
-  CUDA_TRY(cudaMemsetAsync(d_stat, 0xff, 8, stream));
-  double2* up = (double2*)d_up;
+  d.map_off = 0; d.rank_off = n; d.sprow_off = n + b; d.sparse_off = 0; d.nsparse = 0; d.ws_off = 0;
+  Q.i32.resize(n + b + n + 1, 0);
+  for (int k = 0; k < n; ++k) Q.i32[k] = k;
+  for (int k = 0; k < b; ++k) Q.i32[n + k] = k;
+  Q.elims.push_back(d);
+  Q.slabels.assign(std::max(s, 1), 0);
+  for (int k = 0; k < s; ++k) Q.slabels[k] = k;
+  LaunchGroup G;
+  std::memset(&G, 0, sizeof(G));
+  G.begin = 0; G.end = 1; G.path = path; G.max_n = n; G.max_s = s; G.max_b = b;
+  G.nb = path == 1 ? pick_nb_host(s) : 0;
+  if (path == 1 && G.nb == 0) return fail_status(st, FIND_EINVAL, "block too large");
+  G.ws_elems = path == 1 ? find_scratch_elems(n, s, G.nb) : 0;
+  Q.groups.push_back(G);
+  Q.arena_elems[kArenaUp] = 2 * (int64_t)n * n;
+  Q.arena_elems[kArenaDown0] = 2 * (int64_t)b * b + 2;
+  Q.arena_elems[kArenaDown1] = 0;
+  Q.ws_elems = G.ws_elems;
+  find_build_tasks(&Q);
+  int rc = find_plan_upload(&Q, st);
+  if (rc) { find_plan_free_device(&Q); return rc; }
+  const size_t wsb = find_solve_workspace_bytes(&Q, 1, 1);
+  void* ws = nullptr;
+  cudaError_t ce = cudaMalloc(&ws, wsb);
+  if (ce != cudaSuccess) { find_plan_free_device(&Q); return fail_status(st, FIND_ECUDA, cudaGetErrorString(ce)); }
+  SolveParams prm = make_params(&Q, ws, 1);
+  prm.compute_gless = gless;
+  prm.rtol = rtol;
+  prm.a_vals = prm.arena[kArenaUp];  // unused: no sparse entries
+  prm.s_vals = prm.arena[kArenaUp];
+  prm.s_broadcast = 1;
+  prm.dbg_l = (double2*)l_out;
+  double2* up = prm.arena[kArenaUp];
   auto put = [&](double2* dst, const void* src, int rows, int cols) -> cudaError_t {
     if (!rows || !cols) return cudaSuccess;
     return cudaMemcpy2DAsync(dst, (size_t)n * 16, src, (size_t)cols * 16, (size_t)cols * 16, rows,
                              cudaMemcpyDeviceToDevice, stream);
   };
-  CUDA_TRY(put(up, ass, s, s));
-  CUDA_TRY(put(up + s, asb, s, b));
-  CUDA_TRY(put(up + (int64_t)s * n, abs_, b, s));
-  CUDA_TRY(put(up + (int64_t)s * n + s, abb, b, b));
-  if (gless) {
-    double2* rs = up + (int64_t)n * n;
-    CUDA_TRY(put(rs, sss, s, s));
-    CUDA_TRY(put(rs + s, ssb, s, b));
-    CUDA_TRY(put(rs + (int64_t)s * n, sbs, b, s));
-    CUDA_TRY(put(rs + (int64_t)s * n + s, sbb, b, b));
-  }
-  SolveParams p;
-  std::memset(&p, 0, sizeof(p));
-  p.elims = (const ElimDesc*)d_desc;
-  p.i32 = (const int32_t*)d_i32;
-  p.sparse = nullptr;
-  p.a_vals = (const double2*)d_up;  // unused (no sparse entries)
-  p.s_vals = (const double2*)d_up;
-  p.compute_gless = gless;
-  p.rtol = rtol;
-  p.arena[kArenaUp] = up;
-  p.arena[kArenaDown0] = (double2*)d_out;
-  p.arena[kArenaDown1] = (double2*)d_out;
-  p.scratch = (double2*)d_scr;
-  p.scratch_elems = scr;
-  p.status = (unsigned long long*)d_stat;
-  p.dbg_l = (double2*)l_out;
-  if (path == 0) {
-    const int nmax = n, ld = n + 1;
-    const size_t smem = (size_t)kSmallWarps * (2 * nmax * ld + 64) * sizeof(double2);
-    CUDA_TRY(cudaFuncSetAttribute(small_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
-    small_elim_kernel<<<dim3(1, 1), kSmallWarps * 32, smem, stream>>>(p, 1, nmax, ld);
-  } else {
-    const int nb = pick_nb(s);
-    if (nb == 0) {
-      if (st) { st->code = FIND_EINVAL; std::snprintf(st->message, sizeof(st->message), "block too large"); }
-      return FIND_EINVAL;
+  int out = FIND_OK;
+  do {
+    if ((ce = cudaMemsetAsync(ws, 0, wsb, stream)) != cudaSuccess) break;
+    if ((ce = cudaMemsetAsync(ws, 0xff, 8, stream)) != cudaSuccess) break;
+    if ((ce = put(up, ass, s, s)) != cudaSuccess) break;
+    if ((ce = put(up + s, asb, s, b)) != cudaSuccess) break;
+    if ((ce = put(up + (int64_t)s * n, abs_, b, s)) != cudaSuccess) break;
+    if ((ce = put(up + (int64_t)s * n + s, abb, b, b)) != cudaSuccess) break;
+    if (gless) {
+      double2* rs = up + (int64_t)n * n;
+      if ((ce = put(rs, sss, s, s)) != cudaSuccess) break;
+      if ((ce = put(rs + s, ssb, s, b)) != cudaSuccess) break;
+      if ((ce = put(rs + (int64_t)s * n, sbs, b, s)) != cudaSuccess) break;
+      if ((ce = put(rs + (int64_t)s * n + s, sbb, b, b)) != cudaSuccess) break;
     }
-    size_t smem = kGemmSmem;
-    if (nb == 32) {
-      smem = std::max(smem, cta_panel_smem<32>(s));
-      CUDA_TRY(cudaFuncSetAttribute(cta_elim_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
-      cta_elim_kernel<32><<<dim3(1, 1), kThreads, smem, stream>>>(p, 1);
-    } else if (nb == 16) {
-      smem = std::max(smem, cta_panel_smem<16>(s));
-      CUDA_TRY(cudaFuncSetAttribute(cta_elim_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
-      cta_elim_kernel<16><<<dim3(1, 1), kThreads, smem, stream>>>(p, 1);
-    } else {
-      smem = std::max(smem, cta_panel_smem<8>(s));
-      CUDA_TRY(cudaFuncSetAttribute(cta_elim_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
-      cta_elim_kernel<8><<<dim3(1, 1), kThreads, smem, stream>>>(p, 1);
+    out = run_groups(&Q, prm, 0, 1, 1, stream, st);
+    if (out) break;
+    if (b && (ce = cudaMemcpyAsync(u_out, prm.arena[kArenaDown0], (size_t)b * b * 16, cudaMemcpyDeviceToDevice,
+                                   stream)) != cudaSuccess) break;
+    if (gless && b &&
+        (ce = cudaMemcpyAsync(r_out, prm.arena[kArenaDown0] + (int64_t)b * b, (size_t)b * b * 16,
+                              cudaMemcpyDeviceToDevice, stream)) != cudaSuccess) break;
+    unsigned long long key = ~0ull;
+    if ((ce = cudaMemcpyAsync(&key, ws, 8, cudaMemcpyDeviceToHost, stream)) != cudaSuccess) break;
+    if ((ce = cudaStreamSynchronize(stream)) != cudaSuccess) break;
+    if (key != ~0ull) {
+      if (st) {
+        st->code = FIND_ESINGULAR;
+        st->node_id = (int64_t)(key & 0xffff);
+        st->cluster_label = 0;
+        st->energy_idx = 0;
+        std::snprintf(st->message, sizeof(st->message), "singular pivot at elimination position %d", (int)(key & 0xffff));
+      }
+      out = FIND_ESINGULAR;
     }
-  }
-  CUDA_TRY(cudaGetLastError());
-  if (b) CUDA_TRY(cudaMemcpyAsync(u_out, d_out, (size_t)b * b * 16, cudaMemcpyDeviceToDevice, stream));
-  if (gless && b) CUDA_TRY(cudaMemcpyAsync(r_out, (double2*)d_out + (int64_t)b * b, (size_t)b * b * 16, cudaMemcpyDeviceToDevice, stream));
-  unsigned long long key = ~0ull;
-  CUDA_TRY(cudaMemcpyAsync(&key, d_stat, 8, cudaMemcpyDeviceToHost, stream));
-  CUDA_TRY(cudaStreamSynchronize(stream));
-  cudaFree(d_desc); cudaFree(d_i32); cudaFree(d_up); cudaFree(d_out); cudaFree(d_scr); cudaFree(d_stat);
-  if (key != ~0ull) {
-    if (st) {
-      st->code = FIND_ESINGULAR;
-      st->node_id = (int64_t)(key & 0xffff);
-      st->cluster_label = 0;
-      st->energy_idx = 0;
-      std::snprintf(st->message, sizeof(st->message), "singular pivot at elimination position %d", (int)(key & 0xffff));
-    }
-    return FIND_ESINGULAR;
-  }
-  return FIND_OK;
+  } while (0);
+  cudaFree(ws);
+  find_plan_free_device(&Q);
+  if (ce != cudaSuccess) return fail_status(st, FIND_ECUDA, cudaGetErrorString(ce));
+  return out;
 }
+
+}  // extern "C"

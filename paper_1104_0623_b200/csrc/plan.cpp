@@ -23,6 +23,9 @@
 
 using namespace findb200;
 
+int64_t find_scratch_elems(int64_t n, int64_t s, int nb);
+void find_build_tasks(find_plan* P);
+
 namespace {
 
 void set_status(find_status* st, int code, const char* msg) {
@@ -35,12 +38,118 @@ void set_status(find_status* st, int code, const char* msg) {
   std::snprintf(st->message, sizeof(st->message), "%s", msg);
 }
 
-// Scratch (complex elements) of one CTA-path elimination: M, MS, inverse
-// diagonal blocks (nb <= 32), pivots/permutation (int32, 4 per complex slot).
-int64_t scratch_elems(int64_t n, int64_t s) {
-  int64_t e = 2 * n * n + ((s + 31) / 32) * 1024 + 1024 + (3 * n + 3) / 4 + 2;
+}  // namespace
+
+// Scratch (complex elements) of one CTA-path elimination: M (n x n), MS
+// (n x n), pivots / permutation / inverse permutation (3 s int32), scale, and
+// the inverted diagonal blocks L_jj^-1, U_jj^-1 of every panel (nb x nb).
+// Must match scratch_of() in find_solve.cu.
+int64_t find_scratch_elems(int64_t n, int64_t s, int nb) {
+  int64_t e = 2 * n * n + (3 * s + 132 + 3) / 4 + 1 + (n + 31) / 32;
+  if (nb > 0) e += 2 * ((s + nb - 1) / nb) * (int64_t)nb * nb;
   return (e + 1) & ~int64_t(1);
 }
+
+// Flattened task lists of every phase launch (see LaunchKind).
+void find_build_tasks(find_plan* P) {
+  P->tasks.clear();
+  P->specs.clear();
+  auto spec = [&](int32_t kind, int32_t step, int32_t nb, int32_t g, int64_t off) {
+    LaunchSpec L;
+    L.kind = kind; L.step = step; L.nb = nb; L.group = g;
+    L.task_off = off;
+    L.task_count = (int64_t)P->tasks.size() - off;
+    if (L.task_count > 0 || kind == kLSmall) P->specs.push_back(L);
+  };
+  for (int32_t gi = 0; gi < (int32_t)P->groups.size(); ++gi) {
+    LaunchGroup& G = P->groups[gi];
+    G.spec_begin = (int64_t)P->specs.size();
+    if (G.path == 0) {
+      LaunchSpec L;
+      L.kind = kLSmall; L.step = 0; L.nb = 0; L.group = gi;
+      L.task_off = G.begin; L.task_count = G.end - G.begin;
+      P->specs.push_back(L);
+      G.spec_end = (int64_t)P->specs.size();
+      continue;
+    }
+    const int nb = G.nb;
+    auto push = [&](int32_t e, int32_t a, int32_t b, int32_t c) { P->tasks.push_back({e, a, b, c}); };
+    int64_t off = (int64_t)P->tasks.size();
+    for (int64_t e = G.begin; e < G.end; ++e) {
+      const ElimDesc& d = P->elims[e];
+      for (int r0 = 0; r0 < d.n; r0 += kRowChunk) push((int32_t)e, r0, std::min(kRowChunk, d.n - r0), 0);
+    }
+    spec(kLGatherA, 0, nb, gi, off);
+    const int steps = nb ? (G.max_s + nb - 1) / nb : 0;
+    for (int j = 0; j < steps; ++j) {
+      off = (int64_t)P->tasks.size();
+      for (int64_t e = G.begin; e < G.end; ++e)
+        if (P->elims[e].s > j * nb) push((int32_t)e, j, 0, 0);
+      spec(kLPanel, j, nb, gi, off);
+      off = (int64_t)P->tasks.size();
+      for (int64_t e = G.begin; e < G.end; ++e) {
+        const ElimDesc& d = P->elims[e];
+        if (d.s <= j * nb) continue;
+        const int j1 = std::min(d.s, (j + 1) * nb);
+        for (int c0 = j1; c0 < d.n; c0 += kTile) push((int32_t)e, 0, c0, 0);
+        for (int r0 = 0; r0 < d.b; r0 += kTile) push((int32_t)e, 1, r0, 0);
+        for (int c0 = 0; c0 < j * nb; c0 += kTile) push((int32_t)e, 2, c0, 0);  // interchanges on L columns
+      }
+      spec(kLTrsm, j, nb, gi, off);
+      off = (int64_t)P->tasks.size();
+      for (int64_t e = G.begin; e < G.end; ++e) {
+        const ElimDesc& d = P->elims[e];
+        if (d.s <= j * nb) continue;
+        const int j1 = std::min(d.s, (j + 1) * nb), m = d.n - j1;
+        const int t = (m + kTile - 1) / kTile;
+        for (int tm = 0; tm < t; ++tm)
+          for (int tn = 0; tn < t; ++tn) push((int32_t)e, tm, tn, 0);
+      }
+      spec(kLTrail, j, nb, gi, off);
+    }
+    for (int j = steps - 1; j >= 0; --j) {
+      off = (int64_t)P->tasks.size();
+      for (int64_t e = G.begin; e < G.end; ++e) {
+        const ElimDesc& d = P->elims[e];
+        if (d.s <= j * nb || d.b == 0) continue;
+        for (int tm = 0; tm < (d.b + kTile - 1) / kTile; ++tm) push((int32_t)e, tm, 0, 0);
+      }
+      spec(kLXSolve, j, nb, gi, off);
+    }
+    off = (int64_t)P->tasks.size();
+    for (int64_t e = G.begin; e < G.end; ++e) push((int32_t)e, 0, 0, 0);
+    spec(kLFinish, 0, nb, gi, off);
+    off = (int64_t)P->tasks.size();
+    for (int64_t e = G.begin; e < G.end; ++e) {
+      const ElimDesc& d = P->elims[e];
+      for (int r0 = 0; r0 < d.n; r0 += kRowChunk) push((int32_t)e, r0, std::min(kRowChunk, d.n - r0), 0);
+    }
+    spec(kLGatherS, 0, nb, gi, off);
+    off = (int64_t)P->tasks.size();
+    for (int64_t e = G.begin; e < G.end; ++e) {
+      const ElimDesc& d = P->elims[e];
+      if (d.s == 0 || d.b == 0) continue;
+      for (int tm = 0; tm < (d.b + kTile - 1) / kTile; ++tm)
+        for (int tn = 0; tn < (d.n + kTile - 1) / kTile; ++tn) push((int32_t)e, tm, tn, 0);
+    }
+    spec(kLTGemm, 0, nb, gi, off);
+    off = (int64_t)P->tasks.size();
+    for (int64_t e = G.begin; e < G.end; ++e) {
+      const ElimDesc& d = P->elims[e];
+      if (d.b == 0) continue;
+      for (int tm = 0; tm < (d.b + kTile - 1) / kTile; ++tm)
+        for (int tn = 0; tn < (d.b + kTile - 1) / kTile; ++tn) push((int32_t)e, tm, tn, 0);
+    }
+    spec(kLRGemm, 0, nb, gi, off);
+    off = (int64_t)P->tasks.size();
+    for (int64_t e = G.begin; e < G.end; ++e)
+      if (P->elims[e].kind == kFinal) push((int32_t)e, 0, 0, 0);
+    spec(kLFinal, 0, nb, gi, off);
+    G.spec_end = (int64_t)P->specs.size();
+  }
+}
+
+namespace {
 
 constexpr int32_t kSmallMaxN = 32;  // warp-per-elimination path up to this merged size
 
@@ -248,6 +357,14 @@ struct Builder {
       }
     }
     d.nsparse = (int32_t)((int64_t)P->sparse.size() - d.sparse_off);
+    d.sprow_off = (int64_t)P->i32.size();
+    {
+      int64_t t = d.sparse_off;
+      for (int32_t k = 0; k <= n; ++k) {
+        while (t < (int64_t)P->sparse.size() && P->sparse[t].i < k) ++t;
+        P->i32.push_back((int32_t)(t - d.sparse_off));
+      }
+    }
     if (kind == kUpMerge || kind == kDownMerge) {
       // structure exceptions (kernels.py:192-202): off-diagonal entries of the
       // S_l x S_r / S_r x S_l blocks and any entry of X, Y, Q, R.  All of them
@@ -309,10 +426,14 @@ struct Builder {
         G.max_n = G.max_s = G.max_b = 0;
         int64_t ws = 0;
         for (int64_t k = gb; k < ge; ++k) {
-          ElimDesc& d = P->elims[k];
+          const ElimDesc& d = P->elims[k];
           G.max_n = std::max(G.max_n, d.n); G.max_s = std::max(G.max_s, d.s); G.max_b = std::max(G.max_b, d.b);
+        }
+        G.nb = path == 1 ? pick_nb_host(G.max_s) : 0;
+        for (int64_t k = gb; k < ge; ++k) {
+          ElimDesc& d = P->elims[k];
           d.ws_off = ws;
-          if (path == 1) ws += scratch_elems(d.n, d.s);
+          if (path == 1) ws += find_scratch_elems(d.n, d.s, G.nb);
         }
         G.ws_elems = ws;
         P->ws_elems = std::max(P->ws_elems, ws);
@@ -433,6 +554,7 @@ int find_plan_create(int64_t nx, int64_t ny, const int64_t* indptr, const int64_
     B.build_tree();
     B.annotate();
     B.schedule();
+    find_build_tasks(P);
   } catch (const std::exception& e) {
     set_status(st, FIND_EINVAL, e.what());
     delete P;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -33,7 +34,48 @@ struct alignas(16) ElimDesc {
   int64_t sparse_off;        // sparse entries [sparse_off, sparse_off+nsparse)
   int64_t ws_off;            // complex-element offset of this elimination's scratch (per energy)
   int64_t slabel_off;        // int64 host-only array: S labels in merged order (error reporting)
+  int64_t sprow_off;         // int32[n+1]: per merged row, offsets of its sparse entries (relative)
 };
+
+// Phase launches of the CTA path (one launch = one kind over a task list).
+enum LaunchKind : int32_t {
+  kLSmall = 0,     // warp-per-elimination fused kernel (s+b <= 32)
+  kLGatherA = 1,   // merged A into scratch                    tasks {e, row0, nrows}
+  kLPanel = 2,     // panel LU with pivot search (step j)       tasks {e, j}
+  kLTrsm = 3,      // U12 = L_jj^-1 A12 / L21 = A21 U_jj^-1     tasks {e, type, start}
+  kLTrail = 4,     // trailing update (DMMA tiles)              tasks {e, tm, tn}
+  kLXSolve = 5,    // X = Y L11^-1, block column j              tasks {e, tm}
+  kLFinish = 6,    // pivot permutation + store U               tasks {e}
+  kLGatherS = 7,   // merged, pivot-permuted Sigma              tasks {e, row0, nrows}
+  kLTGemm = 8,     // T = S_B: - X S_S:                         tasks {e, tm, tn}
+  kLRGemm = 9,     // R = T_B - T_S X^H (+ store)               tasks {e, tm, tn}
+  kLFinal = 10,    // leaf inverse + G^< sandwich               tasks {e}
+};
+
+struct Task { int32_t e, a, b, c; };
+
+struct LaunchSpec {
+  int32_t kind, step, nb, group;
+  int64_t task_off, task_count;
+};
+
+// Panel width of a group: the S rows of a panel live in registers, ceil(max_s/256)
+// rows per thread, NB complex each (<= 128 doubles per thread).
+// (NB=32: register panel, one row per thread, up to 256 rows; NB=16/8: shared-memory panel)
+inline int pick_nb_host(int64_t max_s) {
+  if (const char* f = std::getenv("FIND_B200_NB")) {  // test hook: force the panel width
+    const int nb = std::atoi(f);
+    if ((nb == 32 && max_s <= 256) || (nb == 16 && max_s * 17 * 16 <= 220 * 1024) ||
+        (nb == 8 && max_s * 9 * 16 <= 220 * 1024))
+      return nb;
+  }
+  if (max_s <= 256) return 32;
+  if (max_s * 17 * 16 <= 220 * 1024) return 16;
+  if (max_s * 9 * 16 <= 220 * 1024) return 8;
+  return 0;
+}
+constexpr int kTile = 64;       // DMMA output tile edge
+constexpr int kRowChunk = 16;   // gather rows per CTA
 
 struct LaunchGroup {
   int64_t begin, end;  // ElimDesc range
@@ -42,6 +84,9 @@ struct LaunchGroup {
   int32_t level;
   int32_t max_n, max_s, max_b;
   int64_t ws_elems;    // scratch per energy used by this group
+  int32_t nb;          // panel width of the CTA path (0: unsupported size)
+  int32_t pad;
+  int64_t spec_begin, spec_end;  // launches of this group
 };
 
 struct SparseEntry {  // merged (row, col) <- csr value slot
@@ -73,6 +118,8 @@ struct find_plan {
   std::vector<int64_t> slabels;             // S labels (merged order) per elimination
   std::vector<findb200::SparseEntry> sparse;
   std::vector<int64_t> exc_slots[2];         // CSR slots of structure-exception entries (up, down)
+  std::vector<findb200::Task> tasks;
+  std::vector<findb200::LaunchSpec> specs;
   int64_t arena_elems[3] = {0, 0, 0};
   int64_t ws_elems = 0;
   int32_t max_n = 0, max_s = 0, max_b = 0, depth = 0, n_leaves = 0;
@@ -82,4 +129,5 @@ struct find_plan {
   void* d_elims = nullptr;
   void* d_i32 = nullptr;
   void* d_sparse = nullptr;
+  void* d_tasks = nullptr;
 };
