@@ -83,6 +83,7 @@ struct SolveParams {
   int64_t nnz;
   int32_t s_broadcast;
   int32_t compute_gless;
+  int32_t rsym;  // 0 general; +1 Sigma (hence every R) Hermitian; -1 skew-Hermitian
   double rtol;
   double2* arena[3];
   int64_t arena_elems[3];
@@ -1075,32 +1076,38 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SolveParams P, const T
   }
 }
 
-// ---- T = MS[s:, :] - X MS[:s, :]
+// ---- T = MS[s:, :] - X MS[:s, :]   (c = 0: S columns, c = 1/2: B columns)
 __global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const Task* tasks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw);
   const Task t = tasks[blockIdx.x];
+  if (t.c == 2 && P.rsym != 0) return;  // upper-triangle tile of a (skew-)Hermitian R
   const int e = blockIdx.y;
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s, b = d.b;
   const Scr S = scratch_of(P, d, e);
-  const int i0 = t.a * kTile, c0 = t.b * kTile;
+  const int i0 = t.a * kTile;
+  const int c0 = t.c == 0 ? t.b * kTile : s + t.b * kTile;
+  const int cend = t.c == 0 ? s : n;
   Tile64 T;
   T.zero();
-  T.mma(S.M + (int64_t)(s + i0) * n, n, S.MS + c0, n, min(kTile, b - i0), min(kTile, n - c0), s, smem);
+  T.mma(S.M + (int64_t)(s + i0) * n, n, S.MS + c0, n, min(kTile, b - i0), min(kTile, cend - c0), s, smem);
   T.for_each([&](int r, int c, double2 v) {
-    if (i0 + r < b && c0 + c < n) {
+    if (i0 + r < b && c0 + c < cend) {
       double2* p = S.MS + (int64_t)(s + i0 + r) * n + c0 + c;
       *p = csub(*p, v);
     }
   });
 }
 
-// ---- R = T[:, s:] - T[:, :s] X^H, stored sorted (or kept for the final step)
+// ---- R = T[:, s:] - T[:, :s] X^H, stored sorted (or kept for the final step).
+// Symmetric mode: lower-triangle tiles only, the upper triangle is written as
+// the (skew-)conjugate mirror (element (i, j) for i >= j only: deterministic).
 __global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const Task* tasks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw);
   const Task t = tasks[blockIdx.x];
+  if (t.c == 2 && P.rsym != 0) return;
   const int e = blockIdx.y;
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s, b = d.b;
@@ -1111,6 +1118,8 @@ __global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const
   T.mma(S.MS + (int64_t)(s + i0) * n, n, S.M + (int64_t)(s + c0) * n, n, min(kTile, b - i0), min(kTile, b - c0), s,
         smem);
   const bool store = d.kind != kFinal && d.out_arena >= 0;
+  const bool mirror = store && P.rsym != 0;
+  const double sg = P.rsym < 0 ? -1.0 : 1.0;
   double2* out = store ? P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off + (int64_t)b * b
                        : nullptr;
   const int32_t* rank = P.i32 + d.rank_off;
@@ -1119,8 +1128,14 @@ __global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const
     if (i < b && jj < b) {
       double2* p = S.MS + (int64_t)(s + i) * n + s + jj;
       const double2 val = csub(*p, v);
-      if (store) out[(int64_t)rank[i] * b + rank[jj]] = val;
-      else *p = val;
+      if (!store) {
+        *p = val;
+      } else if (!mirror) {
+        out[(int64_t)rank[i] * b + rank[jj]] = val;
+      } else if (i >= jj) {
+        out[(int64_t)rank[i] * b + rank[jj]] = val;
+        if (i != jj) out[(int64_t)rank[jj] * b + rank[i]] = make_double2(sg * val.x, -sg * val.y);
+      }
     }
   });
 }
@@ -1215,13 +1230,68 @@ int set_attrs(find_status* st) {
   return FIND_OK;
 }
 
-// Enqueue the launches of groups [g_begin, g_end).
+// Side streams for the concurrent groups of a phase (per device, created once).
+constexpr int kSideStreams = 4;
+struct SideStreams {
+  int device = -1;
+  cudaStream_t s[kSideStreams] = {};
+  cudaEvent_t fork[64] = {}, join[64] = {};
+  int next = 0;
+};
+SideStreams g_side;
+
+int side_init(find_status* st) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (g_side.device == dev) return FIND_OK;
+  for (int i = 0; i < kSideStreams; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&g_side.s[i], cudaStreamNonBlocking));
+  for (int i = 0; i < 64; ++i) {
+    CUDA_TRY(cudaEventCreateWithFlags(&g_side.fork[i], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&g_side.join[i], cudaEventDisableTiming));
+  }
+  g_side.device = dev;
+  return FIND_OK;
+}
+
+int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE, cudaStream_t stream,
+                  find_status* st);
+
+// Enqueue the launches of groups [g_begin, g_end): phase by phase; the groups
+// of a phase fork onto side streams and join back into `stream`.
 int run_groups(const find_plan* P, const SolveParams& prm, int64_t g_begin, int64_t g_end, int nE,
                cudaStream_t stream, find_status* st) {
   int rc = set_attrs(st);
   if (rc) return rc;
+  if ((rc = side_init(st))) return rc;
+  int64_t gi = g_begin;
+  while (gi < g_end) {
+    int64_t ge = gi;
+    while (ge < g_end && P->groups[ge].phase == P->groups[gi].phase) ++ge;
+    if (ge - gi == 1) {
+      if ((rc = run_one_group(P, prm, gi, nE, stream, st))) return rc;
+    } else {
+      const int slot = g_side.next;
+      g_side.next = (g_side.next + 1) % 64;
+      CUDA_TRY(cudaEventRecord(g_side.fork[slot], stream));
+      const int width = (int)std::min<int64_t>(ge - gi, kSideStreams);
+      for (int k = 0; k < width; ++k) CUDA_TRY(cudaStreamWaitEvent(g_side.s[k], g_side.fork[slot], 0));
+      for (int64_t g = gi; g < ge; ++g)
+        if ((rc = run_one_group(P, prm, g, nE, g_side.s[(g - gi) % kSideStreams], st))) return rc;
+      for (int k = 0; k < width; ++k) {
+        const int js = (slot + 1 + k) % 64;
+        CUDA_TRY(cudaEventRecord(g_side.join[js], g_side.s[k]));
+        CUDA_TRY(cudaStreamWaitEvent(stream, g_side.join[js], 0));
+      }
+    }
+    gi = ge;
+  }
+  return FIND_OK;
+}
+
+int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE, cudaStream_t stream,
+                  find_status* st) {
   const Task* dtasks = (const Task*)P->d_tasks;
-  for (int64_t gi = g_begin; gi < g_end; ++gi) {
+  {
     const LaunchGroup& G = P->groups[gi];
     if (G.path == 1 && G.nb == 0) return fail_status(st, FIND_EINVAL, "elimination block too large for this build");
     for (int64_t si = G.spec_begin; si < G.spec_end; ++si) {
@@ -1367,7 +1437,8 @@ int find_solve_groups(find_plan* P, const void* a_vals, const void* s_vals, int3
   prm.a_vals = (const double2*)a_vals;
   prm.s_vals = (const double2*)s_vals;
   prm.s_broadcast = s_broadcast;
-  prm.compute_gless = compute_gless;
+  prm.compute_gless = compute_gless ? 1 : 0;
+  prm.rsym = compute_gless == 2 ? 1 : (compute_gless == 3 ? -1 : 0);
   prm.rtol = rtol;
   prm.gr_out = (double2*)gr_out;
   prm.gl_out = (double2*)gl_out;

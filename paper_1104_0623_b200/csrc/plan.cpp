@@ -25,6 +25,7 @@ using namespace findb200;
 
 int64_t find_scratch_elems(int64_t n, int64_t s, int nb);
 void find_build_tasks(find_plan* P);
+void find_assign_phases(find_plan* P);
 
 namespace {
 
@@ -48,6 +49,32 @@ int64_t find_scratch_elems(int64_t n, int64_t s, int nb) {
   int64_t e = 2 * n * n + (3 * s + 132 + 3) / 4 + 1 + (n + 31) / 32;
   if (nb > 0) e += 2 * ((s + nb - 1) / nb) * (int64_t)nb * nb;
   return (e + 1) & ~int64_t(1);
+}
+
+// Phases: the groups of one upward level; or the downward merges of level L
+// together with the final leaf steps of level L-1 (both depend only on the
+// downward level L-1).  Groups of a phase run concurrently on side streams,
+// so each gets a disjoint scratch range (offsets are rebased here).
+void find_assign_phases(find_plan* P) {
+  int32_t phase = -1;
+  int32_t cur_key = INT32_MIN;
+  int64_t base = 0;
+  P->ws_elems = 0;
+  for (auto& G : P->groups) {
+    // key of the phase this group belongs to
+    int32_t key = G.pass == 0 ? -1000 - G.level : (G.pass == 1 ? G.level : G.level + 1);
+    if (key != cur_key) {
+      ++phase;
+      cur_key = key;
+      base = 0;
+    }
+    G.phase = phase;
+    if (G.path == 1) {
+      for (int64_t k = G.begin; k < G.end; ++k) P->elims[k].ws_off += base;
+      base += G.ws_elems;
+    }
+    P->ws_elems = std::max(P->ws_elems, base);
+  }
 }
 
 // Flattened task lists of every phase launch (see LaunchKind).
@@ -125,20 +152,27 @@ void find_build_tasks(find_plan* P) {
       for (int r0 = 0; r0 < d.n; r0 += kRowChunk) push((int32_t)e, r0, std::min(kRowChunk, d.n - r0), 0);
     }
     spec(kLGatherS, 0, nb, gi, off);
+    // T = S_B: - X S_S: : tiles over the S columns (c = 0) and the B columns
+    // (c = 1); with (skew-)Hermitian Sigma only the lower-triangle B tiles
+    // (c = 2 marks tiles the symmetric mode may skip: tn > tm, non-final)
     off = (int64_t)P->tasks.size();
     for (int64_t e = G.begin; e < G.end; ++e) {
       const ElimDesc& d = P->elims[e];
       if (d.s == 0 || d.b == 0) continue;
-      for (int tm = 0; tm < (d.b + kTile - 1) / kTile; ++tm)
-        for (int tn = 0; tn < (d.n + kTile - 1) / kTile; ++tn) push((int32_t)e, tm, tn, 0);
+      const int tb = (d.b + kTile - 1) / kTile;
+      for (int tm = 0; tm < tb; ++tm) {
+        for (int tn = 0; tn < (d.s + kTile - 1) / kTile; ++tn) push((int32_t)e, tm, tn, 0);
+        for (int tn = 0; tn < tb; ++tn) push((int32_t)e, tm, tn, (tn > tm && d.kind != kFinal) ? 2 : 1);
+      }
     }
     spec(kLTGemm, 0, nb, gi, off);
     off = (int64_t)P->tasks.size();
     for (int64_t e = G.begin; e < G.end; ++e) {
       const ElimDesc& d = P->elims[e];
       if (d.b == 0) continue;
-      for (int tm = 0; tm < (d.b + kTile - 1) / kTile; ++tm)
-        for (int tn = 0; tn < (d.b + kTile - 1) / kTile; ++tn) push((int32_t)e, tm, tn, 0);
+      const int tb = (d.b + kTile - 1) / kTile;
+      for (int tm = 0; tm < tb; ++tm)
+        for (int tn = 0; tn < tb; ++tn) push((int32_t)e, tm, tn, (tn > tm && d.kind != kFinal) ? 2 : 1);
     }
     spec(kLRGemm, 0, nb, gi, off);
     off = (int64_t)P->tasks.size();
@@ -411,25 +445,36 @@ struct Builder {
     const std::vector<int64_t> empty;
 
     auto emit_groups = [&](int64_t begin, int32_t pass, int32_t level) {
-      // sort the level's eliminations by merged size, split into paths
+      // sort the level's eliminations by size class; warp path for s+b <= 32,
+      // CTA path split by s so every launch gets a right-sized panel kernel
       int64_t end = (int64_t)P->elims.size();
       if (end == begin) return;
-      std::stable_sort(P->elims.begin() + begin, P->elims.end(),
-                       [](const ElimDesc& a, const ElimDesc& b) { return a.n < b.n; });
-      int64_t split = begin;
-      while (split < end && P->elims[split].n <= kSmallMaxN) ++split;
-      for (int path = 0; path < 2; ++path) {
-        int64_t gb = path == 0 ? begin : split, ge = path == 0 ? split : end;
-        if (gb == ge) continue;
+      auto cls = [](const ElimDesc& d) -> int {
+        if (d.n <= kSmallMaxN) return 0;
+        if (d.s <= 64) return 1;
+        if (d.s <= 128) return 2;
+        if (d.s <= 256) return 3;
+        return 4;
+      };
+      std::stable_sort(P->elims.begin() + begin, P->elims.end(), [&](const ElimDesc& a, const ElimDesc& b) {
+        const int ca = cls(a), cb = cls(b);
+        return ca != cb ? ca < cb : a.n < b.n;
+      });
+      int64_t gb = begin;
+      while (gb < end) {
+        const int c = cls(P->elims[gb]);
+        int64_t ge = gb;
+        while (ge < end && cls(P->elims[ge]) == c) ++ge;
+        const int path = c == 0 ? 0 : 1;
         LaunchGroup G;
+        std::memset(&G, 0, sizeof(G));
         G.begin = gb; G.end = ge; G.path = path; G.pass = pass; G.level = level;
-        G.max_n = G.max_s = G.max_b = 0;
-        int64_t ws = 0;
         for (int64_t k = gb; k < ge; ++k) {
           const ElimDesc& d = P->elims[k];
           G.max_n = std::max(G.max_n, d.n); G.max_s = std::max(G.max_s, d.s); G.max_b = std::max(G.max_b, d.b);
         }
         G.nb = path == 1 ? pick_nb_host(G.max_s) : 0;
+        int64_t ws = 0;
         for (int64_t k = gb; k < ge; ++k) {
           ElimDesc& d = P->elims[k];
           d.ws_off = ws;
@@ -441,6 +486,7 @@ struct Builder {
         P->max_n = std::max(P->max_n, G.max_n);
         P->max_s = std::max(P->max_s, G.max_s);
         P->max_b = std::max(P->max_b, G.max_b);
+        gb = ge;
       }
     };
 
@@ -554,6 +600,7 @@ int find_plan_create(int64_t nx, int64_t ny, const int64_t* indptr, const int64_
     B.build_tree();
     B.annotate();
     B.schedule();
+    find_assign_phases(P);
     find_build_tasks(P);
   } catch (const std::exception& e) {
     set_status(st, FIND_EINVAL, e.what());

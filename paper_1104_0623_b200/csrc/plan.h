@@ -85,7 +85,7 @@ struct LaunchGroup {
   int32_t max_n, max_s, max_b;
   int64_t ws_elems;    // scratch per energy used by this group
   int32_t nb;          // panel width of the CTA path (0: unsupported size)
-  int32_t pad;
+  int32_t phase;       // groups of one phase are independent and run concurrently
   int64_t spec_begin, spec_end;  // launches of this group
 };
 

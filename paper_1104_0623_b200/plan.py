@@ -140,8 +140,11 @@ class Plan:
             return self._ws
 
     def run(self, a_dev, s_dev, gr_dev, gl_dev, compute_gless=True, pivot_rtol=1e-12, s_broadcast=True, ws=None,
-            stream=None, groups=(0, -1), check=True):
-        """Enqueue the solve on `stream` for a_dev [nE, nnz] (torch complex128, CUDA)."""
+            stream=None, groups=(0, -1), check=True, sigma_sym=0):
+        """Enqueue the solve on `stream` for a_dev [nE, nnz] (torch complex128, CUDA).
+
+        sigma_sym: +1 if Sigma^< is exactly Hermitian, -1 if exactly skew-Hermitian
+        (then every R block is too and only its lower triangle is computed)."""
         import torch
 
         L = _native.lib()
@@ -155,7 +158,7 @@ class Plan:
         st = _native.FindStatus()
         rc = L.find_solve_groups(
             self._h, C.c_void_p(a_dev.data_ptr()), C.c_void_p(s_dev.data_ptr() if s_dev is not None else 0),
-            int(s_broadcast), n_e, int(compute_gless), float(pivot_rtol), C.c_void_p(gr_dev.data_ptr()),
+            int(s_broadcast), n_e, (0 if not compute_gless else {1: 2, -1: 3}.get(int(sigma_sym), 1)), float(pivot_rtol), C.c_void_p(gr_dev.data_ptr()),
             C.c_void_p(gl_dev.data_ptr() if gl_dev is not None else 0), C.c_void_p(ws.data_ptr()), ws.numel(),
             int(groups[0]), int(groups[1]), C.c_void_p(stream.cuda_stream), C.byref(st))
         if rc != _native.FIND_OK:

@@ -89,6 +89,17 @@ def sigma_on_pattern(a: sp.csr_matrix, sigma: sp.csr_matrix) -> np.ndarray:
     return out
 
 
+def sigma_symmetry(sigma_csr) -> int:
+    """+1 if exactly Hermitian, -1 if exactly skew-Hermitian, else 0."""
+    m = sigma_csr.tocsr()
+    h = m.conj().T.tocsr()
+    if (m - h).count_nonzero() == 0:
+        return 1
+    if (m + h).count_nonzero() == 0:
+        return -1
+    return 0
+
+
 def _validate(mesh, a, sigma, config):
     """solver.py:591-608."""
     if a.n != mesh.n:
@@ -122,7 +133,8 @@ def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, compute_gless=True, pivot_rtol=1e-12):
+def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, compute_gless=True, pivot_rtol=1e-12,
+                 sigma_sym=0):
     """Run the plan on host value arrays a_vals [nE, nnz], s_vals [nnz] or [nE, nnz].
 
     Host -> device copies, the level-batched kernels, status check and the
@@ -144,10 +156,11 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
     gl_d = torch.empty((n_e, plan.n), dtype=torch.complex128, device=dev) if compute_gless else None
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     ev[0].record(stream)
-    ws = plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, stream=stream, groups=(0, plan.first_down_group))
+    ws = plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, stream=stream,
+                  groups=(0, plan.first_down_group), sigma_sym=sigma_sym)
     ev[1].record(stream)
     plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, ws=ws, stream=stream,
-             groups=(plan.first_down_group, -1))
+             groups=(plan.first_down_group, -1), sigma_sym=sigma_sym)
     ev[2].record(stream)
     plan.check_status(ws, n_e, stream)
     gr = gr_d.cpu().numpy()
@@ -170,8 +183,9 @@ def solve(mesh, a, sigma, config: SolverConfig) -> SelectedInverse:
     plan, _ = plan_for(mesh.nx, mesh.ny, am.indptr, am.indices, config.leaf_max)
     s_vals = sigma_on_pattern(am, _csr_sorted(sigma.matrix)) if config.compute_gless else None
     sigma_herm = is_hermitian(sigma.matrix) if sigma is not None else False
+    ssym = sigma_symmetry(sigma.matrix) if config.compute_gless else 0
     t1 = time.perf_counter()
-    gr, gl, t_up, t_down = solve_values(plan, am.data[None, :], s_vals, config.compute_gless, config.pivot_rtol)
+    gr, gl, t_up, t_down = solve_values(plan, am.data[None, :], s_vals, config.compute_gless, config.pivot_rtol, ssym)
     t3 = time.perf_counter()
     ledger = plan.ledger(config.kernel, config.compute_gless, sigma_herm, config.sigma_mode)
     return SelectedInverse(
@@ -201,8 +215,9 @@ def solve_batch(mesh, a_list, sigma, config: SolverConfig) -> SelectedInverseBat
     plan, _ = plan_for(mesh.nx, mesh.ny, am0.indptr, am0.indices, config.leaf_max)
     s_vals = sigma_on_pattern(am0, _csr_sorted(sigma.matrix)) if config.compute_gless else None
     sigma_herm = is_hermitian(sigma.matrix) if sigma is not None else False
+    ssym = sigma_symmetry(sigma.matrix) if config.compute_gless else 0
     t1 = time.perf_counter()
-    gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol)
+    gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol, ssym)
     t3 = time.perf_counter()
     return SelectedInverseBatch(gr, gl, plan.ledger(config.kernel, config.compute_gless, sigma_herm, config.sigma_mode),
                                 {"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},

@@ -251,3 +251,20 @@ def test_cfg1_full_scale_properties(cuda):
             x = lu.solve(e)  # x = A^{-H} e_i  ->  G^r_ii = conj(x_i), G^<_ii = x^H Sigma x
             assert abs(gr[k, i] - np.conj(x[i])) < 1e-10 * np.max(np.abs(gr[k]))
             assert abs(gl[k, i] - np.vdot(x, sig @ x)) < 1e-10 * np.max(np.abs(gl[k]))
+
+
+def test_symmetric_r_mode_matches_general(cuda):
+    """Skew-Hermitian Sigma^< (i*Gamma): the lower-triangle R path equals the general path."""
+    from paper_1104_0623_b200.plan import plan_for
+    from paper_1104_0623_b200.solver import sigma_symmetry, solve_values
+
+    g = load_golden("c5_16x12")
+    p = problem_from_golden(g)
+    assert sigma_symmetry(p.sigma_csr()) == -1
+    plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
+    gr0, gl0, _, _ = solve_values(plan, p.a_vals_all(), p.s_vals, sigma_sym=0)
+    gr1, gl1, _, _ = solve_values(plan, p.a_vals_all(), p.s_vals, sigma_sym=-1)
+    assert np.array_equal(gr0, gr1)
+    assert rel(gl1, gl0) < 1e-13
+    for k in range(p.energies.size):
+        assert rel(gl1[k], g["gl"][k]) < TOL

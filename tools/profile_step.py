@@ -27,7 +27,7 @@ gr = torch.empty((p.energies.size, p.n), dtype=torch.complex128, device=dev)
 gl = torch.empty_like(gr)
 ws = plan.workspace(p.energies.size, True, dev)
 for _ in range(a.reps):
-    plan.run(ad, sd, gr, gl, ws=ws)
+    plan.run(ad, sd, gr, gl, ws=ws, sigma_sym=-1)
 plan.check_status(ws, p.energies.size)
 torch.cuda.synchronize()
 print("launches per solve", plan.launch_count())
