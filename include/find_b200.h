@@ -137,6 +137,12 @@ int find_solve_groups(find_plan* plan, const void* a_vals, const void* s_vals, i
 int find_plan_groups(const find_plan* plan, int32_t* pass, int32_t* level, int32_t* path, int64_t* count,
                      int32_t* max_n, int32_t* max_s, int32_t* max_b);
 
+/* Kernel-launch table in issue order (find_solve_launch_count() entries):
+ * launch kind (0 warp path, 1 gather A, 2 panel, 3 TRSM, 4 trailing, 5 X
+ * solve, 6 finish, 7 gather Sigma, 8 T, 9 R, 10 final), panel step, launch
+ * group, task count.  Any pointer may be NULL. */
+int find_plan_specs(const find_plan* plan, int32_t* kind, int32_t* step, int32_t* group, int64_t* tasks);
+
 /* Synchronise `stream` and decode the device status of the last find_solve
  * that used `ws`. */
 int find_solve_status(find_plan* plan, void* ws, int32_t n_energies, void* stream, find_status* st);

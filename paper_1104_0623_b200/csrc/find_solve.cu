@@ -601,17 +601,86 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(SolveParams P, const T
   }
 }
 
+// Inverses of the jb x jb diagonal block D (smem, ld NB+1) of a factored panel,
+// both at once with all T threads by recursive doubling:
+//   [A 0; C B]^-1 = [A^-1 0; -B^-1 C A^-1  B^-1]   (unit lower L)
+//   [A C; 0 B]^-1 = [A^-1 -A^-1 C B^-1; 0  B^-1]   (upper U)
+// Li, Ui, W: smem [NB][NB+1]; padding rows/cols >= jb act as identity.
+template <int NB, int T>
+__device__ void block_tri_inverses(double2 (*D)[NB + 1], int jb, double2 (*Li)[NB + 1], double2 (*Ui)[NB + 1],
+                                   double2 (*W)[NB + 1]) {
+  const int tid = threadIdx.x;
+  for (int q = tid; q < NB * NB; q += T) {
+    const int r = q / NB, c = q % NB;
+    Li[r][c] = r == c ? make_double2(1.0, 0.0) : cz();
+    Ui[r][c] = r == c ? (r < jb ? cinv(D[r][r]) : make_double2(1.0, 0.0)) : cz();
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int bs = 1; bs < NB; bs *= 2) {
+    // phase 1: W_L[i][j] = sum_q L[i][q] Li[q][j]  (i in B, q, j in A);  W_U[i][j] = sum_q Ui[i][q] U[q][j] (i, q in A, j in B)
+    for (int q = tid; q < (NB / 2) * bs; q += T) {
+      const int pair = q / (bs * bs), loc = q % (bs * bs);
+      const int k = pair * 2 * bs, a = loc / bs, b = loc % bs;
+      {  // lower: row i = k+bs+a (B), col j = k+b (A)
+        const int i = k + bs + a, jc = k + b;
+        double2 acc = cz();
+#pragma unroll 1
+        for (int qq = jc; qq < k + bs; ++qq)
+          if (i < jb && qq < jb) acc = cfma(acc, D[i][qq], Li[qq][jc]);
+        W[i][jc] = acc;
+      }
+      {  // upper: row i = k+a (A), col j = k+bs+b (B)
+        const int i = k + a, jc = k + bs + b;
+        double2 acc = cz();
+#pragma unroll 1
+        for (int qq = i; qq < k + bs; ++qq)
+          if (qq < jb && jc < jb) acc = cfma(acc, Ui[i][qq], D[qq][jc]);
+        W[i][jc] = acc;
+      }
+    }
+    __syncthreads();
+    // phase 2: Li[i][j] = -sum_p Li[i][p] W[p][j] (p in B, p <= i);  Ui[i][j] = -sum_p W[i][p] Ui[p][j] (p in B, p <= j)
+    for (int q = tid; q < (NB / 2) * bs; q += T) {
+      const int pair = q / (bs * bs), loc = q % (bs * bs);
+      const int k = pair * 2 * bs, a = loc / bs, b = loc % bs;
+      {
+        const int i = k + bs + a, jc = k + b;
+        double2 acc = cz();
+#pragma unroll 1
+        for (int p = k + bs; p <= i; ++p) acc = cfma(acc, Li[i][p], W[p][jc]);
+        Li[i][jc] = make_double2(-acc.x, -acc.y);
+      }
+      {
+        const int i = k + a, jc = k + bs + b;
+        double2 acc = cz();
+#pragma unroll 1
+        for (int p = k + bs; p <= jc; ++p) acc = cfma(acc, W[i][p], Ui[p][jc]);
+        Ui[i][jc] = make_double2(-acc.x, -acc.y);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---- panel LU of the S rows [j0, s) x [j0, j1) with partial pivoting (kernels.py:237-252)
-// 128-thread CTAs (several per SM); rows live in registers (row r = tid + 128 k);
-// per column one pivot search + one broadcast barrier; the owner of the pivot
-// row publishes it with its reciprocal.  Also writes L_jj^-1 / U_jj^-1.
+// Thread t keeps physical row t of the panel in registers for the whole panel;
+// a pivot interchange only swaps the *logical positions* of two threads (no
+// data moves).  The current pivot column is always register 0: the rank-1
+// update writes its result shifted left, so the column loop is a compact loop.
+// Finished multipliers stream to a staging row in MS (unused until the Sigma
+// phase); every row is written once, to its final position, at the end.
+// Per column: one block argmax (shuffles + 1 barrier) + one broadcast barrier.
 template <int NB, int T>
 __global__ void __launch_bounds__(T) panel_kernel(SolveParams P, const Task* tasks) {
-  constexpr int RPT = 1;
   __shared__ double cand_v[2][T / 32];
   __shared__ int cand_i[2][T / 32];
-  __shared__ double2 prow[2][NB + 1], orow[2][NB];
-  __shared__ double2 tri[NB][NB + 1];
+  __shared__ double2 prow[2][NB + 1];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2 (*tri)[NB + 1] = reinterpret_cast<double2 (*)[NB + 1]>(smem_raw);  // 4 x [NB][NB+1] (dynamic)
+  double2 (*tli)[NB + 1] = tri + NB;
+  double2 (*tui)[NB + 1] = tli + NB;
+  double2 (*tw)[NB + 1] = tui + NB;
   __shared__ int s_bad, s_nd;
   __shared__ int lpiv[NB], dsrc[2 * NB], ddst[2 * NB];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -619,17 +688,16 @@ __global__ void __launch_bounds__(T) panel_kernel(SolveParams P, const Task* tas
   const int e = blockIdx.y;
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s;
-  const int j = t.a, j0 = j * NB, jb = min(NB, s - j0), j1 = j0 + jb, R = s - j0;
+  const int j = t.a, j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
   const Scr S = scratch_of(P, d, e, NB);
   double2* M = S.M;
+  double2* Lst = S.MS + (int64_t)tid * NB;  // this thread's finished multipliers
   if (tid == 0) s_bad = INT32_MAX;
-  double2 row[RPT][NB];
+  const bool has = tid < R;
+  int pos = tid;  // logical position of this thread's row
+  double2 row[NB];
 #pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int r = tid + k * T;
-#pragma unroll
-    for (int c = 0; c < NB; ++c) row[k][c] = (r < R && c < jb) ? M[(int64_t)(j0 + r) * n + j0 + c] : cz();
-  }
+  for (int c = 0; c < NB; ++c) row[c] = (has && c < jb) ? M[(int64_t)(j0 + tid) * n + j0 + c] : cz();
   double scale;
   if (j == 0) {
     scale = 0.0;
@@ -643,69 +711,49 @@ __global__ void __launch_bounds__(T) panel_kernel(SolveParams P, const Task* tas
   } else {
     scale = *reinterpret_cast<volatile double*>(S.scale);
   }
-#pragma unroll
-  for (int jj = 0; jj < NB; ++jj) {
-    if (jj >= jb) break;
+#pragma unroll 1
+  for (int jj = 0; jj < jb; ++jj) {
     const int buf = jj & 1;
-    double v = -1.0;
-    int vi = INT32_MAX;
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-      const int r = tid + k * T;
-      if (r >= jj && r < R) {
-        const double a = cabs1(row[k][jj]);
-        if (a > v) { v = a; vi = r; }
-      }
-    }
+    double v = (has && pos >= jj) ? cabs1(row[0]) : -1.0;
+    int vi = (has && pos >= jj) ? pos : INT32_MAX;
     block_argmax<T>(v, vi, cand_v[buf], cand_i[buf]);
     const int pr = vi;
+    const bool winner = has && pos == pr;
+    if (winner) {
 #pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-      const int r = tid + k * T;
-      if (r == pr) {
+      for (int c = 0; c < NB; ++c) prow[buf][c] = row[c];
+      prow[buf][NB] = cinv(row[0]);
+      // final U row jj (columns jj..jb-1); its multipliers follow after the loop
+      double2* dst = M + (int64_t)(j0 + jj) * n + j0;
 #pragma unroll
-        for (int c = 0; c < NB; ++c) prow[buf][c] = row[k][c];
-        prow[buf][NB] = cinv(row[k][jj]);
-      }
-      if (r == jj) {
-#pragma unroll
-        for (int c = 0; c < NB; ++c) orow[buf][c] = row[k][c];
-      }
+      for (int c = 0; c < NB; ++c)
+        if (jj + c < jb) dst[jj + c] = row[c];
+      if (cabs(row[0]) < P.rtol * scale) atomicMin(&s_bad, j0 + jj);
     }
     if (tid == 0) { lpiv[jj] = pr; S.PIV[j0 + jj] = j0 + pr; }
     __syncthreads();
-    const double2 uinv = prow[buf][NB];
-    if (tid == 0 && cabs(prow[buf][jj]) < P.rtol * scale) atomicMin(&s_bad, j0 + jj);
+    if (winner) pos = jj;
+    else if (has && pos == jj) pos = pr;
+    if (has && pos > jj) {
+      const double2 uinv = prow[buf][NB];
+      const double2 l = cmul(row[0], uinv);
+      Lst[jj] = l;
 #pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-      const int r = tid + k * T;
-      if (r == jj) {
-#pragma unroll
-        for (int c = 0; c < NB; ++c) row[k][c] = prow[buf][c];
-      } else if (r == pr) {
-#pragma unroll
-        for (int c = 0; c < NB; ++c) row[k][c] = orow[buf][c];
-      }
-      if (r > jj && r < R) {
-        const double2 l = cmul(row[k][jj], uinv);
-        row[k][jj] = l;
-#pragma unroll
-        for (int c = jj + 1; c < NB; ++c) row[k][c] = cfms(row[k][c], l, prow[buf][c]);
-      }
+      for (int c = 1; c < NB; ++c) row[c - 1] = cfms(row[c], l, prow[buf][c]);
+      row[NB - 1] = cz();
     }
   }
+  // every row's multipliers (columns < min(pos, jb)) to its final position
+  if (has) {
+    double2* dst = M + (int64_t)(j0 + pos) * n + j0;
+    const int nl = min(pos, jb);
+    double2 buf[NB];
 #pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int r = tid + k * T;
-    if (r < R) {
+    for (int c = 0; c < NB; ++c)
+      if (c < nl) buf[c] = Lst[c];
 #pragma unroll
-      for (int c = 0; c < NB; ++c)
-        if (c < jb) M[(int64_t)(j0 + r) * n + j0 + c] = row[k][c];
-    }
-    if (r < jb) {
-#pragma unroll
-      for (int c = 0; c < NB; ++c) tri[r][c] = row[k][c];
-    }
+    for (int c = 0; c < NB; ++c)
+      if (c < nl) dst[c] = buf[c];
   }
   // net row permutation of this panel's interchanges (rows that moved: <= 2 NB)
   if (tid == 0) {
@@ -728,9 +776,7 @@ __global__ void __launch_bounds__(T) panel_kernel(SolveParams P, const Task* tas
       if (key[k] != val[k]) { ddst[nd] = key[k]; dsrc[nd] = val[k]; ++nd; }
     s_nd = nd;
   }
-  __syncthreads();
-  // publish the net permutation for the TRSM launch, which applies it to the
-  // columns outside the panel
+  __syncthreads();  // final panel rows are in M (global writes of this CTA are visible after the barrier)
   {
     const int nd = s_nd;
     if (tid == 0) S.PERM[0] = nd;
@@ -739,38 +785,21 @@ __global__ void __launch_bounds__(T) panel_kernel(SolveParams P, const Task* tas
       S.PERM[1 + 2 * NB + k] = ddst[k];
     }
   }
-  // L_jj^-1 (warp 0) and U_jj^-1 (warp 1), lane = column, right-looking in registers
-  if (warp < 2 && lane < jb) {
-    const int c = lane;
-    double2 x[NB];
-    double2* out = (warp == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
-    if (warp == 0) {
-#pragma unroll
-      for (int r = 0; r < NB; ++r) x[r] = (r == c) ? make_double2(1.0, 0.0) : cz();
-#pragma unroll
-      for (int m = 0; m < NB; ++m)
-        if (m >= c && m < jb)
-#pragma unroll
-          for (int r = m + 1; r < NB; ++r)
-            if (r < jb) x[r] = cfms(x[r], tri[r][m], x[m]);
-    } else {
-#pragma unroll
-      for (int r = 0; r < NB; ++r) x[r] = (r == c) ? make_double2(1.0, 0.0) : cz();
-#pragma unroll
-      for (int m = NB - 1; m >= 0; --m)
-        if (m < jb && m <= c) {
-          x[m] = cmul(x[m], cinv(tri[m][m]));
-#pragma unroll
-          for (int r = 0; r < NB; ++r)
-            if (r < m) x[r] = cfms(x[r], tri[r][m], x[m]);
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < NB; ++r) out[r * NB + c] = (r < jb) ? x[r] : cz();
+  for (int q = tid; q < NB * NB; q += T) {
+    const int r = q / NB, c = q % NB;
+    tri[r][c] = (r < jb && c < jb) ? M[(int64_t)(j0 + r) * n + j0 + c] : cz();
   }
-  if (warp < 2 && lane >= jb && lane < NB) {  // zero padding columns of the inverse blocks
-    double2* out = (warp == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
-    for (int r = 0; r < NB; ++r) out[r * NB + lane] = cz();
+  __syncthreads();
+  block_tri_inverses<NB, T>(tri, jb, tli, tui, tw);
+  {
+    double2* lo = S.LINV + (int64_t)j * NB * NB;
+    double2* uo = S.UINV + (int64_t)j * NB * NB;
+    for (int q = tid; q < NB * NB; q += T) {
+      const int r = q / NB, c = q % NB;
+      const bool in = r < jb && c < jb;
+      lo[q] = in ? tli[r][c] : cz();
+      uo[q] = in ? tui[r][c] : cz();
+    }
   }
   if (tid == 0 && s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
 }
@@ -1213,6 +1242,11 @@ int set_attrs(find_status* st) {
   if (done) return FIND_OK;
   const int mx = (int)kMaxSmem;
   CUDA_TRY(cudaFuncSetAttribute(small_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  const int psm = 4 * 32 * 33 * (int)sizeof(double2);
+  CUDA_TRY(cudaFuncSetAttribute(panel_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
+  CUDA_TRY(cudaFuncSetAttribute(panel_kernel<32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
+  CUDA_TRY(cudaFuncSetAttribute(panel_kernel<32, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<32>()));
@@ -1255,6 +1289,11 @@ int side_init(find_status* st) {
 
 int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE, cudaStream_t stream,
                   find_status* st);
+// register-resident panel rows (default) vs shared-memory panel (FIND_B200_SMEM_PANEL=1)
+const bool g_reg_panel = [] {
+  const char* f = std::getenv("FIND_B200_SMEM_PANEL");
+  return !(f && f[0] == '1');
+}();
 
 // Enqueue the launches of groups [g_begin, g_end): phase by phase; the groups
 // of a phase fork onto side streams and join back into `stream`.
@@ -1316,9 +1355,12 @@ int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE
         case kLGatherS: gather_kernel<true><<<grid, kThreads, 0, stream>>>(prm, tk); break;
         case kLPanel: {
           const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
-          if (L.nb == 32 && rmax <= 64) panel_kernel<32, 64><<<grid, 64, 0, stream>>>(prm, tk);
-          else if (L.nb == 32 && rmax <= 128) panel_kernel<32, 128><<<grid, 128, 0, stream>>>(prm, tk);
-          else if (L.nb == 32) panel_kernel<32, 256><<<grid, 256, 0, stream>>>(prm, tk);
+          constexpr size_t psm = 4 * 32 * 33 * sizeof(double2);
+          if (L.nb == 32 && g_reg_panel && rmax <= 64) panel_kernel<32, 64><<<grid, 64, psm, stream>>>(prm, tk);
+          else if (L.nb == 32 && g_reg_panel && rmax <= 128) panel_kernel<32, 128><<<grid, 128, psm, stream>>>(prm, tk);
+          else if (L.nb == 32 && g_reg_panel) panel_kernel<32, 256><<<grid, 256, psm, stream>>>(prm, tk);
+          else if (L.nb == 32)
+            panel_smem_kernel<32><<<grid, kThreads, (size_t)std::max(rmax, 1) * 33 * sizeof(double2), stream>>>(prm, tk);
           else if (L.nb == 16)
             panel_smem_kernel<16><<<grid, kThreads, (size_t)G.max_s * 17 * sizeof(double2), stream>>>(prm, tk);
           else panel_smem_kernel<8><<<grid, kThreads, (size_t)G.max_s * 9 * sizeof(double2), stream>>>(prm, tk);
@@ -1467,6 +1509,17 @@ int find_plan_groups(const find_plan* P, int32_t* pass, int32_t* level, int32_t*
     if (max_n) max_n[g] = G.max_n;
     if (max_s) max_s[g] = G.max_s;
     if (max_b) max_b[g] = G.max_b;
+  }
+  return FIND_OK;
+}
+
+int find_plan_specs(const find_plan* P, int32_t* kind, int32_t* step, int32_t* group, int64_t* tasks) {
+  if (!P) return FIND_EINVAL;
+  for (size_t i = 0; i < P->specs.size(); ++i) {
+    if (kind) kind[i] = P->specs[i].kind;
+    if (step) step[i] = P->specs[i].step;
+    if (group) group[i] = P->specs[i].group;
+    if (tasks) tasks[i] = P->specs[i].task_count;
   }
   return FIND_OK;
 }

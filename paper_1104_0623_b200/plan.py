@@ -128,6 +128,17 @@ class Plan:
     def launch_count(self) -> int:
         return int(_native.lib().find_solve_launch_count(self._h))
 
+    KIND_NAMES = ("warp", "gatherA", "panel", "trsm", "trail", "xsolve", "finish", "gatherS", "tgemm", "rgemm", "final")
+
+    def specs(self) -> dict:
+        """Kernel-launch table in issue order: kind, step, group, task count."""
+        k = self.launch_count()
+        out = {x: np.zeros(k, np.int32) for x in ("kind", "step", "group")}
+        tasks = np.zeros(k, np.int64)
+        _native.lib().find_plan_specs(self._h, _i32p(out["kind"]), _i32p(out["step"]), _i32p(out["group"]), _i64p(tasks))
+        out["tasks"] = tasks
+        return out
+
     # ---- device execution (torch tensors for memory/streams only) ----
     def workspace(self, n_energies: int, compute_gless: bool, device):
         import torch
