@@ -439,6 +439,7 @@ struct Tile {
       for (int c = 0; c < NT; ++c) acc[a][c][0][0] = acc[a][c][0][1] = acc[a][c][1][0] = acc[a][c][1][1] = 0.0;
   }
 
+  template <bool BT2 = BT>
   __device__ __forceinline__ void load(const double2* A, int64_t lda, const double2* B, int64_t ldb, int Mv, int Nv,
                                        int K, int kc, double2* st) {
     const int tid = threadIdx.x;
@@ -451,7 +452,7 @@ struct Tile {
       const bool ok = row < Mv && k0 + kk < K;
       cp_async16(As + row * kSK + kk, ok ? A + (int64_t)row * lda + k0 + kk : A, ok);
     }
-    if (BT) {
+    if (BT2) {
 #pragma unroll
       for (int q = tid; q < BN * kKC; q += kThreads) {
         const int col = q / kKC, kk = q % kKC;
@@ -469,6 +470,7 @@ struct Tile {
     cp_async_commit();
   }
 
+  template <bool BT2 = BT>
   __device__ __forceinline__ void mma(const double2* A, int64_t lda, const double2* B, int64_t ldb, int Mv, int Nv,
                                       int K, double2* smem) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -480,10 +482,10 @@ struct Tile {
     // zero padding of partial tiles is not multiplied
     const int mtv = min(MT, max(0, (Mv - wm * MT * 8 + 7) / 8));
     const int ntv = min(NT, max(0, (Nv - wn * NT * 8 + 7) / 8));
-    load(A, lda, B, ldb, Mv, Nv, K, 0, smem);
+    load<BT2>(A, lda, B, ldb, Mv, Nv, K, 0, smem);
     for (int kc = 0; kc < nk; ++kc) {
       if (kc + 1 < nk) {
-        load(A, lda, B, ldb, Mv, Nv, K, kc + 1, smem + ((kc + 1) & 1) * STAGE);
+        load<BT2>(A, lda, B, ldb, Mv, Nv, K, kc + 1, smem + ((kc + 1) & 1) * STAGE);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
@@ -501,7 +503,7 @@ struct Tile {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           b[nt] = Bs[(wn * NT * 8 + nt * 8 + fr) * kSK + kk + fc];
-          if (BT) b[nt].y = -b[nt].y;
+          if (BT2) b[nt].y = -b[nt].y;
         }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
@@ -537,7 +539,7 @@ struct Tile {
   }
 };
 using Tile64 = Tile<2, 4, 4, 2, false>;
-using Tile64H = Tile<2, 4, 4, 2, true>;
+
 template <int NB>
 struct XTileSel;
 template <>
@@ -601,62 +603,54 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(SolveParams P, const T
   }
 }
 
-// Inverses of the jb x jb diagonal block D (smem, ld NB+1) of a factored panel,
-// both at once with all T threads by recursive doubling:
-//   [A 0; C B]^-1 = [A^-1 0; -B^-1 C A^-1  B^-1]   (unit lower L)
-//   [A C; 0 B]^-1 = [A^-1 -A^-1 C B^-1; 0  B^-1]   (upper U)
-// Li, Ui, W: smem [NB][NB+1]; padding rows/cols >= jb act as identity.
-template <int NB, int T>
-__device__ void block_tri_inverses(double2 (*D)[NB + 1], int jb, double2 (*Li)[NB + 1], double2 (*Ui)[NB + 1],
-                                   double2 (*W)[NB + 1]) {
+// Inverse of one triangle of the jb x jb diagonal block D (smem, ld NB+1) of a
+// factored panel, with all kThreads threads, by recursive doubling:
+//   LOWER (unit L):  [A 0; C B]^-1 = [A^-1 0; -B^-1 C A^-1  B^-1]
+//   upper (U):       [A C; 0 B]^-1 = [A^-1 -A^-1 C B^-1; 0  B^-1]
+// X, W: smem [NB][NB+1]; rows/cols >= jb act as identity.
+template <int NB, bool LOWER>
+__device__ void block_tri_inverse(const double2 (*D)[NB + 1], int jb, double2 (*X)[NB + 1], double2 (*W)[NB + 1]) {
   const int tid = threadIdx.x;
-  for (int q = tid; q < NB * NB; q += T) {
+  for (int q = tid; q < NB * NB; q += kThreads) {
     const int r = q / NB, c = q % NB;
-    Li[r][c] = r == c ? make_double2(1.0, 0.0) : cz();
-    Ui[r][c] = r == c ? (r < jb ? cinv(D[r][r]) : make_double2(1.0, 0.0)) : cz();
+    X[r][c] = r != c ? cz() : ((LOWER || r >= jb) ? make_double2(1.0, 0.0) : cinv(D[r][r]));
   }
   __syncthreads();
 #pragma unroll 1
   for (int bs = 1; bs < NB; bs *= 2) {
-    // phase 1: W_L[i][j] = sum_q L[i][q] Li[q][j]  (i in B, q, j in A);  W_U[i][j] = sum_q Ui[i][q] U[q][j] (i, q in A, j in B)
-    for (int q = tid; q < (NB / 2) * bs; q += T) {
+    for (int q = tid; q < (NB / 2) * bs; q += kThreads) {
       const int pair = q / (bs * bs), loc = q % (bs * bs);
       const int k = pair * 2 * bs, a = loc / bs, b = loc % bs;
-      {  // lower: row i = k+bs+a (B), col j = k+b (A)
+      double2 acc = cz();
+      if (LOWER) {  // W[i][j] = sum_q L[i][q] X[q][j], i in B, q and j in A
         const int i = k + bs + a, jc = k + b;
-        double2 acc = cz();
 #pragma unroll 1
         for (int qq = jc; qq < k + bs; ++qq)
-          if (i < jb && qq < jb) acc = cfma(acc, D[i][qq], Li[qq][jc]);
+          if (i < jb && qq < jb) acc = cfma(acc, D[i][qq], X[qq][jc]);
         W[i][jc] = acc;
-      }
-      {  // upper: row i = k+a (A), col j = k+bs+b (B)
+      } else {  // W[i][j] = sum_q X[i][q] U[q][j], i and q in A, j in B
         const int i = k + a, jc = k + bs + b;
-        double2 acc = cz();
 #pragma unroll 1
         for (int qq = i; qq < k + bs; ++qq)
-          if (qq < jb && jc < jb) acc = cfma(acc, Ui[i][qq], D[qq][jc]);
+          if (qq < jb && jc < jb) acc = cfma(acc, X[i][qq], D[qq][jc]);
         W[i][jc] = acc;
       }
     }
     __syncthreads();
-    // phase 2: Li[i][j] = -sum_p Li[i][p] W[p][j] (p in B, p <= i);  Ui[i][j] = -sum_p W[i][p] Ui[p][j] (p in B, p <= j)
-    for (int q = tid; q < (NB / 2) * bs; q += T) {
+    for (int q = tid; q < (NB / 2) * bs; q += kThreads) {
       const int pair = q / (bs * bs), loc = q % (bs * bs);
       const int k = pair * 2 * bs, a = loc / bs, b = loc % bs;
-      {
+      double2 acc = cz();
+      if (LOWER) {  // X[i][j] = -sum_p X[i][p] W[p][j], p in B
         const int i = k + bs + a, jc = k + b;
-        double2 acc = cz();
 #pragma unroll 1
-        for (int p = k + bs; p <= i; ++p) acc = cfma(acc, Li[i][p], W[p][jc]);
-        Li[i][jc] = make_double2(-acc.x, -acc.y);
-      }
-      {
+        for (int p = k + bs; p <= i; ++p) acc = cfma(acc, X[i][p], W[p][jc]);
+        X[i][jc] = make_double2(-acc.x, -acc.y);
+      } else {  // X[i][j] = -sum_p W[i][p] X[p][j], p in B
         const int i = k + a, jc = k + bs + b;
-        double2 acc = cz();
 #pragma unroll 1
-        for (int p = k + bs; p <= jc; ++p) acc = cfma(acc, W[i][p], Ui[p][jc]);
-        Ui[i][jc] = make_double2(-acc.x, -acc.y);
+        for (int p = k + bs; p <= jc; ++p) acc = cfma(acc, W[i][p], X[p][jc]);
+        X[i][jc] = make_double2(-acc.x, -acc.y);
       }
     }
     __syncthreads();
@@ -672,15 +666,10 @@ __device__ void block_tri_inverses(double2 (*D)[NB + 1], int jb, double2 (*Li)[N
 // phase); every row is written once, to its final position, at the end.
 // Per column: one block argmax (shuffles + 1 barrier) + one broadcast barrier.
 template <int NB, int T>
-__global__ void __launch_bounds__(T) panel_kernel(SolveParams P, const Task* tasks) {
+__global__ void __launch_bounds__(T, 512 / T) panel_kernel(SolveParams P, const Task* tasks) {
   __shared__ double cand_v[2][T / 32];
   __shared__ int cand_i[2][T / 32];
   __shared__ double2 prow[2][NB + 1];
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2 (*tri)[NB + 1] = reinterpret_cast<double2 (*)[NB + 1]>(smem_raw);  // 4 x [NB][NB+1] (dynamic)
-  double2 (*tli)[NB + 1] = tri + NB;
-  double2 (*tui)[NB + 1] = tli + NB;
-  double2 (*tw)[NB + 1] = tui + NB;
   __shared__ int s_bad, s_nd;
   __shared__ int lpiv[NB], dsrc[2 * NB], ddst[2 * NB];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -747,13 +736,8 @@ __global__ void __launch_bounds__(T) panel_kernel(SolveParams P, const Task* tas
   if (has) {
     double2* dst = M + (int64_t)(j0 + pos) * n + j0;
     const int nl = min(pos, jb);
-    double2 buf[NB];
-#pragma unroll
-    for (int c = 0; c < NB; ++c)
-      if (c < nl) buf[c] = Lst[c];
-#pragma unroll
-    for (int c = 0; c < NB; ++c)
-      if (c < nl) dst[c] = buf[c];
+#pragma unroll 8
+    for (int c = 0; c < nl; ++c) dst[c] = Lst[c];
   }
   // net row permutation of this panel's interchanges (rows that moved: <= 2 NB)
   if (tid == 0) {
@@ -785,22 +769,6 @@ __global__ void __launch_bounds__(T) panel_kernel(SolveParams P, const Task* tas
       S.PERM[1 + 2 * NB + k] = ddst[k];
     }
   }
-  for (int q = tid; q < NB * NB; q += T) {
-    const int r = q / NB, c = q % NB;
-    tri[r][c] = (r < jb && c < jb) ? M[(int64_t)(j0 + r) * n + j0 + c] : cz();
-  }
-  __syncthreads();
-  block_tri_inverses<NB, T>(tri, jb, tli, tui, tw);
-  {
-    double2* lo = S.LINV + (int64_t)j * NB * NB;
-    double2* uo = S.UINV + (int64_t)j * NB * NB;
-    for (int q = tid; q < NB * NB; q += T) {
-      const int r = q / NB, c = q % NB;
-      const bool in = r < jb && c < jb;
-      lo[q] = in ? tli[r][c] : cz();
-      uo[q] = in ? tui[r][c] : cz();
-    }
-  }
   if (tid == 0 && s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
 }
 
@@ -816,7 +784,7 @@ __global__ void __launch_bounds__(kThreads) panel_smem_kernel(SolveParams P, con
   __shared__ double2 s_uinv;
   __shared__ int s_bad, s_nd;
   __shared__ int lpiv[NB], dsrc[2 * NB], ddst[2 * NB];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   const Task t = tasks[blockIdx.x];
   const int e = blockIdx.y;
   const ElimDesc d = P.elims[t.e];
@@ -910,34 +878,6 @@ __global__ void __launch_bounds__(kThreads) panel_smem_kernel(SolveParams P, con
       S.PERM[1 + 2 * NB + k] = ddst[k];
     }
   }
-  if (warp < 2 && lane < NB) {
-    const int c = lane;
-    double2 x[NB];
-    double2* out = (warp == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
-#pragma unroll
-    for (int r = 0; r < NB; ++r) x[r] = (r == c) ? make_double2(1.0, 0.0) : cz();
-    if (c < jb) {
-      if (warp == 0) {
-#pragma unroll
-        for (int m = 0; m < NB; ++m)
-          if (m >= c && m < jb)
-#pragma unroll
-            for (int r = m + 1; r < NB; ++r)
-              if (r < jb) x[r] = cfms(x[r], panel[r * PS + m], x[m]);
-      } else {
-#pragma unroll
-        for (int m = NB - 1; m >= 0; --m)
-          if (m < jb && m <= c) {
-            x[m] = cmul(x[m], cinv(panel[m * PS + m]));
-#pragma unroll
-            for (int r = 0; r < NB; ++r)
-              if (r < m) x[r] = cfms(x[r], panel[r * PS + m], x[m]);
-          }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < NB; ++r) out[r * NB + c] = (r < jb && c < jb) ? x[r] : cz();
-  }
   if (tid == 0 && s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
 }
 
@@ -980,6 +920,26 @@ __global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Tas
     __syncthreads();
     if (t.a == 2) return;
   }
+  {  // the diagonal block's inverse this tile needs (L for U12 tiles, U for L21 tiles), published to the
+     // elimination's LINV/UINV slot; every tile of the elimination writes the same values
+    typedef double2 Row[NB + 1];
+    Row* Dm = reinterpret_cast<Row*>(smem);
+    Row* Xm = Dm + NB;
+    Row* Wm = Xm + NB;
+    for (int q = threadIdx.x; q < NB * NB; q += kThreads) {
+      const int r = q / NB, c = q % NB;
+      Dm[r][c] = (r < jb && c < jb) ? M[(int64_t)(j0 + r) * n + j0 + c] : cz();
+    }
+    __syncthreads();
+    if (t.a == 0) block_tri_inverse<NB, true>(Dm, jb, Xm, Wm);
+    else block_tri_inverse<NB, false>(Dm, jb, Xm, Wm);
+    double2* out = (t.a == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
+    for (int q = threadIdx.x; q < NB * NB; q += kThreads) {
+      const int r = q / NB, c = q % NB;
+      out[q] = (r < jb && c < jb) ? Xm[r][c] : cz();
+    }
+    __syncthreads();
+  }
   if (t.a == 0) {
     using TT = typename TrsmTiles<NB>::U;
     const int c0 = t.b;
@@ -1018,9 +978,37 @@ __global__ void __launch_bounds__(kThreads, 2) trail_kernel(SolveParams P, const
   T.zero();
   T.mma(M + (int64_t)r0 * n + j0, n, M + (int64_t)j0 * n + c0, n, min(kTile, n - r0), min(kTile, n - c0), jb, smem);
   T.for_each([&](int r, int c, double2 v) {
-    if (r0 + r < n && c0 + c < n) {
+    if (r0 + r < n && c0 + c < n && (r0 + r < s || c0 + c < s)) {
       double2* p = M + (int64_t)(r0 + r) * n + c0 + c;
       *p = csub(*p, v);
+    }
+  });
+}
+
+// ---- U = A_BB - Y U12 in one K = s pass (Y = M[s:, :s] = A_BS U11^-1, U12 = M[:s, s:]),
+// stored sorted (solver.py:234-243); final steps keep U_f in M for the epilogue
+__global__ void __launch_bounds__(kThreads, 2) schur_kernel(SolveParams P, const Task* tasks) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, b = d.b;
+  double2* M = scratch_of(P, d, e).M;
+  const int i0 = t.a * kTile, c0 = t.b * kTile;
+  Tile64 T;
+  T.zero();
+  T.mma(M + (int64_t)(s + i0) * n, n, M + s + c0, n, min(kTile, b - i0), min(kTile, b - c0), s, smem);
+  const bool store = d.kind != kFinal && d.out_arena >= 0;
+  double2* out = store ? P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off : nullptr;
+  const int32_t* rank = P.i32 + d.rank_off;
+  T.for_each([&](int r, int c, double2 v) {
+    const int i = i0 + r, jj = c0 + c;
+    if (i < b && jj < b) {
+      double2* p = M + (int64_t)(s + i) * n + s + jj;
+      const double2 val = csub(*p, v);
+      if (store) out[(int64_t)rank[i] * b + rank[jj]] = val;
+      else *p = val;
     }
   });
 }
@@ -1068,7 +1056,7 @@ __global__ void __launch_bounds__(kThreads) xsolve_kernel(SolveParams P, const T
   }
 }
 
-// ---- pivot permutation (sigma), optional L (unit-test shim), store U sorted (solver.py:234-243)
+// ---- pivot permutation sigma and its inverse (+ L for the unit-test shim)
 __global__ void __launch_bounds__(kThreads) finish_kernel(SolveParams P, const Task* tasks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int* sig = reinterpret_cast<int*>(smem_raw);
@@ -1095,43 +1083,33 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SolveParams P, const T
   if (P.dbg_l && t.e == 0 && e == 0)
     for (int64_t q = tid; q < (int64_t)b * s; q += kThreads)
       P.dbg_l[(q / s) * s + sig[q % s]] = S.M[(int64_t)(s + q / s) * n + q % s];
-  if (d.kind != kFinal && d.out_arena >= 0) {
-    double2* out = P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off;
-    const int32_t* rank = P.i32 + d.rank_off;
-    for (int64_t q = tid; q < (int64_t)b * b; q += kThreads) {
-      const int i = (int)(q / b), jj = (int)(q % b);
-      out[(int64_t)rank[i] * b + rank[jj]] = S.M[(int64_t)(s + i) * n + s + jj];
-    }
-  }
 }
 
-// ---- T = MS[s:, :] - X MS[:s, :]   (c = 0: S columns, c = 1/2: B columns)
+// ---- T_S = MS[s:, :s] - X MS[:s, :s]   (the S columns of T = Sigma'_B: - X Sigma'_S:)
 __global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const Task* tasks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw);
   const Task t = tasks[blockIdx.x];
-  if (t.c == 2 && P.rsym != 0) return;  // upper-triangle tile of a (skew-)Hermitian R
   const int e = blockIdx.y;
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s, b = d.b;
   const Scr S = scratch_of(P, d, e);
-  const int i0 = t.a * kTile;
-  const int c0 = t.c == 0 ? t.b * kTile : s + t.b * kTile;
-  const int cend = t.c == 0 ? s : n;
+  const int i0 = t.a * kTile, c0 = t.b * kTile;
   Tile64 T;
   T.zero();
-  T.mma(S.M + (int64_t)(s + i0) * n, n, S.MS + c0, n, min(kTile, b - i0), min(kTile, cend - c0), s, smem);
+  T.mma(S.M + (int64_t)(s + i0) * n, n, S.MS + c0, n, min(kTile, b - i0), min(kTile, s - c0), s, smem);
   T.for_each([&](int r, int c, double2 v) {
-    if (i0 + r < b && c0 + c < cend) {
+    if (i0 + r < b && c0 + c < s) {
       double2* p = S.MS + (int64_t)(s + i0 + r) * n + c0 + c;
       *p = csub(*p, v);
     }
   });
 }
 
-// ---- R = T[:, s:] - T[:, :s] X^H, stored sorted (or kept for the final step).
-// Symmetric mode: lower-triangle tiles only, the upper triangle is written as
-// the (skew-)conjugate mirror (element (i, j) for i >= j only: deterministic).
+// ---- R = Sigma'_BB - X Sigma'_SB - T_S X^H in one pass (two K = s products into one
+// accumulator), stored sorted (or kept in MS for the final step).  Symmetric mode:
+// lower-triangle tiles only; the upper triangle is written as the (skew-)conjugate
+// mirror of elements (i >= j), so results stay deterministic.
 __global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const Task* tasks) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw);
@@ -1142,10 +1120,11 @@ __global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const
   const int n = d.n, s = d.s, b = d.b;
   const Scr S = scratch_of(P, d, e);
   const int i0 = t.a * kTile, c0 = t.b * kTile;
-  Tile64H T;
+  const int mv = min(kTile, b - i0), nv = min(kTile, b - c0);
+  Tile64 T;
   T.zero();
-  T.mma(S.MS + (int64_t)(s + i0) * n, n, S.M + (int64_t)(s + c0) * n, n, min(kTile, b - i0), min(kTile, b - c0), s,
-        smem);
+  T.mma<false>(S.M + (int64_t)(s + i0) * n, n, S.MS + s + c0, n, mv, nv, s, smem);         // X Sigma'_SB
+  T.mma<true>(S.MS + (int64_t)(s + i0) * n, n, S.M + (int64_t)(s + c0) * n, n, mv, nv, s, smem);  // T_S X^H
   const bool store = d.kind != kFinal && d.out_arena >= 0;
   const bool mirror = store && P.rsym != 0;
   const double sg = P.rsym < 0 ? -1.0 : 1.0;
@@ -1234,7 +1213,8 @@ size_t xsolve_smem() {
 
 template <int NB>
 size_t trsm_smem() {
-  return std::max(std::max(TrsmTiles<NB>::U::SMEM, TrsmTiles<NB>::L::SMEM), (size_t)2 * NB * kTile * sizeof(double2));
+  return std::max(std::max(std::max(TrsmTiles<NB>::U::SMEM, TrsmTiles<NB>::L::SMEM), (size_t)2 * NB * kTile * sizeof(double2)),
+                  (size_t)3 * NB * (NB + 1) * sizeof(double2));
 }
 
 int set_attrs(find_status* st) {
@@ -1243,10 +1223,7 @@ int set_attrs(find_status* st) {
   const int mx = (int)kMaxSmem;
   CUDA_TRY(cudaFuncSetAttribute(small_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  const int psm = 4 * 32 * 33 * (int)sizeof(double2);
-  CUDA_TRY(cudaFuncSetAttribute(panel_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
-  CUDA_TRY(cudaFuncSetAttribute(panel_kernel<32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
-  CUDA_TRY(cudaFuncSetAttribute(panel_kernel<32, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
+
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<32>()));
@@ -1254,7 +1231,8 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<8>()));
   CUDA_TRY(cudaFuncSetAttribute(trail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(tgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
-  CUDA_TRY(cudaFuncSetAttribute(rgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64H::SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(rgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(schur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<32>()));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<16>()));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<8>()));
@@ -1355,10 +1333,9 @@ int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE
         case kLGatherS: gather_kernel<true><<<grid, kThreads, 0, stream>>>(prm, tk); break;
         case kLPanel: {
           const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
-          constexpr size_t psm = 4 * 32 * 33 * sizeof(double2);
-          if (L.nb == 32 && g_reg_panel && rmax <= 64) panel_kernel<32, 64><<<grid, 64, psm, stream>>>(prm, tk);
-          else if (L.nb == 32 && g_reg_panel && rmax <= 128) panel_kernel<32, 128><<<grid, 128, psm, stream>>>(prm, tk);
-          else if (L.nb == 32 && g_reg_panel) panel_kernel<32, 256><<<grid, 256, psm, stream>>>(prm, tk);
+          if (L.nb == 32 && g_reg_panel && rmax <= 64) panel_kernel<32, 64><<<grid, 64, 0, stream>>>(prm, tk);
+          else if (L.nb == 32 && g_reg_panel && rmax <= 128) panel_kernel<32, 128><<<grid, 128, 0, stream>>>(prm, tk);
+          else if (L.nb == 32 && g_reg_panel) panel_kernel<32, 256><<<grid, 256, 0, stream>>>(prm, tk);
           else if (L.nb == 32)
             panel_smem_kernel<32><<<grid, kThreads, (size_t)std::max(rmax, 1) * 33 * sizeof(double2), stream>>>(prm, tk);
           else if (L.nb == 16)
@@ -1381,7 +1358,8 @@ int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE
           finish_kernel<<<grid, kThreads, std::max<size_t>((size_t)G.max_s * sizeof(int), 16), stream>>>(prm, tk);
           break;
         case kLTGemm: tgemm_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk); break;
-        case kLRGemm: rgemm_kernel<<<grid, kThreads, Tile64H::SMEM, stream>>>(prm, tk); break;
+        case kLRGemm: rgemm_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk); break;
+        case kLSchur: schur_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk); break;
         case kLFinal: {
           const int cmax = std::max(1, G.max_b);
           const size_t smem = (size_t)kSmallWarps * 2 * cmax * (cmax + 1) * sizeof(double2);

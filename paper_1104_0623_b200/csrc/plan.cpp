@@ -130,10 +130,20 @@ void find_build_tasks(find_plan* P) {
         const int j1 = std::min(d.s, (j + 1) * nb), m = d.n - j1;
         const int t = (m + kTile - 1) / kTile;
         for (int tm = 0; tm < t; ++tm)
-          for (int tn = 0; tn < t; ++tn) push((int32_t)e, tm, tn, 0);
+          for (int tn = 0; tn < t; ++tn)  // the B x B block is updated once, by the Schur launch
+            if (j1 + tm * kTile < d.s || j1 + tn * kTile < d.s) push((int32_t)e, tm, tn, 0);
       }
       spec(kLTrail, j, nb, gi, off);
     }
+    off = (int64_t)P->tasks.size();
+    for (int64_t e = G.begin; e < G.end; ++e) {
+      const ElimDesc& d = P->elims[e];
+      if (d.b == 0) continue;
+      const int tb = (d.b + kTile - 1) / kTile;
+      for (int tm = 0; tm < tb; ++tm)
+        for (int tn = 0; tn < tb; ++tn) push((int32_t)e, tm, tn, 0);
+    }
+    spec(kLSchur, 0, nb, gi, off);
     for (int j = steps - 1; j >= 0; --j) {
       off = (int64_t)P->tasks.size();
       for (int64_t e = G.begin; e < G.end; ++e) {
@@ -160,10 +170,8 @@ void find_build_tasks(find_plan* P) {
       const ElimDesc& d = P->elims[e];
       if (d.s == 0 || d.b == 0) continue;
       const int tb = (d.b + kTile - 1) / kTile;
-      for (int tm = 0; tm < tb; ++tm) {
+      for (int tm = 0; tm < tb; ++tm)
         for (int tn = 0; tn < (d.s + kTile - 1) / kTile; ++tn) push((int32_t)e, tm, tn, 0);
-        for (int tn = 0; tn < tb; ++tn) push((int32_t)e, tm, tn, (tn > tm && d.kind != kFinal) ? 2 : 1);
-      }
     }
     spec(kLTGemm, 0, nb, gi, off);
     off = (int64_t)P->tasks.size();

@@ -47,9 +47,10 @@ enum LaunchKind : int32_t {
   kLXSolve = 5,    // X = Y L11^-1, block column j              tasks {e, tm}
   kLFinish = 6,    // pivot permutation + store U               tasks {e}
   kLGatherS = 7,   // merged, pivot-permuted Sigma              tasks {e, row0, nrows}
-  kLTGemm = 8,     // T = S_B: - X S_S:                         tasks {e, tm, tn}
-  kLRGemm = 9,     // R = T_B - T_S X^H (+ store)               tasks {e, tm, tn}
+  kLTGemm = 8,     // T_S = S_BS - X S_SS                       tasks {e, tm, tn}
+  kLRGemm = 9,     // R = S_BB - X S_SB - T_S X^H (+ store)     tasks {e, tm, tn, sym-skip}
   kLFinal = 10,    // leaf inverse + G^< sandwich               tasks {e}
+  kLSchur = 11,    // U = A_BB - Y U12 (K = s), stored sorted  tasks {e, tm, tn}
 };
 
 struct Task { int32_t e, a, b, c; };
