@@ -331,7 +331,7 @@ def run_b200(args):
         "work_per_energy_mults": W,
         "roofline": roofline,
         "e2e": e2e,
-        "gpu_launches": int(plan.launch_count() * args.steps),
+        "gpu_launches": int(plan.launch_count(n_e) * args.steps),
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -137,18 +137,20 @@ int find_solve_groups(find_plan* plan, const void* a_vals, const void* s_vals, i
 int find_plan_groups(const find_plan* plan, int32_t* pass, int32_t* level, int32_t* path, int64_t* count,
                      int32_t* max_n, int32_t* max_s, int32_t* max_b);
 
-/* Kernel-launch table in issue order (find_solve_launch_count() entries):
- * launch kind (0 warp path, 1 gather A, 2 panel, 3 TRSM, 4 trailing, 5 X
- * solve, 6 finish, 7 gather Sigma, 8 T, 9 R, 10 final), panel step, launch
- * group, task count.  Any pointer may be NULL. */
-int find_plan_specs(const find_plan* plan, int32_t* kind, int32_t* step, int32_t* group, int64_t* tasks);
+/* Kernel-launch table of a find_solve over n_energies points, in issue order
+ * (find_solve_launch_count() entries): launch kind (0 warp path, 1 gather A,
+ * 2 panel, 3 TRSM, 4 trailing, 5 X solve, 6 finish, 7 gather Sigma, 8 T_S,
+ * 9 R, 10 final, 11 Schur, 12 fused LU), panel step, launch group, task
+ * count.  Any pointer may be NULL. */
+int find_plan_specs(const find_plan* plan, int32_t n_energies, int32_t* kind, int32_t* step, int32_t* group,
+                    int64_t* tasks);
 
 /* Synchronise `stream` and decode the device status of the last find_solve
  * that used `ws`. */
 int find_solve_status(find_plan* plan, void* ws, int32_t n_energies, void* stream, find_status* st);
 
-/* Number of kernel launches one find_solve enqueues. */
-int64_t find_solve_launch_count(const find_plan* plan);
+/* Number of kernel launches one find_solve over n_energies points enqueues. */
+int64_t find_solve_launch_count(const find_plan* plan, int32_t n_energies);
 
 /* Unit-test shim with the reference's kernel-level signature
  * schur_update + sigma_update (kernels.py:363-392) for ONE dense
@@ -156,7 +158,7 @@ int64_t find_solve_launch_count(const find_plan* plan);
  * Sigma blocks (may be NULL), all row-major device buffers; writes
  * u_out[b*b], r_out[b*b], l_out[b*s] (L = A(B,S) A(S,S)^{-1}).  Runs the
  * same device code path as find_solve (force_path: -1 auto, 0 warp path,
- * 1 CTA path).  Returns FIND_ESINGULAR with st->node_id = position k of the
+ * 1 blocked CTA path, 2 CTA-per-elimination shared-memory path).  Returns FIND_ESINGULAR with st->node_id = position k of the
  * failing pivot. */
 int find_schur_sigma_update(int32_t s, int32_t b, const void* ass, const void* asb, const void* abs_,
                             const void* abb, const void* sss, const void* ssb, const void* sbs,

@@ -72,9 +72,9 @@ def lib():
         "find_solve_groups": (i32, [P, P, P, i32, i32, i32, dbl, P, P, P, sz, i64, i64, P, st]),
         "find_plan_groups": (i32, [P, pi32, pi32, pi32, pi64, pi32, pi32, pi32]),
         "find_solve_status": (i32, [P, P, i32, P, st]),
-        "find_solve_launch_count": (i64, [P]),
+        "find_solve_launch_count": (i64, [P, i32]),
         "find_plan_exception_slots": (i64, [P, i32, pi64, i64]),
-        "find_plan_specs": (i32, [P, pi32, pi32, pi32, pi64]),
+        "find_plan_specs": (i32, [P, i32, pi32, pi32, pi32, pi64]),
         "find_schur_sigma_update": (i32, [i32, i32, P, P, P, P, P, P, P, P, dbl, P, P, P, i32, P, st]),
     }
     for name, (res, args) in sig.items():

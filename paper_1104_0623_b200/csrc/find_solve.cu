@@ -392,6 +392,192 @@ __device__ void block_argmax(double& v, int& vi, double* cv, int* ci) {
   }
 }
 
+// ================================================================== mid path
+// One 128-thread CTA per (elimination, energy) for 32 < s+b <= 64: the merged
+// matrix, LU, X and the U / R products all in shared memory (the warp path's
+// algorithm, CTA-wide).
+constexpr int kMidThreads = 128;
+constexpr int kMidMaxN = 64;
+__host__ __device__ constexpr int mid_smem_elems(int nmax, int xcap) { return nmax * (nmax + 1) + xcap + 3 * kMidMaxN / 4 + 2 * kMidMaxN + 16; }
+
+template <int NT>
+__device__ __forceinline__ void block_max(double& v, double* cv) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) cv[warp] = v;
+  __syncthreads();
+  v = cv[0];
+  for (int w = 1; w < NT / 32; ++w) v = fmax(v, cv[w]);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kMidThreads) mid_elim_kernel(SolveParams P, int64_t count, int nmax, int xcap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int NT = kMidThreads;
+  __shared__ double cv[2][NT / 32];
+  __shared__ int ci[2][NT / 32];
+  __shared__ double2 s_uinv;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  const int64_t idx = blockIdx.x;
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[idx];
+  const int64_t elim_global = P.elim_base + idx;
+  const int n = d.n, s = d.s, b = d.b;
+  const int ld = nmax + 1;
+  double2* MA = reinterpret_cast<double2*>(smem_raw);
+  double2* XC = MA + nmax * ld;
+  double2* LC = XC + xcap;  // multipliers of the current column [64]
+  int* piv = reinterpret_cast<int*>(LC + kMidMaxN);
+  int* sig = piv + kMidMaxN;
+  int* isg = sig + kMidMaxN;
+  const int32_t* map = P.i32 + d.map_off;
+  const int32_t* rank = P.i32 + d.rank_off;
+  const double2* lblk = d.left_arena >= 0 ? P.arena[d.left_arena] + (int64_t)e * P.arena_elems[d.left_arena] + d.left_off : nullptr;
+  const double2* rblk = d.right_arena >= 0 ? P.arena[d.right_arena] + (int64_t)e * P.arena_elems[d.right_arena] + d.right_off : nullptr;
+  const double2* av = P.a_vals + (int64_t)e * P.nnz;
+  const SparseEntry* sp = P.sparse + d.sparse_off;
+  if (tid == 0) s_bad = INT32_MAX;
+
+  // ---- gather A ----
+  for (int q = tid; q < n * n; q += NT) {
+    const int i = q / n, j = q % n;
+    MA[i * ld + j] = block_entry(d, lblk, rblk, map[i], map[j]);
+  }
+  __syncthreads();
+  for (int q = tid; q < d.nsparse; q += NT) {
+    const SparseEntry en = sp[q];
+    MA[en.i * ld + en.j] = ldg2(av + en.csr);
+  }
+  __syncthreads();
+  double scale = 0.0;
+  for (int q = tid; q < s * s; q += NT) scale = fmax(scale, cabs(MA[(q / s) * ld + q % s]));
+  block_max<NT>(scale, cv[0]);
+  if (tid == 0 && s > 0 && scale == 0.0) s_bad = 0;
+
+  // ---- partial LU, pivot search among the S rows ----
+  for (int k = 0; k < s; ++k) {
+    double v = -1.0;
+    int vi = INT32_MAX;
+    for (int r = k + tid; r < s; r += NT) {
+      const double a = cabs1(MA[r * ld + k]);
+      if (a > v) { v = a; vi = r; }
+    }
+    block_argmax<NT>(v, vi, cv[k & 1], ci[k & 1]);
+    const int pr = vi;
+    if (tid == 0) {
+      piv[k] = pr;
+      const double2 u = MA[pr * ld + k];
+      s_uinv = cinv(u);
+      if (cabs(u) < P.rtol * scale) atomicMin(&s_bad, k);
+    }
+    if (pr != k)
+      for (int c = tid; c < n; c += NT) {
+        const double2 tmp = MA[k * ld + c];
+        MA[k * ld + c] = MA[pr * ld + c];
+        MA[pr * ld + c] = tmp;
+      }
+    __syncthreads();
+    const double2 uinv = s_uinv;
+    const int rows = n - k - 1;
+    for (int r = tid; r < rows; r += NT) {
+      const double2 l = cmul(MA[(k + 1 + r) * ld + k], uinv);
+      LC[r] = l;
+      MA[(k + 1 + r) * ld + k] = l;
+    }
+    __syncthreads();
+    for (int q = tid; q < rows * rows; q += NT) {
+      const int r = q / rows, c = q % rows;
+      double2* p = MA + (k + 1 + r) * ld + k + 1 + c;
+      *p = cfms(*p, LC[r], MA[k * ld + k + 1 + c]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && s_bad != INT32_MAX) report_bad(P, elim_global, e, s_bad);
+
+  // ---- X = Y L11^-1 (row per thread) -> XC [b][s] ----
+  for (int i = tid; i < b; i += NT) {
+    double2* rw = MA + (s + i) * ld;
+    for (int k = s - 1; k >= 0; --k) {
+      double2 acc = rw[k];
+      for (int m = k + 1; m < s; ++m) acc = cfms(acc, rw[m], MA[m * ld + k]);
+      rw[k] = acc;
+    }
+    for (int k = 0; k < s; ++k) XC[i * s + k] = rw[k];
+  }
+  if (tid == 0) {
+    for (int k = 0; k < s; ++k) sig[k] = k;
+    for (int k = 0; k < s; ++k) { const int tmp = sig[k]; sig[k] = sig[piv[k]]; sig[piv[k]] = tmp; }
+  }
+  __syncthreads();
+  if (P.dbg_l && idx == 0 && e == 0)
+    for (int q = tid; q < b * s; q += NT) P.dbg_l[(int64_t)(q / s) * s + sig[q % s]] = XC[q];
+  double2* UF = XC + b * s;
+  if (d.kind == kFinal) {
+    for (int q = tid; q < b * b; q += NT) UF[q] = MA[(s + q / b) * ld + s + q % b];
+  } else if (d.out_arena >= 0) {
+    double2* out = P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off;
+    for (int q = tid; q < b * b; q += NT) {
+      const int i = q / b, j = q % b;
+      out[(int64_t)rank[i] * b + rank[j]] = MA[(s + i) * ld + s + j];
+    }
+  }
+  __syncthreads();
+  double2* MS = MA;
+  if (P.compute_gless) {
+    const double2* lr = lblk ? lblk + (int64_t)d.p * d.p : nullptr;
+    const int q0 = n - d.p;
+    const double2* rr = rblk ? rblk + (int64_t)q0 * q0 : nullptr;
+    const double2* sv = P.s_vals + (P.s_broadcast ? 0 : (int64_t)e * P.nnz);
+    for (int k = tid; k < n; k += NT) {
+      if (k >= s) isg[k] = k;
+      else isg[sig[k]] = k;
+    }
+    __syncthreads();
+    for (int q = tid; q < n * n; q += NT) {
+      const int i = q / n, j = q % n;
+      MS[i * ld + j] = block_entry(d, lr, rr, map[i < s ? sig[i] : i], map[j < s ? sig[j] : j]);
+    }
+    __syncthreads();
+    for (int q = tid; q < d.nsparse; q += NT) {
+      const SparseEntry en = sp[q];
+      MS[isg[en.i] * ld + isg[en.j]] = ldg2(sv + en.csr);
+    }
+    __syncthreads();
+    // T_S = S'_BS - X S'_SS
+    for (int q = tid; q < b * s; q += NT) {
+      const int i = q / s, c = q % s;
+      double2 acc = MS[(s + i) * ld + c];
+      for (int m = 0; m < s; ++m) acc = cfms(acc, XC[i * s + m], MS[m * ld + c]);
+      MS[(s + i) * ld + c] = acc;
+    }
+    __syncthreads();
+    // R = S'_BB - X S'_SB - T_S X^H
+    const bool store = d.kind != kFinal && d.out_arena >= 0;
+    const bool mirror = store && P.rsym != 0;
+    const double sgn = P.rsym < 0 ? -1.0 : 1.0;
+    double2* out = store ? P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off + (int64_t)b * b
+                         : nullptr;
+    for (int q = tid; q < b * b; q += NT) {
+      const int i = q / b, j = q % b;
+      if (mirror && j > i) continue;
+      double2 acc = MS[(s + i) * ld + s + j];
+      for (int m = 0; m < s; ++m) {
+        acc = cfms(acc, XC[i * s + m], MS[m * ld + s + j]);
+        acc = cfms(acc, MS[(s + i) * ld + m], cconj(XC[j * s + m]));
+      }
+      if (!store) {
+        MS[(s + i) * ld + s + j] = acc;
+      } else {
+        out[(int64_t)rank[i] * b + rank[j]] = acc;
+        if (mirror && i != j) out[(int64_t)rank[j] * b + rank[i]] = make_double2(sgn * acc.x, -sgn * acc.y);
+      }
+    }
+    __syncthreads();
+  }
+  if (d.kind == kFinal && tid < 32) final_epilogue_warp(P, d, elim_global, e, UF, b, MS + s * ld + s, ld, tid);
+}
+
 struct Scr {
   double2* M;   // merged A, then L\U, Y/X, U               [n][n]
   double2* MS;  // merged, pivot-permuted Sigma, then T, R  [n][n]
@@ -403,6 +589,7 @@ struct Scr {
   double* pmax;   // per gather row chunk: max |A(S,S)| over its rows   [ceil(n/16)]
   double2* LINV;  // per panel j: L_jj^-1  [NB][NB]   (valid when nb > 0)
   double2* UINV;  // per panel j: U_jj^-1  [NB][NB]
+  double2* X;     // X = Y L11^-1   [b][s]            (valid when nb > 0)
 };
 // Layout must match find_scratch_elems() in plan.cpp.
 __device__ __forceinline__ Scr scratch_of(const SolveParams& P, const ElimDesc& d, int e, int nb = 0) {
@@ -419,6 +606,7 @@ __device__ __forceinline__ Scr scratch_of(const SolveParams& P, const ElimDesc& 
   r.pmax = r.scale + 2;
   r.LINV = r.M + 2 * nn + ints + 1 + (d.n + 31) / 32;
   r.UINV = nb ? r.LINV + (int64_t)((d.s + nb - 1) / nb) * nb * nb : r.LINV;
+  r.X = nb ? r.UINV + (int64_t)((d.s + nb - 1) / nb) * nb * nb : r.LINV;
   return r;
 }
 
@@ -666,18 +854,29 @@ __device__ void block_tri_inverse(const double2 (*D)[NB + 1], int jb, double2 (*
 // phase); every row is written once, to its final position, at the end.
 // Per column: one block argmax (shuffles + 1 barrier) + one broadcast barrier.
 template <int NB, int T>
-__global__ void __launch_bounds__(T, 512 / T) panel_kernel(SolveParams P, const Task* tasks) {
-  __shared__ double cand_v[2][T / 32];
-  __shared__ int cand_i[2][T / 32];
-  __shared__ double2 prow[2][NB + 1];
-  __shared__ int s_bad, s_nd;
-  __shared__ int lpiv[NB], dsrc[2 * NB], ddst[2 * NB];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y;
-  const ElimDesc d = P.elims[t.e];
+struct PanelShared {
+  double cand_v[2][T / 32];
+  int cand_i[2][T / 32];
+  double2 prow[2][NB + 1];
+  int s_bad, s_nd;
+  int lpiv[NB], dsrc[2 * NB], ddst[2 * NB];
+};
+
+template <int NB, int T>
+__device__ void panel_body(const SolveParams& P, int64_t eidx, const ElimDesc& d, int e, int j,
+                           PanelShared<NB, T>& sh) {
+  auto& cand_v = sh.cand_v;
+  auto& cand_i = sh.cand_i;
+  auto& prow = sh.prow;
+  auto& s_bad = sh.s_bad;
+  auto& s_nd = sh.s_nd;
+  auto& lpiv = sh.lpiv;
+  auto& dsrc = sh.dsrc;
+  auto& ddst = sh.ddst;
+  const int tid = threadIdx.x;
+  const struct { int64_t e; } t = {eidx};
   const int n = d.n, s = d.s;
-  const int j = t.a, j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
+  const int j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
   const Scr S = scratch_of(P, d, e, NB);
   double2* M = S.M;
   double2* Lst = S.MS + (int64_t)tid * NB;  // this thread's finished multipliers
@@ -770,6 +969,15 @@ __global__ void __launch_bounds__(T, 512 / T) panel_kernel(SolveParams P, const 
     }
   }
   if (tid == 0 && s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
+  __syncthreads();
+}
+
+template <int NB, int T>
+__global__ void __launch_bounds__(T, 512 / T) panel_kernel(SolveParams P, const Task* tasks) {
+  __shared__ PanelShared<NB, T> sh;
+  const Task t = tasks[blockIdx.x];
+  const ElimDesc d = P.elims[t.e];
+  panel_body<NB, T>(P, t.e, d, blockIdx.y, t.a, sh);
 }
 
 // ---- same panel step with the S-row panel in shared memory (R > 256 rows):
@@ -1015,26 +1223,22 @@ __global__ void __launch_bounds__(kThreads, 2) schur_kernel(SolveParams P, const
 
 // ---- X_j = (Y_j - X_{>j} L11[>j, j]) L_jj^-1 for 64 B rows
 template <int NB>
-__global__ void __launch_bounds__(kThreads) xsolve_kernel(SolveParams P, const Task* tasks, int j) {
+__device__ void xsolve_tile(const Scr& S, int n, int s, int j, int r0, double2* smem) {
   using TT = typename XTileSel<NB>::T;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* smem = reinterpret_cast<double2*>(smem_raw);
-  double2* Z = smem + 2 * TT::STAGE;    // [64][NB+1]
+  double2* M = S.M;
+  static_assert(kTile * (NB + 1) + NB * (NB + 1) <= 2 * TT::STAGE, "Z/D staging must fit in the drained stages");
+  double2* Z = smem;                     // [64][NB+1]   (reuses the cp.async stages after the mma)
   double2* D = Z + kTile * (NB + 1);     // [NB][NB+1]
   const int tid = threadIdx.x;
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y;
-  const ElimDesc d = P.elims[t.e];
-  const int n = d.n, s = d.s;
+  const int b = n - s;
   const int j0 = j * NB, jb = min(NB, s - j0), j1 = j0 + jb;
-  double2* M = scratch_of(P, d, e).M;
-  const int r0 = s + t.a * kTile, nr = min(kTile, n - r0);
+  const int nr = min(kTile, b - r0);
   TT T;
   T.zero();
-  if (s > j1) T.mma(M + (int64_t)r0 * n + j1, n, M + (int64_t)j1 * n + j0, n, nr, jb, s - j1, smem);
+  if (s > j1) T.mma(S.X + (int64_t)r0 * s + j1, s, M + (int64_t)j1 * n + j0, n, nr, jb, s - j1, smem);
   for (int q = tid; q < kTile * jb; q += kThreads) {
     const int r = q / jb, c = q % jb;
-    Z[r * (NB + 1) + c] = r < nr ? M[(int64_t)(r0 + r) * n + j0 + c] : cz();
+    Z[r * (NB + 1) + c] = r < nr ? M[(int64_t)(s + r0 + r) * n + j0 + c] : cz();
   }
   for (int q = tid; q < jb * jb; q += kThreads) D[(q / jb) * (NB + 1) + q % jb] = M[(int64_t)(j0 + q / jb) * n + j0 + q % jb];
   __syncthreads();
@@ -1052,20 +1256,26 @@ __global__ void __launch_bounds__(kThreads) xsolve_kernel(SolveParams P, const T
   __syncthreads();
   for (int q = tid; q < nr * jb; q += kThreads) {
     const int r = q / jb, c = q % jb;
-    M[(int64_t)(r0 + r) * n + j0 + c] = Z[r * (NB + 1) + c];
+    S.X[(int64_t)(r0 + r) * s + j0 + c] = Z[r * (NB + 1) + c];
   }
+  __syncthreads();
 }
 
-// ---- pivot permutation sigma and its inverse (+ L for the unit-test shim)
-__global__ void __launch_bounds__(kThreads) finish_kernel(SolveParams P, const Task* tasks) {
+// ---- X_j = (Y_j - X_{>j} L11[>j, j]) L_jj^-1 for 64 B rows (X in its own buffer; Y stays for the Schur launch)
+template <int NB>
+__global__ void __launch_bounds__(kThreads) xsolve_kernel(SolveParams P, const Task* tasks, int j) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int* sig = reinterpret_cast<int*>(smem_raw);
-  const int tid = threadIdx.x;
   const Task t = tasks[blockIdx.x];
   const int e = blockIdx.y;
   const ElimDesc d = P.elims[t.e];
-  const int n = d.n, s = d.s, b = d.b;
-  const Scr S = scratch_of(P, d, e);
+  xsolve_tile<NB>(scratch_of(P, d, e, NB), d.n, d.s, j, t.a * kTile, reinterpret_cast<double2*>(smem_raw));
+}
+
+// ---- pivot permutation sigma and its inverse (+ L for the unit-test shim)
+__device__ void finish_body(const SolveParams& P, int64_t eidx, const ElimDesc& d, int e, int nb, int* sig) {
+  const int tid = threadIdx.x;
+  const int s = d.s, b = d.b;
+  const Scr S = scratch_of(P, d, e, nb);
   for (int k = tid; k < s; k += kThreads) sig[k] = k;
   __syncthreads();
   if (tid == 0)
@@ -1080,13 +1290,131 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SolveParams P, const T
     S.SIG[k] = sig[k];
     S.ISG[sig[k]] = k;
   }
-  if (P.dbg_l && t.e == 0 && e == 0)
-    for (int64_t q = tid; q < (int64_t)b * s; q += kThreads)
-      P.dbg_l[(q / s) * s + sig[q % s]] = S.M[(int64_t)(s + q / s) * n + q % s];
+  if (P.dbg_l && eidx == 0 && e == 0)
+    for (int64_t q = tid; q < (int64_t)b * s; q += kThreads) P.dbg_l[(q / s) * s + sig[q % s]] = S.X[q];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) finish_kernel(SolveParams P, const Task* tasks, int nb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Task t = tasks[blockIdx.x];
+  const ElimDesc d = P.elims[t.e];
+  finish_body(P, t.e, d, blockIdx.y, nb, reinterpret_cast<int*>(smem_raw));
+}
+
+// ---- whole blocked LU of one elimination in one CTA (groups with many medium
+// eliminations): per 32-column panel the register panel step, the row
+// interchanges, the diagonal-block inverses, U12 / L21 DMMA tiles and the
+// trailing DMMA tiles (B x B block excluded); then X = Y L11^-1 and sigma.
+// Same arithmetic and data layout as the phase launches.
+constexpr int kFusedT = 256;
+__global__ void __launch_bounds__(kFusedT, 2) lu_fused_kernel(SolveParams P, const Task* tasks) {
+  constexpr int NB = 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  __shared__ PanelShared<NB, kFusedT> sh;
+  const int tid = threadIdx.x;
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, b = d.b;
+  const Scr S = scratch_of(P, d, e, NB);
+  double2* M = S.M;
+  const int steps = (s + NB - 1) / NB;
+  for (int j = 0; j < steps; ++j) {
+    const int j0 = j * NB, jb = min(NB, s - j0), j1 = j0 + jb;
+    panel_body<NB, kFusedT>(P, t.e, d, e, j, sh);
+    // row interchanges on the columns outside the panel (staged through smem)
+    const int nd = S.PERM[0];
+    if (nd > 0) {
+      const int other = n - jb;
+      const int cap = 4096 / nd;
+      for (int cb = 0; cb < other; cb += cap) {
+        const int cn = min(cap, other - cb);
+        for (int q = tid; q < nd * cn; q += kFusedT) {
+          const int k = q / cn, x = cb + q % cn;
+          const int col = x < j0 ? x : x + jb;
+          smem[q] = M[(int64_t)(j0 + S.PERM[1 + k]) * n + col];
+        }
+        __syncthreads();
+        for (int q = tid; q < nd * cn; q += kFusedT) {
+          const int k = q / cn, x = cb + q % cn;
+          const int col = x < j0 ? x : x + jb;
+          M[(int64_t)(j0 + S.PERM[1 + 2 * NB + k]) * n + col] = smem[q];
+        }
+        __syncthreads();
+      }
+    }
+    // inverses of the diagonal block
+    {
+      typedef double2 Row[NB + 1];
+      Row* Dm = reinterpret_cast<Row*>(smem);
+      Row* Xm = Dm + NB;
+      Row* Wm = Xm + NB;
+      for (int q = tid; q < NB * NB; q += kFusedT) {
+        const int r = q / NB, c = q % NB;
+        Dm[r][c] = (r < jb && c < jb) ? M[(int64_t)(j0 + r) * n + j0 + c] : cz();
+      }
+      __syncthreads();
+      for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 0) block_tri_inverse<NB, true>(Dm, jb, Xm, Wm);
+        else block_tri_inverse<NB, false>(Dm, jb, Xm, Wm);
+        double2* out = (pass == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
+        for (int q = tid; q < NB * NB; q += kFusedT) {
+          const int r = q / NB, c = q % NB;
+          out[q] = (r < jb && c < jb) ? Xm[r][c] : cz();
+        }
+        __syncthreads();
+      }
+    }
+    // U12 = L_jj^-1 A12 and L21 = A21 U_jj^-1
+    for (int c0 = j1; c0 < n; c0 += kTile) {
+      using TT = TrsmTiles<NB>::U;
+      double2* B = M + (int64_t)j0 * n + c0;
+      TT T;
+      T.zero();
+      T.mma(S.LINV + (int64_t)j * NB * NB, NB, B, n, jb, min(kTile, n - c0), jb, smem);
+      T.for_each([&](int r, int c, double2 v) {
+        if (r < jb && c0 + c < n) B[(int64_t)r * n + c] = v;
+      });
+      __syncthreads();
+    }
+    for (int r0 = s; r0 < n; r0 += kTile) {
+      using TT = TrsmTiles<NB>::L;
+      double2* A = M + (int64_t)r0 * n + j0;
+      TT T;
+      T.zero();
+      T.mma(A, n, S.UINV + (int64_t)j * NB * NB, NB, min(kTile, n - r0), jb, jb, smem);
+      T.for_each([&](int r, int c, double2 v) {
+        if (r0 + r < n && c < jb) A[(int64_t)r * n + c] = v;
+      });
+      __syncthreads();
+    }
+    // trailing update (the B x B block is left to the Schur launch)
+    for (int r0 = j1; r0 < n; r0 += kTile)
+      for (int c0 = j1; c0 < n; c0 += kTile) {
+        if (r0 >= s && c0 >= s) continue;
+        Tile64 T;
+        T.zero();
+        T.mma(M + (int64_t)r0 * n + j0, n, M + (int64_t)j0 * n + c0, n, min(kTile, n - r0), min(kTile, n - c0), jb,
+              smem);
+        T.for_each([&](int r, int c, double2 v) {
+          if (r0 + r < n && c0 + c < n && (r0 + r < s || c0 + c < s)) {
+            double2* p = M + (int64_t)(r0 + r) * n + c0 + c;
+            *p = csub(*p, v);
+          }
+        });
+        __syncthreads();
+      }
+  }
+  // X = Y L11^-1, block columns right to left
+  for (int j = steps - 1; j >= 0; --j)
+    for (int r0 = 0; r0 < b; r0 += kTile) xsolve_tile<NB>(S, n, s, j, r0, smem);
+  finish_body(P, t.e, d, e, NB, reinterpret_cast<int*>(smem));
 }
 
 // ---- T_S = MS[s:, :s] - X MS[:s, :s]   (the S columns of T = Sigma'_B: - X Sigma'_S:)
-__global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const Task* tasks) {
+__global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const Task* tasks, int nb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw);
   const Task t = tasks[blockIdx.x];
@@ -1097,7 +1425,8 @@ __global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const
   const int i0 = t.a * kTile, c0 = t.b * kTile;
   Tile64 T;
   T.zero();
-  T.mma(S.M + (int64_t)(s + i0) * n, n, S.MS + c0, n, min(kTile, b - i0), min(kTile, s - c0), s, smem);
+  const Scr SX = scratch_of(P, d, e, nb);
+  T.mma(SX.X + (int64_t)i0 * s, s, S.MS + c0, n, min(kTile, b - i0), min(kTile, s - c0), s, smem);
   T.for_each([&](int r, int c, double2 v) {
     if (i0 + r < b && c0 + c < s) {
       double2* p = S.MS + (int64_t)(s + i0 + r) * n + c0 + c;
@@ -1110,7 +1439,7 @@ __global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const
 // accumulator), stored sorted (or kept in MS for the final step).  Symmetric mode:
 // lower-triangle tiles only; the upper triangle is written as the (skew-)conjugate
 // mirror of elements (i >= j), so results stay deterministic.
-__global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const Task* tasks) {
+__global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const Task* tasks, int nb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw);
   const Task t = tasks[blockIdx.x];
@@ -1123,8 +1452,9 @@ __global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const
   const int mv = min(kTile, b - i0), nv = min(kTile, b - c0);
   Tile64 T;
   T.zero();
-  T.mma<false>(S.M + (int64_t)(s + i0) * n, n, S.MS + s + c0, n, mv, nv, s, smem);         // X Sigma'_SB
-  T.mma<true>(S.MS + (int64_t)(s + i0) * n, n, S.M + (int64_t)(s + c0) * n, n, mv, nv, s, smem);  // T_S X^H
+  const Scr SX = scratch_of(P, d, e, nb);
+  T.mma<false>(SX.X + (int64_t)i0 * s, s, S.MS + s + c0, n, mv, nv, s, smem);          // X Sigma'_SB
+  T.mma<true>(S.MS + (int64_t)(s + i0) * n, n, SX.X + (int64_t)c0 * s, s, mv, nv, s, smem);  // T_S X^H
   const bool store = d.kind != kFinal && d.out_arena >= 0;
   const bool mirror = store && P.rsym != 0;
   const double sg = P.rsym < 0 ? -1.0 : 1.0;
@@ -1208,7 +1538,7 @@ size_t ws_header_bytes() { return 256; }
 template <int NB>
 size_t xsolve_smem() {
   using TT = typename XTileSel<NB>::T;
-  return TT::SMEM + (size_t)(kTile * (NB + 1) + NB * (NB + 1)) * sizeof(double2);
+  return TT::SMEM;
 }
 
 template <int NB>
@@ -1222,6 +1552,7 @@ int set_attrs(find_status* st) {
   if (done) return FIND_OK;
   const int mx = (int)kMaxSmem;
   CUDA_TRY(cudaFuncSetAttribute(small_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(mid_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
 
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -1233,6 +1564,7 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(tgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(rgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(schur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(lu_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<32>()));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<16>()));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<8>()));
@@ -1305,13 +1637,27 @@ int run_groups(const find_plan* P, const SolveParams& prm, int64_t g_begin, int6
   return FIND_OK;
 }
 
+// Fused-LU launches (one CTA per elimination and energy) instead of the
+// level-batched phase launches: opt-in (FIND_B200_FUSED=1, for groups that fill
+// the GPU); measured slower than the phase launches once the mid path takes the
+// small eliminations (profiles/r01_*).
+bool use_fused(const LaunchGroup& G, int nE) {
+  if (G.fspec_end <= G.fspec_begin) return false;
+  static const int force = [] {
+    const char* f = std::getenv("FIND_B200_FUSED");
+    return f ? std::atoi(f) : 0;
+  }();
+  return force == 1 && (G.end - G.begin) * (int64_t)nE >= 2 * 148;
+}
+
 int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE, cudaStream_t stream,
                   find_status* st) {
   const Task* dtasks = (const Task*)P->d_tasks;
   {
     const LaunchGroup& G = P->groups[gi];
     if (G.path == 1 && G.nb == 0) return fail_status(st, FIND_EINVAL, "elimination block too large for this build");
-    for (int64_t si = G.spec_begin; si < G.spec_end; ++si) {
+    const bool fused = use_fused(G, nE);
+    for (int64_t si = fused ? G.fspec_begin : G.spec_begin; si < (fused ? G.fspec_end : G.spec_end); ++si) {
       const LaunchSpec& L = P->specs[si];
       if (!prm.compute_gless && (L.kind == kLGatherS || L.kind == kLTGemm)) continue;
       const Task* tk = dtasks + L.task_off;
@@ -1327,6 +1673,17 @@ int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE
           const size_t smem = (size_t)kSmallWarps * small_warp_elems(nmax, ld, xcap) * sizeof(double2);
           small_elim_kernel<<<dim3((unsigned)((L.task_count + kSmallWarps - 1) / kSmallWarps), (unsigned)nE),
                               kSmallWarps * 32, smem, stream>>>(p, L.task_count, nmax, ld, xcap);
+          break;
+        }
+        case kLMid: {
+          SolveParams p = prm;
+          p.elims = prm.elims + L.task_off;
+          p.elim_base = L.task_off;
+          const int nmax = std::max(1, G.max_n);
+          const int xcap = G.max_b * G.max_s + G.max_b * G.max_b;
+          const size_t smem = (size_t)mid_smem_elems(nmax, xcap) * sizeof(double2);
+          mid_elim_kernel<<<dim3((unsigned)L.task_count, (unsigned)nE), kMidThreads, smem, stream>>>(p, L.task_count, nmax,
+                                                                                                   xcap);
           break;
         }
         case kLGatherA: gather_kernel<false><<<grid, kThreads, 0, stream>>>(prm, tk); break;
@@ -1355,11 +1712,12 @@ int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE
           else xsolve_kernel<8><<<grid, kThreads, xsolve_smem<8>(), stream>>>(prm, tk, L.step);
           break;
         case kLFinish:
-          finish_kernel<<<grid, kThreads, std::max<size_t>((size_t)G.max_s * sizeof(int), 16), stream>>>(prm, tk);
+          finish_kernel<<<grid, kThreads, std::max<size_t>((size_t)G.max_s * sizeof(int), 16), stream>>>(prm, tk, L.nb);
           break;
-        case kLTGemm: tgemm_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk); break;
-        case kLRGemm: rgemm_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk); break;
+        case kLTGemm: tgemm_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk, L.nb); break;
+        case kLRGemm: rgemm_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk, L.nb); break;
         case kLSchur: schur_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk); break;
+        case kLLuFused: lu_fused_kernel<<<grid, kFusedT, Tile64::SMEM, stream>>>(prm, tk); break;
         case kLFinal: {
           const int cmax = std::max(1, G.max_b);
           const size_t smem = (size_t)kSmallWarps * 2 * cmax * (cmax + 1) * sizeof(double2);
@@ -1440,7 +1798,12 @@ size_t find_solve_workspace_bytes(const find_plan* P, int32_t nE, int32_t comput
   return b;
 }
 
-int64_t find_solve_launch_count(const find_plan* P) { return P ? (int64_t)P->specs.size() : 0; }
+int64_t find_solve_launch_count(const find_plan* P, int32_t nE) {
+  if (!P) return 0;
+  int64_t k = 0;
+  for (const LaunchGroup& G : P->groups) k += use_fused(G, nE) ? G.fspec_end - G.fspec_begin : G.spec_end - G.spec_begin;
+  return k;
+}
 
 int find_solve_groups(find_plan* P, const void* a_vals, const void* s_vals, int32_t s_broadcast, int32_t nE,
                       int32_t compute_gless, double rtol, void* gr_out, void* gl_out, void* ws, size_t ws_bytes,
@@ -1491,13 +1854,17 @@ int find_plan_groups(const find_plan* P, int32_t* pass, int32_t* level, int32_t*
   return FIND_OK;
 }
 
-int find_plan_specs(const find_plan* P, int32_t* kind, int32_t* step, int32_t* group, int64_t* tasks) {
+int find_plan_specs(const find_plan* P, int32_t nE, int32_t* kind, int32_t* step, int32_t* group, int64_t* tasks) {
   if (!P) return FIND_EINVAL;
-  for (size_t i = 0; i < P->specs.size(); ++i) {
-    if (kind) kind[i] = P->specs[i].kind;
-    if (step) step[i] = P->specs[i].step;
-    if (group) group[i] = P->specs[i].group;
-    if (tasks) tasks[i] = P->specs[i].task_count;
+  int64_t i = 0;
+  for (const LaunchGroup& G : P->groups) {
+    const bool f = use_fused(G, nE);
+    for (int64_t si = f ? G.fspec_begin : G.spec_begin; si < (f ? G.fspec_end : G.spec_end); ++si, ++i) {
+      if (kind) kind[i] = P->specs[si].kind;
+      if (step) step[i] = P->specs[si].step;
+      if (group) group[i] = P->specs[si].group;
+      if (tasks) tasks[i] = P->specs[si].task_count;
+    }
   }
   return FIND_OK;
 }
@@ -1544,8 +1911,9 @@ int find_schur_sigma_update(int32_t s, int32_t b, const void* ass, const void* a
   const int n = s + b;
   const bool gless = (r_out != nullptr || b == 0) && (s == 0 || sss) && (s == 0 || b == 0 || (ssb && sbs)) &&
                      (b == 0 || sbb);
-  int path = force_path >= 0 ? force_path : (n <= 32 ? 0 : 1);
+  int path = force_path >= 0 ? force_path : (n <= 32 ? 0 : (n <= kMidMaxN ? 2 : 1));
   if (path == 0 && n > 32) path = 1;
+  if (path == 2 && n > kMidMaxN) path = 1;
   // a one-elimination plan: left block = [[ass, asb], [abs, abb]] (+ Sigma), identity maps
   find_plan Q;
   Q.n = n;

@@ -47,7 +47,7 @@ void set_status(find_status* st, int code, const char* msg) {
 // Must match scratch_of() in find_solve.cu.
 int64_t find_scratch_elems(int64_t n, int64_t s, int nb) {
   int64_t e = 2 * n * n + (3 * s + 132 + 3) / 4 + 1 + (n + 31) / 32;
-  if (nb > 0) e += 2 * ((s + nb - 1) / nb) * (int64_t)nb * nb;
+  if (nb > 0) e += 2 * ((s + nb - 1) / nb) * (int64_t)nb * nb + (n - s) * s;  // + X [b][s]
   return (e + 1) & ~int64_t(1);
 }
 
@@ -91,9 +91,10 @@ void find_build_tasks(find_plan* P) {
   for (int32_t gi = 0; gi < (int32_t)P->groups.size(); ++gi) {
     LaunchGroup& G = P->groups[gi];
     G.spec_begin = (int64_t)P->specs.size();
-    if (G.path == 0) {
+    G.fspec_begin = G.fspec_end = 0;
+    if (G.path == 0 || G.path == 2) {
       LaunchSpec L;
-      L.kind = kLSmall; L.step = 0; L.nb = 0; L.group = gi;
+      L.kind = G.path == 0 ? kLSmall : kLMid; L.step = 0; L.nb = 0; L.group = gi;
       L.task_off = G.begin; L.task_count = G.end - G.begin;
       P->specs.push_back(L);
       G.spec_end = (int64_t)P->specs.size();
@@ -188,12 +189,34 @@ void find_build_tasks(find_plan* P) {
       if (P->elims[e].kind == kFinal) push((int32_t)e, 0, 0, 0);
     spec(kLFinal, 0, nb, gi, off);
     G.spec_end = (int64_t)P->specs.size();
+    // fused alternative: gatherA, fused LU (+X, sigma), then the same tail launches
+    G.fspec_begin = G.fspec_end = (int64_t)P->specs.size();
+    if (nb == 32 && G.max_s <= 256) {
+      std::vector<LaunchSpec> tail;
+      LaunchSpec ga{};
+      for (int64_t si = G.spec_begin; si < G.spec_end; ++si) {
+        const LaunchSpec& L = P->specs[si];
+        if (L.kind == kLGatherA) ga = L;
+        if (L.kind == kLSchur || L.kind == kLGatherS || L.kind == kLTGemm || L.kind == kLRGemm || L.kind == kLFinal)
+          tail.push_back(L);
+      }
+      off = (int64_t)P->tasks.size();
+      for (int64_t e = G.begin; e < G.end; ++e) push((int32_t)e, 0, 0, 0);
+      LaunchSpec lu{};
+      lu.kind = kLLuFused; lu.step = 0; lu.nb = nb; lu.group = gi;
+      lu.task_off = off; lu.task_count = (int64_t)P->tasks.size() - off;
+      P->specs.push_back(ga);
+      P->specs.push_back(lu);
+      for (const LaunchSpec& L : tail) P->specs.push_back(L);
+      G.fspec_end = (int64_t)P->specs.size();
+    }
   }
 }
 
 namespace {
 
 constexpr int32_t kSmallMaxN = 32;  // warp-per-elimination path up to this merged size
+constexpr int32_t kMidMaxN = 64;    // CTA-per-elimination shared-memory path up to this merged size
 
 struct Builder {
   find_plan* P;
@@ -459,6 +482,7 @@ struct Builder {
       if (end == begin) return;
       auto cls = [](const ElimDesc& d) -> int {
         if (d.n <= kSmallMaxN) return 0;
+        if (d.n <= kMidMaxN) return 5;
         if (d.s <= 64) return 1;
         if (d.s <= 128) return 2;
         if (d.s <= 256) return 3;
@@ -473,7 +497,7 @@ struct Builder {
         const int c = cls(P->elims[gb]);
         int64_t ge = gb;
         while (ge < end && cls(P->elims[ge]) == c) ++ge;
-        const int path = c == 0 ? 0 : 1;
+        const int path = c == 0 ? 0 : (c == 5 ? 2 : 1);
         LaunchGroup G;
         std::memset(&G, 0, sizeof(G));
         G.begin = gb; G.end = ge; G.path = path; G.pass = pass; G.level = level;

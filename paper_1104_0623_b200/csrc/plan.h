@@ -51,6 +51,8 @@ enum LaunchKind : int32_t {
   kLRGemm = 9,     // R = S_BB - X S_SB - T_S X^H (+ store)     tasks {e, tm, tn, sym-skip}
   kLFinal = 10,    // leaf inverse + G^< sandwich               tasks {e}
   kLSchur = 11,    // U = A_BB - Y U12 (K = s), stored sorted  tasks {e, tm, tn}
+  kLLuFused = 12,  // whole blocked LU + X + sigma in one CTA    tasks {e}
+  kLMid = 13,      // CTA-per-elimination smem kernel (32 < s+b <= 64)
 };
 
 struct Task { int32_t e, a, b, c; };
@@ -80,14 +82,15 @@ constexpr int kRowChunk = 16;   // gather rows per CTA
 
 struct LaunchGroup {
   int64_t begin, end;  // ElimDesc range
-  int32_t path;        // 0 = warp-per-elimination small path, 1 = CTA blocked path
+  int32_t path;        // 0 = warp-per-elimination, 1 = blocked (phase launches), 2 = CTA-per-elimination smem
   int32_t pass;        // 0 up, 1 down, 2 final
   int32_t level;
   int32_t max_n, max_s, max_b;
   int64_t ws_elems;    // scratch per energy used by this group
   int32_t nb;          // panel width of the CTA path (0: unsupported size)
   int32_t phase;       // groups of one phase are independent and run concurrently
-  int64_t spec_begin, spec_end;  // launches of this group
+  int64_t spec_begin, spec_end;    // launches of this group (level-batched phase launches)
+  int64_t fspec_begin, fspec_end;  // alternative with one fused-LU CTA per elimination (empty if n/a)
 };
 
 struct SparseEntry {  // merged (row, col) <- csr value slot

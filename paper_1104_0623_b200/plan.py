@@ -125,17 +125,19 @@ class Plan:
     def workspace_bytes(self, n_energies: int, compute_gless: bool = True) -> int:
         return int(_native.lib().find_solve_workspace_bytes(self._h, n_energies, int(compute_gless)))
 
-    def launch_count(self) -> int:
-        return int(_native.lib().find_solve_launch_count(self._h))
+    def launch_count(self, n_energies: int = 1) -> int:
+        return int(_native.lib().find_solve_launch_count(self._h, int(n_energies)))
 
-    KIND_NAMES = ("warp", "gatherA", "panel", "trsm", "trail", "xsolve", "finish", "gatherS", "tgemm", "rgemm", "final")
+    KIND_NAMES = ("warp", "gatherA", "panel", "trsm", "trail", "xsolve", "finish", "gatherS", "tgemm", "rgemm", "final",
+                  "schur", "lu_fused")
 
-    def specs(self) -> dict:
-        """Kernel-launch table in issue order: kind, step, group, task count."""
-        k = self.launch_count()
+    def specs(self, n_energies: int = 1) -> dict:
+        """Kernel-launch table of a solve over n_energies points, in issue order."""
+        k = self.launch_count(n_energies)
         out = {x: np.zeros(k, np.int32) for x in ("kind", "step", "group")}
         tasks = np.zeros(k, np.int64)
-        _native.lib().find_plan_specs(self._h, _i32p(out["kind"]), _i32p(out["step"]), _i32p(out["group"]), _i64p(tasks))
+        _native.lib().find_plan_specs(self._h, int(n_energies), _i32p(out["kind"]), _i32p(out["step"]),
+                                      _i32p(out["group"]), _i64p(tasks))
         out["tasks"] = tasks
         return out
 

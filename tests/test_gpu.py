@@ -56,7 +56,7 @@ def ref_update(ass, asb, abs_, abb, sss, ssb, sbs, sbb):
     return u, r, l
 
 
-@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("path", [0, 1, 2])
 def test_shim_scalar_case(cuda, path):
     # test_kernels.py:51-60: U = 2.5, L = 0.5 exactly
     rc, st, u, r, l = shim(np.array([[2.0]]), np.array([[1.0]]), np.array([[1.0]]), np.array([[3.0]]), path=path)
@@ -64,7 +64,7 @@ def test_shim_scalar_case(cuda, path):
     assert u[0, 0] == 2.5 and l[0, 0] == 0.5
 
 
-@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("path", [0, 1, 2])
 def test_shim_identity_pivot(cuda, path):
     # test_kernels.py:39-48
     abs_ = np.random.default_rng(0).standard_normal((3, 2)).astype(complex)
@@ -74,14 +74,14 @@ def test_shim_identity_pivot(cuda, path):
     assert np.array_equal(u, abb) and np.array_equal(l, abs_)
 
 
-@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("path", [0, 1, 2])
 def test_shim_singular_pivot_position(cuda, path):
     # test_kernels.py:80-91: zero A(S,S) fails at position 0 (node = s_labels[0])
     rc, st, *_ = shim(np.zeros((2, 2)), np.zeros((2, 1)), np.zeros((1, 2)), np.eye(1), path=path)
     assert rc == 2 and st.node_id == 0
 
 
-@pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("path", [0, 1, 2])
 def test_shim_sigma_scalar_expansion(cuda, path):
     # test_kernels.py:102-106: R = 1 + |l|^2 for S = I, L = l
     lv = 0.5 + 0.5j
@@ -90,7 +90,8 @@ def test_shim_sigma_scalar_expansion(cuda, path):
     assert rc == 0 and np.isclose(r[0, 0], 1 + abs(lv) ** 2)
 
 
-@pytest.mark.parametrize("s,b,path", [(2, 4, 0), (7, 3, 0), (16, 16, 0), (20, 12, 0), (7, 3, 1), (30, 40, 1),
+@pytest.mark.parametrize("s,b,path", [(2, 4, 0), (7, 3, 0), (16, 16, 0), (20, 12, 0), (7, 3, 2), (20, 16, 2),
+                                      (40, 24, 2), (1, 50, 2), (60, 2, 2), (0, 40, 2), (64, 0, 2), (7, 3, 1), (30, 40, 1),
                                       (64, 33, 1), (100, 90, 1), (257, 194, 1), (300, 5, 1), (0, 9, 1), (9, 0, 1),
                                       (500, 120, 1), (33, 1, 1)])
 def test_shim_dense_vs_numpy(cuda, s, b, path):
@@ -114,6 +115,16 @@ def test_shim_pivoting_needed(cuda):
     s, b = 70, 20
     ass, asb, abs_, abb = dense_input(s, b, seed=5, shift=0.0)
     ass[np.arange(s), np.arange(s)] = 0.0
+    for path in (1,):
+        rc, st, u, r, l = shim(ass, asb, abs_, abb, path=path)
+        ue, _, le = ref_update(ass, asb, abs_, abb, np.eye(s), np.zeros((s, b)), np.zeros((b, s)), np.eye(b))
+        assert rc == 0 and rel(u, ue) < 1e-10 and rel(l, le) < 1e-10
+    ass3, asb3, abs3, abb3 = dense_input(40, 20, seed=9, shift=0.0)
+    ass3[np.arange(40), np.arange(40)] = 0.0
+    for path in (2, 1):
+        rc, st, u, r, l = shim(ass3, asb3, abs3, abb3, path=path)
+        ue, _, le = ref_update(ass3, asb3, abs3, abb3, np.eye(40), np.zeros((40, 20)), np.zeros((20, 40)), np.eye(20))
+        assert rc == 0 and rel(u, ue) < 1e-10 and rel(l, le) < 1e-10
     for path in (1,):
         rc, st, u, r, l = shim(ass, asb, abs_, abb, path=path)
         assert rc == 0

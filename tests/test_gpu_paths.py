@@ -1,0 +1,50 @@
+"""Both CTA-path variants (level-batched phase launches and the fused per-elimination
+LU) against the reference's golden outputs, selected through FIND_B200_FUSED in a
+fresh process (the choice is read once per process)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import json, sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import numpy as np
+from conftest import load_golden, problem_from_golden, stencil_ops
+from paper_1104_0623_b200 import Mesh, SolverConfig, SparseOperator, solve, solve_batch
+out = {{}}
+for name in ("cfg0", "c5_16x12", "c9_20x20", "c5_8x30"):
+    g = load_golden(name); p = problem_from_golden(g)
+    ops = [SparseOperator(p.a_csr(k)) for k in range(p.energies.size)]
+    r = solve_batch(Mesh(p.nx, p.ny), ops, SparseOperator(p.sigma_csr()), SolverConfig())
+    out[name] = [float(np.max(np.abs(r.gr_diag - g["gr"])) / np.max(np.abs(g["gr"]))),
+                 float(np.max(np.abs(r.gless_diag - g["gl"])) / np.max(np.abs(g["gl"])))]
+for name in ("stencil_16x16", "stencil_8x8"):
+    g = load_golden(name); mesh, a, s = stencil_ops(g)
+    r = solve(mesh, a, s, SolverConfig(leaf_max=2))
+    out[name] = [float(np.max(np.abs(r.gr_diag - g["gr_2"])) / np.max(np.abs(g["gr_2"]))),
+                 float(np.max(np.abs(r.gless_diag - g["gl_2"])) / np.max(np.abs(g["gl_2"])))]
+print("RESULT", json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [{"FIND_B200_FUSED": "1"}, {"FIND_B200_FUSED": "0"},
+                                 {"FIND_B200_FUSED": "0", "FIND_B200_NB": "16"},
+                                 {"FIND_B200_FUSED": "0", "FIND_B200_NB": "8"},
+                                 {"FIND_B200_FUSED": "0", "FIND_B200_SMEM_PANEL": "1"}])
+def test_cta_path_variants_match_golden(cuda, env):
+    code = SCRIPT.format(root=str(ROOT), tests=str(ROOT / "tests"))
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("RESULT")][-1]
+    res = json.loads(line[len("RESULT "):])
+    for name, (egr, egl) in res.items():
+        assert egr < 1e-10 and egl < 1e-10, (name, egr, egl, env)

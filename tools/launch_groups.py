@@ -18,7 +18,7 @@ from paper_1104_0623_b200.plan import Plan  # noqa: E402
 cfg = int(sys.argv[sys.argv.index("--config") + 1]) if "--config" in sys.argv else 1
 p = config_problem(cfg, 1)
 plan = Plan(p.nx, p.ny, p.indptr, p.indices)
-sp = plan.specs()
+sp = plan.specs(int(sys.argv[sys.argv.index("--energies") + 1]) if "--energies" in sys.argv else 16)
 L = len(sp["kind"])
 data = load(sys.argv[1])
 data = data[len(data) - L:]

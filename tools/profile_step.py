@@ -30,4 +30,4 @@ for _ in range(a.reps):
     plan.run(ad, sd, gr, gl, ws=ws, sigma_sym=-1)
 plan.check_status(ws, p.energies.size)
 torch.cuda.synchronize()
-print("launches per solve", plan.launch_count())
+print("launches per solve", plan.launch_count(p.energies.size))
