@@ -111,8 +111,9 @@ int find_plan_upload(find_plan* plan, find_status* st);
  *   gl_out   device, [n_energies][n] complex128  diag(G^<) (NULL if !compute_gless)
  *   compute_gless  0: diag(G^r) only; 1: also diag(G^<); 2 / 3: also diag(G^<)
  *            and Sigma^< is Hermitian / skew-Hermitian (e.g. i*Gamma), so every
- *            R block is too and only its lower triangle is computed (the
- *            upper one is mirrored) -- the paper's symmetry saving for R
+ *            R block is too; the upward pass then computes only the lower
+ *            triangle of each R and mirrors it (the paper's symmetry saving
+ *            for R; the downward pass keeps the general product)
  *   ws       device workspace of >= find_solve_workspace_bytes()
  *   stream   cudaStream_t
  * Stream-ordered; on return the work is enqueued.  Call find_solve_status()

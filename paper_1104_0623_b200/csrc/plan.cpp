@@ -61,9 +61,10 @@ void find_assign_phases(find_plan* P) {
   int64_t base = 0;
   P->ws_elems = 0;
   for (auto& G : P->groups) {
-    // key of the phase this group belongs to
+    // key of the phase this group belongs to; a phase whose scratch would exceed
+    // the cap is continued as a new (sequential) phase
     int32_t key = G.pass == 0 ? -1000 - G.level : (G.pass == 1 ? G.level : G.level + 1);
-    if (key != cur_key) {
+    if (key != cur_key || (G.path == 1 && base > 0 && base + G.ws_elems > kGroupScratchCap)) {
       ++phase;
       cur_key = key;
       base = 0;
@@ -498,6 +499,18 @@ struct Builder {
         int64_t ge = gb;
         while (ge < end && cls(P->elims[ge]) == c) ++ge;
         const int path = c == 0 ? 0 : (c == 5 ? 2 : 1);
+        if (path == 1) {  // bound the scratch of one group (sub-batches run one after another)
+          int32_t ms = 0;
+          for (int64_t k = gb; k < ge; ++k) ms = std::max(ms, P->elims[k].s);
+          const int nbc = pick_nb_host(ms);
+          int64_t acc = 0, k = gb;
+          for (; k < ge; ++k) {
+            const int64_t w = find_scratch_elems(P->elims[k].n, P->elims[k].s, nbc);
+            if (k > gb && acc + w > kGroupScratchCap) break;
+            acc += w;
+          }
+          ge = k;
+        }
         LaunchGroup G;
         std::memset(&G, 0, sizeof(G));
         G.begin = gb; G.end = ge; G.path = path; G.pass = pass; G.level = level;

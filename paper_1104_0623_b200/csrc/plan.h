@@ -69,15 +69,17 @@ inline int pick_nb_host(int64_t max_s) {
   if (const char* f = std::getenv("FIND_B200_NB")) {  // test hook: force the panel width
     const int nb = std::atoi(f);
     if ((nb == 32 && max_s <= 256) || (nb == 16 && max_s * 17 * 16 <= 220 * 1024) ||
-        (nb == 8 && max_s * 9 * 16 <= 220 * 1024))
+        (nb == 8 && max_s * 9 * 16 <= 220 * 1024) || (nb == 4 && max_s * 5 * 16 <= 220 * 1024))
       return nb;
   }
   if (max_s <= 256) return 32;
   if (max_s * 17 * 16 <= 220 * 1024) return 16;
   if (max_s * 9 * 16 <= 220 * 1024) return 8;
+  if (max_s * 5 * 16 <= 220 * 1024) return 4;
   return 0;
 }
 constexpr int kTile = 64;       // DMMA output tile edge
+constexpr int64_t kGroupScratchCap = int64_t(1) << 28;  // complex elements of CTA-path scratch per energy per phase (4 GiB)
 constexpr int kRowChunk = 16;   // gather rows per CTA
 
 struct LaunchGroup {

@@ -129,7 +129,7 @@ class Plan:
         return int(_native.lib().find_solve_launch_count(self._h, int(n_energies)))
 
     KIND_NAMES = ("warp", "gatherA", "panel", "trsm", "trail", "xsolve", "finish", "gatherS", "tgemm", "rgemm", "final",
-                  "schur", "lu_fused")
+                  "schur", "lu_fused", "mid")
 
     def specs(self, n_energies: int = 1) -> dict:
         """Kernel-launch table of a solve over n_energies points, in issue order."""

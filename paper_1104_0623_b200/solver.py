@@ -134,38 +134,61 @@ def _device():
 
 
 def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, compute_gless=True, pivot_rtol=1e-12,
-                 sigma_sym=0):
+                 sigma_sym=0, max_chunk: int | None = None):
     """Run the plan on host value arrays a_vals [nE, nnz], s_vals [nnz] or [nE, nnz].
 
-    Host -> device copies, the level-batched kernels, status check and the
-    device -> host copy of the diagonals.  Returns (gr, gl, device_seconds_up, device_seconds_down)."""
+    Energy points are processed in chunks sized to the free device memory (one
+    find_solve per chunk); per chunk: host -> device copies, the level-batched
+    kernels, status check, device -> host copy of the diagonals.
+    Returns (gr, gl, device_seconds_up, device_seconds_down)."""
     import torch
 
     dev = _device()
     a_vals = np.ascontiguousarray(np.atleast_2d(a_vals), dtype=np.complex128)
     n_e = a_vals.shape[0]
-    stream = torch.cuda.current_stream(dev)
-    a_d = torch.from_numpy(a_vals).to(dev, non_blocking=False)
-    s_d = None
     s_b = True
     if compute_gless:
         s_vals = np.ascontiguousarray(s_vals, dtype=np.complex128)
         s_b = s_vals.ndim == 1
-        s_d = torch.from_numpy(s_vals).to(dev)
-    gr_d = torch.empty((n_e, plan.n), dtype=torch.complex128, device=dev)
-    gl_d = torch.empty((n_e, plan.n), dtype=torch.complex128, device=dev) if compute_gless else None
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    ev[0].record(stream)
-    ws = plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, stream=stream,
-                  groups=(0, plan.first_down_group), sigma_sym=sigma_sym)
-    ev[1].record(stream)
-    plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, ws=ws, stream=stream,
-             groups=(plan.first_down_group, -1), sigma_sym=sigma_sym)
-    ev[2].record(stream)
-    plan.check_status(ws, n_e, stream)
-    gr = gr_d.cpu().numpy()
-    gl = gl_d.cpu().numpy() if gl_d is not None else None
-    return gr, gl, ev[0].elapsed_time(ev[1]) * 1e-3, ev[1].elapsed_time(ev[2]) * 1e-3
+    per_energy = plan.workspace_bytes(2, compute_gless) - plan.workspace_bytes(1, compute_gless)
+    per_energy += (plan.nnz + 2 * plan.n) * 16
+    free, _ = torch.cuda.mem_get_info(dev)
+    held = plan._ws.numel() if plan._ws is not None and plan._ws.device == dev else 0
+    chunk = max(1, min(n_e, int((0.85 * (free + held) - plan.workspace_bytes(1, compute_gless) + per_energy) // per_energy)))
+    if max_chunk:
+        chunk = min(chunk, max_chunk)
+    stream = torch.cuda.current_stream(dev)
+    gr = np.empty((n_e, plan.n), np.complex128)
+    gl = np.empty((n_e, plan.n), np.complex128) if compute_gless else None
+    s_all = torch.from_numpy(s_vals).to(dev) if (compute_gless and s_b) else None
+    t_up = t_down = 0.0
+    for k0 in range(0, n_e, chunk):
+        k1 = min(n_e, k0 + chunk)
+        a_d = torch.from_numpy(a_vals[k0:k1]).to(dev)
+        s_d = s_all if s_b else (torch.from_numpy(s_vals[k0:k1]).to(dev) if compute_gless else None)
+        gr_d = torch.empty((k1 - k0, plan.n), dtype=torch.complex128, device=dev)
+        gl_d = torch.empty((k1 - k0, plan.n), dtype=torch.complex128, device=dev) if compute_gless else None
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        ws = plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, stream=stream,
+                      groups=(0, plan.first_down_group), sigma_sym=sigma_sym)
+        ev[1].record(stream)
+        plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, ws=ws, stream=stream,
+                 groups=(plan.first_down_group, -1), sigma_sym=sigma_sym)
+        ev[2].record(stream)
+        try:
+            plan.check_status(ws, k1 - k0, stream)
+        except Exception as exc:
+            if hasattr(exc, "energy") and exc.energy is not None:
+                exc.energy += k0
+            raise
+        gr[k0:k1] = gr_d.cpu().numpy()
+        if compute_gless:
+            gl[k0:k1] = gl_d.cpu().numpy()
+        t_up += ev[0].elapsed_time(ev[1]) * 1e-3
+        t_down += ev[1].elapsed_time(ev[2]) * 1e-3
+        del a_d, gr_d, gl_d
+    return gr, gl, t_up, t_down
 
 
 def _stats(plan: Plan, a_data: np.ndarray) -> dict:

@@ -279,3 +279,27 @@ def test_symmetric_r_mode_matches_general(cuda):
     assert rel(gl1, gl0) < 1e-13
     for k in range(p.energies.size):
         assert rel(gl1[k], g["gl"][k]) < TOL
+
+
+def test_tall_mesh_gless_against_sparse_lu(cuda):
+    """Deep downward pass (128 x 512, V ~ U[-1,1]): diag(G^<) against independent
+    sparse-LU solves; guards the symmetric-R mode against drift over many levels."""
+    import scipy.sparse.linalg as spla
+
+    from paper_1104_0623_b200.configs import build_problem
+    from paper_1104_0623_b200.plan import plan_for
+    from paper_1104_0623_b200.solver import sigma_symmetry, solve_values
+
+    p = build_problem(128, 512, [1.7], seed=3, stencil=5, vamp=1.0)
+    plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
+    gr, gl, _, _ = solve_values(plan, p.a_vals_all(), p.s_vals, sigma_sym=sigma_symmetry(p.sigma_csr()))
+    assert np.max(np.abs(gl.real)) < 1e-10 * np.max(np.abs(gl))
+    lu = spla.splu(p.a_csr(0).conj().T.tocsc())
+    sig = p.sigma_csr()
+    rng = np.random.default_rng(1)
+    for i in list(rng.choice(p.n, 10, replace=False)) + [0, p.n - 1]:
+        e = np.zeros(p.n, complex)
+        e[i] = 1.0
+        x = lu.solve(e)
+        assert abs(gr[0, i] - np.conj(x[i])) < 1e-10 * np.max(np.abs(gr[0]))
+        assert abs(gl[0, i] - np.vdot(x, sig @ x)) < 1e-10 * np.max(np.abs(gl[0]))
