@@ -303,3 +303,32 @@ def test_tall_mesh_gless_against_sparse_lu(cuda):
         x = lu.solve(e)
         assert abs(gr[0, i] - np.conj(x[i])) < 1e-10 * np.max(np.abs(gr[0]))
         assert abs(gl[0, i] - np.vdot(x, sig @ x)) < 1e-10 * np.max(np.abs(gl[0]))
+
+
+@pytest.mark.parametrize("cfg,n_e,nodes", [(2, 8, 8), (3, 4, 8), (4, 1, 4)])
+def test_full_scale_configs_against_sparse_lu(cuda, cfg, n_e, nodes):
+    """BASELINE configs 2-4 at full mesh size (a subset of their energy points):
+    independent sparse-LU spot checks of diag(G^r), diag(G^<) and their sign structure."""
+    import scipy.sparse.linalg as spla
+
+    from paper_1104_0623_b200.configs import CONFIGS, build_problem
+    from paper_1104_0623_b200.plan import plan_for
+    from paper_1104_0623_b200.solver import sigma_symmetry, solve_values
+
+    c = CONFIGS[cfg]
+    energies = np.asarray(c.energies)[np.unique(np.linspace(0, len(c.energies) - 1, n_e).round().astype(int))]
+    p = build_problem(c.nx, c.ny, energies, seed=cfg, stencil=c.stencil, vamp=c.vamp)
+    plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
+    gr, gl, _, _ = solve_values(plan, p.a_vals_all(), p.s_vals, sigma_sym=sigma_symmetry(p.sigma_csr()))
+    assert np.all(gr.imag < 0)
+    assert np.max(np.abs(gl.real)) < 1e-10 * np.max(np.abs(gl))
+    sig = p.sigma_csr()
+    rng = np.random.default_rng(cfg)
+    for k in sorted({0, p.energies.size - 1}):
+        lu = spla.splu(p.a_csr(k).conj().T.tocsc())
+        for i in list(rng.choice(p.n, nodes, replace=False)) + [0, p.n - 1]:
+            e = np.zeros(p.n, complex)
+            e[i] = 1.0
+            x = lu.solve(e)
+            assert abs(gr[k, i] - np.conj(x[i])) < 1e-10 * np.max(np.abs(gr[k]))
+            assert abs(gl[k, i] - np.vdot(x, sig @ x)) < 1e-10 * np.max(np.abs(gl[k]))
