@@ -178,7 +178,7 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def group_work(plan):
+def _unused_group_work(plan):
     """Algorithmic work (paper ledger, complex mults) per launch group, one energy point."""
     from paper_1104_0623_b200.ledger import plan_ledger
 
@@ -258,39 +258,54 @@ def run_b200(args):
     ms_per_step = dev_ms / args.steps
     value = world * n_e * args.steps / (dev_ms * 1e-3)
 
-    # ---- per-launch-group timing (one extra instrumented step) -> roofline of the dominant kernel ----
-    ng = len(plan.groups["count"])
-    gev = [torch.cuda.Event(enable_timing=True) for _ in range(ng + 1)]
+    # ---- per-launch timing (one extra instrumented step, library CUDA events around every launch)
+    #      -> roofline of the dominant kernel kind, live
+    import ctypes as C
+
+    from paper_1104_0623_b200 import _native
+    from paper_1104_0623_b200.workmodel import KINDS, TENSOR_KINDS, executed_cmacs
+
+    lib = _native.lib()
     with torch.cuda.stream(stream):
         flush.fill_(1)
-        gev[0].record(stream)
-        for g in range(ng):
-            plan.run(a_d, s_d, gr_d, gl_d, ws=ws, stream=stream, groups=(g, g + 1), sigma_sym=ssym)
-            gev[g + 1].record(stream)
-    torch.cuda.synchronize()
-    gms = np.array([gev[g].elapsed_time(gev[g + 1]) for g in range(ng)])
-    gw = group_work(plan) * n_e  # complex mults per launch (all energies)
-    path = plan.groups["path"]
-    kern = {0: "small_elim_kernel", 1: "cta_elim_kernel"}
-    tot = {k: float(gms[path == k].sum()) for k in (0, 1)}
-    dom = max(tot, key=tot.get)
-    sel = path == dom
-    achieved = 8.0 * gw[sel].sum() / (gms[sel].sum() * 1e-3) / 1e12
+        torch.cuda.synchronize()
+        lib.find_solve_timing_enable(1)
+        step()
+        torch.cuda.synchronize()
+        lib.find_solve_timing_enable(0)
+    nl = int(lib.find_solve_timing_read(None, None, None, 0))
+    kk = (C.c_int32 * nl)()
+    gg = (C.c_int32 * nl)()
+    ms = (C.c_float * nl)()
+    lib.find_solve_timing_read(kk, gg, ms, nl)
+    work = executed_cmacs(plan, ssym)
+    per_kind = {}
+    for i in range(nl):
+        name = KINDS[kk[i]]
+        d = per_kind.setdefault(name, {"ms": 0.0, "launches": 0, "cmacs": 0.0, "groups": set()})
+        d["ms"] += ms[i]
+        d["launches"] += 1
+        d["groups"].add(gg[i])
+    for name, d in per_kind.items():
+        d["cmacs"] = sum(work.get((gi, name), 0.0) for gi in d["groups"]) * n_e
+    tot_ms = sum(d["ms"] for d in per_kind.values())
+    kernels = {name: {"ms_per_step": round(d["ms"], 3), "share": round(d["ms"] / tot_ms, 4), "launches": d["launches"],
+                      "tflops": (round(8 * d["cmacs"] / (d["ms"] * 1e-3) / 1e12, 3) if d["cmacs"] and d["ms"] else None)}
+               for name, d in sorted(per_kind.items(), key=lambda kv: -kv[1]["ms"])}
+    dom = max((k for k in per_kind if k in TENSOR_KINDS), key=lambda k: per_kind[k]["ms"])
+    dk = per_kind[dom]
+    achieved = 8 * dk["cmacs"] / (dk["ms"] * 1e-3) / 1e12
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-        "kernel": kern[dom], "launches_per_step": int(sel.sum()),
-        "share_of_step": float(gms[sel].sum() / gms.sum()),
+        "kernel": f"{dom}_kernel", "launches_per_step": dk["launches"], "share_of_step": dk["ms"] / tot_ms,
         "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_fp64_probe.txt); cuBLAS ZGEMM 37.02",
-        "work": "8 x reference ledger W (naive, kernels.py:90-91) of the eliminations in those launches",
+        "work": "executed complex MACs x 8 of those launches (paper_1104_0623_b200/workmodel.py), ÷ their summed "
+                "CUDA-event durations in one instrumented step (concurrent streams: durations overlap)",
     }
     if args.levels and rank == 0:
-        rows = []
-        for g in range(ng):
-            rows.append({k: (int(v[g]) if k != "count" else int(v[g])) for k, v in plan.groups.items()} |
-                        {"ms": float(gms[g]), "mults": float(gw[g]),
-                         "tflops": float(8 * gw[g] / (gms[g] * 1e-3) / 1e12) if gms[g] > 0 else 0.0})
-        Path(args.levels).write_text(json.dumps(rows, indent=1))
+        Path(args.levels).write_text(json.dumps({"kernels": kernels, "launches": [
+            {"kind": KINDS[kk[i]], "group": int(gg[i]), "ms": float(ms[i])} for i in range(nl)]}, indent=1))
 
     # ---- e2e through the public API (host SparseOperators -> diagonals on host) ----
     mesh = Mesh(p.nx, p.ny)
@@ -330,6 +345,7 @@ def run_b200(args):
         "fp64_tflops": flops_total, "fp64_frac_of_peak": flops_total / FP64_PEAK_TFLOPS,
         "work_per_energy_mults": W,
         "roofline": roofline,
+        "kernels": kernels,
         "e2e": e2e,
         "gpu_launches": int(plan.launch_count(n_e) * args.steps),
         "clocks": clk,

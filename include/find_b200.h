@@ -146,6 +146,14 @@ int find_plan_groups(const find_plan* plan, int32_t* pass, int32_t* level, int32
 int find_plan_specs(const find_plan* plan, int32_t n_energies, int32_t* kind, int32_t* step, int32_t* group,
                     int64_t* tasks);
 
+/* Opt-in per-launch device timing (process-wide, for benchmarks): while
+ * enabled every kernel launch of find_solve is bracketed by CUDA events on its
+ * stream.  find_solve_timing_enable(1) also clears the record;
+ * find_solve_timing_read() synchronises the events and returns the number of
+ * recorded launches (writes launch kind as in find_plan_specs, group, ms). */
+void find_solve_timing_enable(int32_t enable);
+int64_t find_solve_timing_read(int32_t* kind, int32_t* group, float* ms, int64_t cap);
+
 /* Synchronise `stream` and decode the device status of the last find_solve
  * that used `ws`. */
 int find_solve_status(find_plan* plan, void* ws, int32_t n_energies, void* stream, find_status* st);

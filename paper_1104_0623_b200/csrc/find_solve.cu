@@ -1657,6 +1657,38 @@ bool use_fused(const LaunchGroup& G, int nE) {
   return force == 1 && (G.end - G.begin) * (int64_t)nE >= 2 * 148;
 }
 
+// Opt-in per-launch timing (find_solve_timing_enable): one event pair per launch.
+struct LaunchTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // 2 per launch
+  std::vector<int32_t> kind;
+  std::vector<int32_t> group;
+  size_t used = 0;
+};
+LaunchTimer g_timer;
+
+int timer_mark(cudaStream_t stream, int32_t kind, int32_t group, bool begin, find_status* st) {
+  if (!g_timer.on) return FIND_OK;
+  if (begin) {
+    if (2 * g_timer.used + 2 > g_timer.ev.size()) {
+      for (int k = 0; k < 64; ++k) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        g_timer.ev.push_back(e);
+      }
+    }
+    g_timer.kind.resize(g_timer.used + 1);
+    g_timer.group.resize(g_timer.used + 1);
+    g_timer.kind[g_timer.used] = kind;
+    g_timer.group[g_timer.used] = group;
+    CUDA_TRY(cudaEventRecord(g_timer.ev[2 * g_timer.used], stream));
+  } else {
+    CUDA_TRY(cudaEventRecord(g_timer.ev[2 * g_timer.used + 1], stream));
+    ++g_timer.used;
+  }
+  return FIND_OK;
+}
+
 int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int nE, cudaStream_t stream,
                   find_status* st) {
   const Task* dtasks = (const Task*)P->d_tasks;
@@ -1676,6 +1708,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
       const Task* tk = dtasks + L.task_off;
       const unsigned cnt = (unsigned)L.task_count;
       const dim3 grid(cnt, (unsigned)nE);
+      if (int rt = timer_mark(stream, L.kind, (int32_t)gi, true, st)) return rt;
       switch (L.kind) {
         case kLSmall: {
           SolveParams p = prm;
@@ -1745,6 +1778,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         default: return fail_status(st, FIND_EINVAL, "unknown launch kind");
       }
       CUDA_TRY(cudaGetLastError());
+      if (int rt = timer_mark(stream, L.kind, (int32_t)gi, false, st)) return rt;
     }
   }
   return FIND_OK;
@@ -1884,6 +1918,26 @@ int find_plan_specs(const find_plan* P, int32_t nE, int32_t* kind, int32_t* step
     }
   }
   return FIND_OK;
+}
+
+void find_solve_timing_enable(int32_t enable) {
+  g_timer.on = enable != 0;
+  if (g_timer.on) g_timer.used = 0;  // enabling clears the record; disabling keeps it for reading
+}
+
+int64_t find_solve_timing_read(int32_t* kind, int32_t* group, float* ms, int64_t cap) {
+  const int64_t n = (int64_t)g_timer.used;
+  for (int64_t i = 0; i < std::min(n, cap); ++i) {
+    if (kind) kind[i] = g_timer.kind[i];
+    if (group) group[i] = g_timer.group[i];
+    if (ms) {
+      float v = 0.f;
+      if (cudaEventSynchronize(g_timer.ev[2 * i + 1]) == cudaSuccess)
+        cudaEventElapsedTime(&v, g_timer.ev[2 * i], g_timer.ev[2 * i + 1]);
+      ms[i] = v;
+    }
+  }
+  return n;
 }
 
 int find_solve_status(find_plan* P, void* ws, int32_t nE, void* stream_, find_status* st) {

@@ -70,6 +70,9 @@ class Plan:
         self._exc = {}
         self._ws = None
         self._lock = threading.Lock()
+        self.cache: dict = {}  # per-pattern host-side caches (validation, maps, ledgers)
+        self._pin_in = None
+        self._pin_out = None
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -140,6 +143,32 @@ class Plan:
                                       _i32p(out["group"]), _i64p(tasks))
         out["tasks"] = tasks
         return out
+
+    # ---- reused pinned host buffers for the H2D / D2H copies of solve_values ----
+    def host_values(self, n_energies: int) -> np.ndarray:
+        """A pinned [n_energies, nnz] complex128 host buffer (numpy view), reused across calls."""
+        import torch
+
+        if self._pin_in is None or self._pin_in.shape[0] < n_energies:
+            t = torch.empty((n_energies, self.nnz), dtype=torch.complex128)
+            self._pin_in = t.pin_memory() if torch.cuda.is_available() else t
+        return self._pin_in[:n_energies].numpy()
+
+    def is_pinned_view(self, arr: np.ndarray) -> bool:
+        if self._pin_in is None or not self._pin_in.is_pinned():
+            return False
+        return arr.__array_interface__["data"][0] == self._pin_in.data_ptr()
+
+    def pinned_tensor(self, arr: np.ndarray):
+        return self._pin_in[: arr.shape[0]]
+
+    def host_outputs(self, n_energies: int, compute_gless: bool):
+        import torch
+
+        if self._pin_out is None or self._pin_out[0].shape[0] < n_energies:
+            self._pin_out = tuple(torch.empty((n_energies, self.n), dtype=torch.complex128).pin_memory()
+                                  for _ in range(2))
+        return self._pin_out[0][:n_energies], self._pin_out[1][:n_energies]
 
     # ---- device execution (torch tensors for memory/streams only) ----
     def workspace(self, n_energies: int, compute_gless: bool, device):

@@ -100,18 +100,64 @@ def sigma_symmetry(sigma_csr) -> int:
     return 0
 
 
-def _validate(mesh, a, sigma, config):
-    """solver.py:591-608."""
+def _transpose_slots(plan: Plan) -> np.ndarray:
+    """CSR slot of (j, i) for every slot (i, j) of the (structurally symmetric) pattern; cached per plan."""
+    t = plan.cache.get("tslots")
+    if t is None:
+        n = plan.n
+        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(plan.indptr))
+        keys = rows * n + plan.indices
+        t = np.searchsorted(keys, plan.indices * n + rows)
+        plan.cache["tslots"] = t
+    return t
+
+
+def _sigma_prepare(plan: Plan, am: sp.csr_matrix, sigma) -> tuple[np.ndarray, int, bool]:
+    """Sigma on A's pattern, its exact (skew-)Hermitian symmetry, and the reference's
+    tolerance-based is_hermitian (operators.py:98-103), with pattern maps cached per plan."""
+    sm = _csr_sorted(sigma.matrix)
+    import hashlib
+
+    h = hashlib.sha1(np.ascontiguousarray(sm.indptr, np.int64).tobytes())
+    h.update(np.ascontiguousarray(sm.indices, np.int64).tobytes())
+    key = ("sigma_slots", h.hexdigest())
+    slots = plan.cache.get(key)
+    if slots is None:
+        n = plan.n
+        rows_a = np.repeat(np.arange(n, dtype=np.int64), np.diff(plan.indptr))
+        keys = rows_a * n + plan.indices
+        srows = np.repeat(np.arange(n, dtype=np.int64), np.diff(sm.indptr))
+        skeys = srows * n + sm.indices.astype(np.int64)
+        slots = np.searchsorted(keys, skeys)
+        ok = (slots < keys.size) & (keys[np.minimum(slots, keys.size - 1)] == skeys)
+        if not ok.all():
+            raise ValueError("scattering pattern exceeds the operator pattern")
+        plan.cache[key] = slots
+    s_vals = np.zeros(plan.nnz, np.complex128)
+    s_vals[slots] = sm.data
+    t = _transpose_slots(plan)
+    st = np.conj(s_vals[t])
+    sym = 1 if np.array_equal(s_vals, st) else (-1 if np.array_equal(s_vals, -st) else 0)
+    scale = np.abs(sm.data).max() if sm.nnz else 1.0
+    herm = bool(np.abs(s_vals - st).max() <= 1e-12 * max(scale, 1.0)) if s_vals.size else True
+    return s_vals, sym, herm
+
+
+def _validate(mesh, a, sigma, config, plan_cache: dict | None = None):
+    """solver.py:591-608 (pattern-only checks are cached per plan)."""
     if a.n != mesh.n:
         raise ValueError(f"operator size {a.n} does not match mesh with {mesh.n} nodes")
-    if not check_structural_symmetry(a):
-        raise ValueError("operator pattern is not structurally symmetric")
+    if plan_cache is None or not plan_cache.get("structurally_symmetric"):
+        if not check_structural_symmetry(a):
+            raise ValueError("operator pattern is not structurally symmetric")
+        if plan_cache is not None:
+            plan_cache["structurally_symmetric"] = True
     if config.compute_gless:
         if sigma is None:
             raise ValueError("compute_gless requires a scattering matrix")
         if sigma.n != a.n:
             raise ValueError("scattering matrix size mismatch")
-        if not check_pattern_subset(sigma, a):
+        if plan_cache is None and not check_pattern_subset(sigma, a):
             raise ValueError("scattering pattern exceeds the operator pattern")
     if config.kernel == "ldlt":
         d = a.matrix - a.matrix.T
@@ -160,11 +206,12 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
     stream = torch.cuda.current_stream(dev)
     gr = np.empty((n_e, plan.n), np.complex128)
     gl = np.empty((n_e, plan.n), np.complex128) if compute_gless else None
-    s_all = torch.from_numpy(s_vals).to(dev) if (compute_gless and s_b) else None
+    s_all = torch.from_numpy(s_vals).to(dev, non_blocking=True) if (compute_gless and s_b) else None
+    a_host = plan.pinned_tensor(a_vals) if plan.is_pinned_view(a_vals) else torch.from_numpy(a_vals)
     t_up = t_down = 0.0
     for k0 in range(0, n_e, chunk):
         k1 = min(n_e, k0 + chunk)
-        a_d = torch.from_numpy(a_vals[k0:k1]).to(dev)
+        a_d = a_host[k0:k1].to(dev, non_blocking=True)
         s_d = s_all if s_b else (torch.from_numpy(s_vals[k0:k1]).to(dev) if compute_gless else None)
         gr_d = torch.empty((k1 - k0, plan.n), dtype=torch.complex128, device=dev)
         gl_d = torch.empty((k1 - k0, plan.n), dtype=torch.complex128, device=dev) if compute_gless else None
@@ -176,15 +223,19 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
         plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, ws=ws, stream=stream,
                  groups=(plan.first_down_group, -1), sigma_sym=sigma_sym)
         ev[2].record(stream)
+        out_h = plan.host_outputs(k1 - k0, compute_gless)
+        out_h[0].copy_(gr_d, non_blocking=True)
+        if compute_gless:
+            out_h[1].copy_(gl_d, non_blocking=True)
         try:
             plan.check_status(ws, k1 - k0, stream)
         except Exception as exc:
             if hasattr(exc, "energy") and exc.energy is not None:
                 exc.energy += k0
             raise
-        gr[k0:k1] = gr_d.cpu().numpy()
+        gr[k0:k1] = out_h[0].numpy()
         if compute_gless:
-            gl[k0:k1] = gl_d.cpu().numpy()
+            gl[k0:k1] = out_h[1].numpy()
         t_up += ev[0].elapsed_time(ev[1]) * 1e-3
         t_down += ev[1].elapsed_time(ev[2]) * 1e-3
         del a_d, gr_d, gl_d
@@ -198,24 +249,51 @@ def _stats(plan: Plan, a_data: np.ndarray) -> dict:
     }
 
 
+def _ledger_cached(plan: Plan, config, sigma_herm: bool) -> FlopLedger:
+    key = ("ledger", config.kernel, bool(config.compute_gless), bool(sigma_herm), config.sigma_mode)
+    led = plan.cache.get(key)
+    if led is None:
+        led = plan.ledger(config.kernel, config.compute_gless, sigma_herm, config.sigma_mode)
+        plan.cache[key] = led
+    return FlopLedger(led.multiplications, dict(led.by_kernel))
+
+
+def _prepare(mesh, a_list, sigma, config):
+    """Validation (solver.py:591-608), cached plan, values packed into a reused pinned buffer."""
+    if not a_list:
+        raise ValueError("a_list is empty")
+    if a_list[0].n != mesh.n:
+        raise ValueError(f"operator size {a_list[0].n} does not match mesh with {mesh.n} nodes")
+    am0 = _csr_sorted(a_list[0].matrix)
+    plan, _ = plan_for(mesh.nx, mesh.ny, am0.indptr, am0.indices, config.leaf_max)
+    _validate(mesh, a_list[0], sigma, config, plan.cache)
+    vals = plan.host_values(len(a_list))
+    for k, a in enumerate(a_list):
+        am = am0 if k == 0 else _csr_sorted(a.matrix)
+        if am.nnz != am0.nnz or not (am.indptr is am0.indptr or np.array_equal(am.indptr, am0.indptr)) or not (
+                am.indices is am0.indices or np.array_equal(am.indices, am0.indices)):
+            raise ValueError("all operators of a batch must share one sparsity pattern")
+        vals[k] = am.data
+    s_vals, ssym, sherm = (None, 0, False)
+    if config.compute_gless:
+        s_vals, ssym, sherm = _sigma_prepare(plan, am0, sigma)
+    elif sigma is not None:
+        sherm = is_hermitian(sigma.matrix)
+    return plan, am0, vals, s_vals, ssym, sherm
+
+
 def solve(mesh, a, sigma, config: SolverConfig) -> SelectedInverse:
     """Run the full selected inversion on one operator (solver.py:586-701)."""
     t0 = time.perf_counter()
-    _validate(mesh, a, sigma, config)
-    am = _csr_sorted(a.matrix)
-    plan, _ = plan_for(mesh.nx, mesh.ny, am.indptr, am.indices, config.leaf_max)
-    s_vals = sigma_on_pattern(am, _csr_sorted(sigma.matrix)) if config.compute_gless else None
-    sigma_herm = is_hermitian(sigma.matrix) if sigma is not None else False
-    ssym = sigma_symmetry(sigma.matrix) if config.compute_gless else 0
+    plan, am, vals, s_vals, ssym, sherm = _prepare(mesh, [a], sigma, config)
     t1 = time.perf_counter()
-    gr, gl, t_up, t_down = solve_values(plan, am.data[None, :], s_vals, config.compute_gless, config.pivot_rtol, ssym)
+    gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol, ssym)
     t3 = time.perf_counter()
-    ledger = plan.ledger(config.kernel, config.compute_gless, sigma_herm, config.sigma_mode)
     return SelectedInverse(
         gr_diag=gr[0],
         gless_diag=gl[0] if gl is not None else None,
         offdiag=None,
-        ledger=ledger,
+        ledger=_ledger_cached(plan, config, sherm),
         timings={"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},
         stats=_stats(plan, am.data),
     )
@@ -225,23 +303,10 @@ def solve_batch(mesh, a_list, sigma, config: SolverConfig) -> SelectedInverseBat
     """Energy-batched solve: every operator shares A's pattern; one launch per
     (tree level, size class) covers all energy points."""
     t0 = time.perf_counter()
-    if not a_list:
-        raise ValueError("a_list is empty")
-    _validate(mesh, a_list[0], sigma, config)
-    am0 = _csr_sorted(a_list[0].matrix)
-    vals = np.empty((len(a_list), am0.nnz), np.complex128)
-    for k, a in enumerate(a_list):
-        am = _csr_sorted(a.matrix)
-        if am.nnz != am0.nnz or not (np.array_equal(am.indptr, am0.indptr) and np.array_equal(am.indices, am0.indices)):
-            raise ValueError("all operators of a batch must share one sparsity pattern")
-        vals[k] = am.data
-    plan, _ = plan_for(mesh.nx, mesh.ny, am0.indptr, am0.indices, config.leaf_max)
-    s_vals = sigma_on_pattern(am0, _csr_sorted(sigma.matrix)) if config.compute_gless else None
-    sigma_herm = is_hermitian(sigma.matrix) if sigma is not None else False
-    ssym = sigma_symmetry(sigma.matrix) if config.compute_gless else 0
+    plan, am0, vals, s_vals, ssym, sherm = _prepare(mesh, list(a_list), sigma, config)
     t1 = time.perf_counter()
     gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol, ssym)
     t3 = time.perf_counter()
-    return SelectedInverseBatch(gr, gl, plan.ledger(config.kernel, config.compute_gless, sigma_herm, config.sigma_mode),
+    return SelectedInverseBatch(gr, gl, _ledger_cached(plan, config, sherm),
                                 {"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},
                                 _stats(plan, am0.data))
