@@ -1582,7 +1582,7 @@ int set_attrs(find_status* st) {
 }
 
 // Side streams for the concurrent groups of a phase (per device, created once).
-constexpr int kSideStreams = 4;
+constexpr int kSideStreams = 8;
 struct SideStreams {
   int device = -1;
   cudaStream_t s[kSideStreams] = {};

@@ -218,6 +218,7 @@ namespace {
 
 constexpr int32_t kSmallMaxN = 32;  // warp-per-elimination path up to this merged size
 constexpr int32_t kMidMaxN = 64;    // CTA-per-elimination shared-memory path up to this merged size
+constexpr int32_t kLanes = 4;       // concurrent sub-groups per blocked-path size class
 
 struct Builder {
   find_plan* P;
@@ -493,24 +494,7 @@ struct Builder {
         const int ca = cls(a), cb = cls(b);
         return ca != cb ? ca < cb : a.n < b.n;
       });
-      int64_t gb = begin;
-      while (gb < end) {
-        const int c = cls(P->elims[gb]);
-        int64_t ge = gb;
-        while (ge < end && cls(P->elims[ge]) == c) ++ge;
-        const int path = c == 0 ? 0 : (c == 5 ? 2 : 1);
-        if (path == 1) {  // bound the scratch of one group (sub-batches run one after another)
-          int32_t ms = 0;
-          for (int64_t k = gb; k < ge; ++k) ms = std::max(ms, P->elims[k].s);
-          const int nbc = pick_nb_host(ms);
-          int64_t acc = 0, k = gb;
-          for (; k < ge; ++k) {
-            const int64_t w = find_scratch_elems(P->elims[k].n, P->elims[k].s, nbc);
-            if (k > gb && acc + w > kGroupScratchCap) break;
-            acc += w;
-          }
-          ge = k;
-        }
+      auto make_group = [&](int64_t gb, int64_t ge, int path) {
         LaunchGroup G;
         std::memset(&G, 0, sizeof(G));
         G.begin = gb; G.end = ge; G.path = path; G.pass = pass; G.level = level;
@@ -531,7 +515,52 @@ struct Builder {
         P->max_n = std::max(P->max_n, G.max_n);
         P->max_s = std::max(P->max_s, G.max_s);
         P->max_b = std::max(P->max_b, G.max_b);
-        gb = ge;
+      };
+      int64_t cb = begin;
+      while (cb < end) {
+        const int c = cls(P->elims[cb]);
+        int64_t ce = cb;
+        while (ce < end && cls(P->elims[ce]) == c) ++ce;
+        const int path = c == 0 ? 0 : (c == 5 ? 2 : 1);
+        if (path != 1) {
+          make_group(cb, ce, path);
+          cb = ce;
+          continue;
+        }
+        // blocked path: up to kLanes interleaved lanes (concurrent sub-groups on side
+        // streams, so one lane's latency-bound panel steps overlap another lane's DMMA
+        // tiles); each lane further split so one group's scratch stays under the cap
+        const int64_t cnt = ce - cb;
+        const int lanes = (int)std::min<int64_t>(kLanes, std::max<int64_t>(1, cnt / 2));
+        if (lanes > 1) {
+          std::vector<ElimDesc> tmp(P->elims.begin() + cb, P->elims.begin() + ce);
+          int64_t w = cb;
+          for (int l = 0; l < lanes; ++l)
+            for (int64_t k = l; k < cnt; k += lanes) P->elims[w++] = tmp[k];
+        }
+        int64_t lb = cb;
+        for (int l = 0; l < lanes; ++l) {
+          const int64_t le = cb + (cnt * (l + 1)) / lanes;  // lane l = [lb, le) after the reorder
+          (void)le;
+          const int64_t lcount = (cnt - l + lanes - 1) / lanes;
+          const int64_t lend = lb + lcount;
+          int32_t ms = 0;
+          for (int64_t k = lb; k < lend; ++k) ms = std::max(ms, P->elims[k].s);
+          const int nbc = pick_nb_host(ms);
+          int64_t gb = lb;
+          while (gb < lend) {
+            int64_t acc = 0, k = gb;
+            for (; k < lend; ++k) {
+              const int64_t wsz = find_scratch_elems(P->elims[k].n, P->elims[k].s, nbc);
+              if (k > gb && acc + wsz > kGroupScratchCap) break;
+              acc += wsz;
+            }
+            make_group(gb, k, 1);
+            gb = k;
+          }
+          lb = lend;
+        }
+        cb = ce;
       }
     };
 
