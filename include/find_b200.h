@@ -141,10 +141,14 @@ int find_plan_groups(const find_plan* plan, int32_t* pass, int32_t* level, int32
 /* Kernel-launch table of a find_solve over n_energies points, in issue order
  * (find_solve_launch_count() entries): launch kind (0 warp path, 1 gather A,
  * 2 panel, 3 TRSM, 4 trailing, 5 X solve, 6 finish, 7 gather Sigma, 8 T_S,
- * 9 R, 10 final, 11 Schur, 12 fused LU), panel step, launch group, task
- * count.  Any pointer may be NULL. */
+ * 9 R, 10 final, 11 Schur, 12 fused LU, 13 mid path), panel step, launch
+ * group, task count.  Any pointer may be NULL. */
 int find_plan_specs(const find_plan* plan, int32_t n_energies, int32_t* kind, int32_t* step, int32_t* group,
                     int64_t* tasks);
+
+/* Per launch group: its phase (the groups of a phase are independent and run
+ * concurrently; phases run in order). */
+int find_plan_group_phases(const find_plan* plan, int32_t* phase);
 
 /* Opt-in per-launch device timing (process-wide, for benchmarks): while
  * enabled every kernel launch of find_solve is bracketed by CUDA events on its

@@ -750,9 +750,7 @@ __device__ __forceinline__ const double2* child_block(const SolveParams& P, cons
 
 // ---- merged A / pivot-permuted Sigma into scratch (solver.py:97-132, 203-205, 227-228)
 template <bool SIGMA>
-__global__ void __launch_bounds__(kThreads) gather_kernel(SolveParams P, const Task* tasks) {
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y;
+__device__ void gather_body(const SolveParams& P, const Task& t, int e) {
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s;
   const Scr S = scratch_of(P, d, e);
@@ -791,6 +789,11 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(SolveParams P, const T
     block_argmax<kThreads>(mx, dummy, cv, ci);
     if (threadIdx.x == 0) S.pmax[r0 / kRowChunk] = mx;
   }
+}
+
+template <bool SIGMA>
+__global__ void __launch_bounds__(kThreads) gather_kernel(SolveParams P, const Task* tasks) {
+  gather_body<SIGMA>(P, tasks[blockIdx.x], blockIdx.y);
 }
 
 // Inverse of one triangle of the jb x jb diagonal block D (smem, ld NB+1) of a
@@ -1104,11 +1107,7 @@ template <>
 struct TrsmTiles<4> { using U = Tile<1, 8, 1, 1, false>; using L = Tile<8, 1, 1, 1, false>; };
 
 template <int NB>
-__global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Task* tasks, int j) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* smem = reinterpret_cast<double2*>(smem_raw);
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y;
+__device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, double2* smem) {
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s;
   const int j0 = j * NB, jb = min(NB, s - j0);
@@ -1175,12 +1174,14 @@ __global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Tas
   }
 }
 
-// ---- trailing update M[j1:, j1:] -= M[j1:, j0:j1] M[j0:j1, j1:]
-__global__ void __launch_bounds__(kThreads, 2) trail_kernel(SolveParams P, const Task* tasks, int j, int nb) {
+template <int NB>
+__global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Task* tasks, int j) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* smem = reinterpret_cast<double2*>(smem_raw);
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y;
+  trsm_body<NB>(P, tasks[blockIdx.x], blockIdx.y, j, reinterpret_cast<double2*>(smem_raw));
+}
+
+// ---- trailing update M[j1:, j1:] -= M[j1:, j0:j1] M[j0:j1, j1:]
+__device__ void trail_body(const SolveParams& P, const Task& t, int e, int j, int nb, double2* smem) {
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s;
   const int j0 = j * nb, jb = min(nb, s - j0), j1 = j0 + jb;
@@ -1197,13 +1198,14 @@ __global__ void __launch_bounds__(kThreads, 2) trail_kernel(SolveParams P, const
   });
 }
 
+__global__ void __launch_bounds__(kThreads, 2) trail_kernel(SolveParams P, const Task* tasks, int j, int nb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  trail_body(P, tasks[blockIdx.x], blockIdx.y, j, nb, reinterpret_cast<double2*>(smem_raw));
+}
+
 // ---- U = A_BB - Y U12 in one K = s pass (Y = M[s:, :s] = A_BS U11^-1, U12 = M[:s, s:]),
 // stored sorted (solver.py:234-243); final steps keep U_f in M for the epilogue
-__global__ void __launch_bounds__(kThreads, 2) schur_kernel(SolveParams P, const Task* tasks) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* smem = reinterpret_cast<double2*>(smem_raw);
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y;
+__device__ void schur_body(const SolveParams& P, const Task& t, int e, double2* smem) {
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s, b = d.b;
   double2* M = scratch_of(P, d, e).M;
@@ -1223,6 +1225,11 @@ __global__ void __launch_bounds__(kThreads, 2) schur_kernel(SolveParams P, const
       else *p = val;
     }
   });
+}
+
+__global__ void __launch_bounds__(kThreads, 2) schur_kernel(SolveParams P, const Task* tasks) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  schur_body(P, tasks[blockIdx.x], blockIdx.y, reinterpret_cast<double2*>(smem_raw));
 }
 
 // ---- X_j = (Y_j - X_{>j} L11[>j, j]) L_jj^-1 for 64 B rows
@@ -1418,11 +1425,7 @@ __global__ void __launch_bounds__(kFusedT, 2) lu_fused_kernel(SolveParams P, con
 }
 
 // ---- T_S = MS[s:, :s] - X MS[:s, :s]   (the S columns of T = Sigma'_B: - X Sigma'_S:)
-__global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const Task* tasks, int nb) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* smem = reinterpret_cast<double2*>(smem_raw);
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y;
+__device__ void tgemm_body(const SolveParams& P, const Task& t, int e, int nb, double2* smem) {
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s, b = d.b;
   const Scr S = scratch_of(P, d, e);
@@ -1439,16 +1442,17 @@ __global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const
   });
 }
 
+__global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const Task* tasks, int nb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  tgemm_body(P, tasks[blockIdx.x], blockIdx.y, nb, reinterpret_cast<double2*>(smem_raw));
+}
+
 // ---- R = Sigma'_BB - X Sigma'_SB - T_S X^H in one pass (two K = s products into one
 // accumulator), stored sorted (or kept in MS for the final step).  Symmetric mode:
 // lower-triangle tiles only; the upper triangle is written as the (skew-)conjugate
 // mirror of elements (i >= j), so results stay deterministic.
-__global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const Task* tasks, int nb) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* smem = reinterpret_cast<double2*>(smem_raw);
-  const Task t = tasks[blockIdx.x];
+__device__ void rgemm_body(const SolveParams& P, const Task& t, int e, int nb, double2* smem) {
   if (t.c == 2 && P.rsym != 0) return;
-  const int e = blockIdx.y;
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s, b = d.b;
   const Scr S = scratch_of(P, d, e);
@@ -1482,19 +1486,16 @@ __global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const
   });
 }
 
-// ---- final leaf step epilogue, warp per (leaf, energy)
-__global__ void __launch_bounds__(kSmallWarps * 32) final_kernel(SolveParams P, const Task* tasks, int64_t count,
-                                                                 int cmax) {
+__global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const Task* tasks, int nb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t idx = (int64_t)blockIdx.x * kSmallWarps + warp;
-  if (idx >= count) return;
-  const Task t = tasks[idx];
-  const int e = blockIdx.y;
+  rgemm_body(P, tasks[blockIdx.x], blockIdx.y, nb, reinterpret_cast<double2*>(smem_raw));
+}
+
+// ---- final leaf step epilogue, warp per (leaf, energy)
+__device__ void final_body_warp(const SolveParams& P, const Task& t, int e, double2* uf, int cmax, int lane) {
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s, c = d.b;
   const int ld = cmax + 1;
-  double2* uf = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * 2 * cmax * ld;
   double2* rf = uf + cmax * ld;
   const Scr S = scratch_of(P, d, e);
   for (int q = lane; q < c * c; q += 32) {
@@ -1503,6 +1504,16 @@ __global__ void __launch_bounds__(kSmallWarps * 32) final_kernel(SolveParams P, 
   }
   __syncwarp();
   final_epilogue_warp(P, d, t.e, e, uf, ld, rf, ld, lane);
+}
+
+__global__ void __launch_bounds__(kSmallWarps * 32) final_kernel(SolveParams P, const Task* tasks, int64_t count,
+                                                                 int cmax) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t idx = (int64_t)blockIdx.x * kSmallWarps + warp;
+  if (idx >= count) return;
+  final_body_warp(P, tasks[idx], blockIdx.y, reinterpret_cast<double2*>(smem_raw) + (size_t)warp * 2 * cmax * (cmax + 1),
+                  cmax, lane);
 }
 
 // ================================================================== host side
@@ -1612,49 +1623,17 @@ const bool g_reg_panel = [] {
   return !(f && f[0] == '1');
 }();
 
-// Enqueue the launches of groups [g_begin, g_end): phase by phase; the groups
-// of a phase fork onto side streams and join back into `stream`.
-int run_groups(const find_plan* P, const SolveParams& prm, int64_t g_begin, int64_t g_end, int nE,
-               cudaStream_t stream, find_status* st) {
-  int rc = set_attrs(st);
-  if (rc) return rc;
-  if ((rc = side_init(st))) return rc;
-  int64_t gi = g_begin;
-  while (gi < g_end) {
-    int64_t ge = gi;
-    while (ge < g_end && P->groups[ge].phase == P->groups[gi].phase) ++ge;
-    if (ge - gi == 1) {
-      if ((rc = run_one_group(P, prm, gi, nE, stream, st))) return rc;
-    } else {
-      const int slot = g_side.next;
-      g_side.next = (g_side.next + 1) % 64;
-      CUDA_TRY(cudaEventRecord(g_side.fork[slot], stream));
-      const int width = (int)std::min<int64_t>(ge - gi, kSideStreams);
-      for (int k = 0; k < width; ++k) CUDA_TRY(cudaStreamWaitEvent(g_side.s[k], g_side.fork[slot], 0));
-      for (int64_t g = gi; g < ge; ++g)
-        if ((rc = run_one_group(P, prm, g, nE, g_side.s[(g - gi) % kSideStreams], st))) return rc;
-      for (int k = 0; k < width; ++k) {
-        const int js = (slot + 1 + k) % 64;
-        CUDA_TRY(cudaEventRecord(g_side.join[js], g_side.s[k]));
-        CUDA_TRY(cudaStreamWaitEvent(stream, g_side.join[js], 0));
-      }
-    }
-    gi = ge;
-  }
-  return FIND_OK;
-}
-
 // Fused-LU launches (one CTA per elimination and energy) instead of the
 // level-batched phase launches: opt-in (FIND_B200_FUSED=1, for groups that fill
 // the GPU); measured slower than the phase launches once the mid path takes the
 // small eliminations (profiles/r01_*).
+const int g_force_fused = [] {
+  const char* f = std::getenv("FIND_B200_FUSED");
+  return f ? std::atoi(f) : 0;
+}();
 bool use_fused(const LaunchGroup& G, int nE) {
   if (G.fspec_end <= G.fspec_begin) return false;
-  static const int force = [] {
-    const char* f = std::getenv("FIND_B200_FUSED");
-    return f ? std::atoi(f) : 0;
-  }();
-  return force == 1 && (G.end - G.begin) * (int64_t)nE >= 2 * 148;
+  return g_force_fused == 1 && (G.end - G.begin) * (int64_t)nE >= 2 * 148;
 }
 
 // Opt-in per-launch timing (find_solve_timing_enable): one event pair per launch.
@@ -1685,6 +1664,38 @@ int timer_mark(cudaStream_t stream, int32_t kind, int32_t group, bool begin, fin
   } else {
     CUDA_TRY(cudaEventRecord(g_timer.ev[2 * g_timer.used + 1], stream));
     ++g_timer.used;
+  }
+  return FIND_OK;
+}
+
+// Enqueue the launches of groups [g_begin, g_end): phase by phase; the groups
+// of a phase fork onto side streams and join back into `stream`.
+int run_groups(const find_plan* P, const SolveParams& prm, int64_t g_begin, int64_t g_end, int nE,
+               cudaStream_t stream, find_status* st) {
+  int rc = set_attrs(st);
+  if (rc) return rc;
+  if ((rc = side_init(st))) return rc;
+  int64_t gi = g_begin;
+  while (gi < g_end) {
+    int64_t ge = gi;
+    while (ge < g_end && P->groups[ge].phase == P->groups[gi].phase) ++ge;
+    if (ge - gi == 1) {
+      if ((rc = run_one_group(P, prm, gi, nE, stream, st))) return rc;
+    } else {
+      const int slot = g_side.next;
+      g_side.next = (g_side.next + 1) % 64;
+      CUDA_TRY(cudaEventRecord(g_side.fork[slot], stream));
+      const int width = (int)std::min<int64_t>(ge - gi, kSideStreams);
+      for (int k = 0; k < width; ++k) CUDA_TRY(cudaStreamWaitEvent(g_side.s[k], g_side.fork[slot], 0));
+      for (int64_t g = gi; g < ge; ++g)
+        if ((rc = run_one_group(P, prm, g, nE, g_side.s[(g - gi) % kSideStreams], st))) return rc;
+      for (int k = 0; k < width; ++k) {
+        const int js = (slot + 1 + k) % 64;
+        CUDA_TRY(cudaEventRecord(g_side.join[js], g_side.s[k]));
+        CUDA_TRY(cudaStreamWaitEvent(stream, g_side.join[js], 0));
+      }
+    }
+    gi = ge;
   }
   return FIND_OK;
 }
@@ -1784,6 +1795,16 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
   return FIND_OK;
 }
 
+// Every kernel launch of a full solve, in enqueue order: f(kind, step, group, tasks).
+template <class F>
+void for_each_launch(const find_plan* P, int nE, F f) {
+  for (const LaunchGroup& G : P->groups) {
+    const bool fu = use_fused(G, nE);
+    for (int64_t si = fu ? G.fspec_begin : G.spec_begin; si < (fu ? G.fspec_end : G.spec_end); ++si)
+      f(P->specs[si].kind, P->specs[si].step, P->specs[si].group, P->specs[si].task_count);
+  }
+}
+
 SolveParams make_params(const find_plan* P, void* ws, int nE) {
   SolveParams prm;
   std::memset(&prm, 0, sizeof(prm));
@@ -1852,8 +1873,15 @@ size_t find_solve_workspace_bytes(const find_plan* P, int32_t nE, int32_t comput
 int64_t find_solve_launch_count(const find_plan* P, int32_t nE) {
   if (!P) return 0;
   int64_t k = 0;
-  for (const LaunchGroup& G : P->groups) k += use_fused(G, nE) ? G.fspec_end - G.fspec_begin : G.spec_end - G.spec_begin;
+  for_each_launch(P, nE, [&](int32_t, int32_t, int32_t, int64_t) { ++k; });
   return k;
+}
+
+int find_plan_group_phases(const find_plan* P, int32_t* phase) {
+  if (!P) return FIND_EINVAL;
+  for (size_t g = 0; g < P->groups.size(); ++g)
+    if (phase) phase[g] = P->groups[g].phase;
+  return FIND_OK;
 }
 
 int find_solve_groups(find_plan* P, const void* a_vals, const void* s_vals, int32_t s_broadcast, int32_t nE,
@@ -1908,15 +1936,13 @@ int find_plan_groups(const find_plan* P, int32_t* pass, int32_t* level, int32_t*
 int find_plan_specs(const find_plan* P, int32_t nE, int32_t* kind, int32_t* step, int32_t* group, int64_t* tasks) {
   if (!P) return FIND_EINVAL;
   int64_t i = 0;
-  for (const LaunchGroup& G : P->groups) {
-    const bool f = use_fused(G, nE);
-    for (int64_t si = f ? G.fspec_begin : G.spec_begin; si < (f ? G.fspec_end : G.spec_end); ++si, ++i) {
-      if (kind) kind[i] = P->specs[si].kind;
-      if (step) step[i] = P->specs[si].step;
-      if (group) group[i] = P->specs[si].group;
-      if (tasks) tasks[i] = P->specs[si].task_count;
-    }
-  }
+  for_each_launch(P, nE, [&](int32_t k, int32_t s, int32_t g, int64_t t) {
+    if (kind) kind[i] = k;
+    if (step) step[i] = s;
+    if (group) group[i] = g;
+    if (tasks) tasks[i] = t;
+    ++i;
+  });
   return FIND_OK;
 }
 

@@ -134,6 +134,12 @@ class Plan:
     KIND_NAMES = ("warp", "gatherA", "panel", "trsm", "trail", "xsolve", "finish", "gatherS", "tgemm", "rgemm", "final",
                   "schur", "lu_fused", "mid")
 
+    def group_phases(self) -> np.ndarray:
+        """Phase of every launch group (groups of a phase are independent; phases run in order)."""
+        ph = np.zeros(len(self.groups["count"]), np.int32)
+        _native.lib().find_plan_group_phases(self._h, _i32p(ph))
+        return ph
+
     def specs(self, n_energies: int = 1) -> dict:
         """Kernel-launch table of a solve over n_energies points, in issue order."""
         k = self.launch_count(n_energies)

@@ -48,3 +48,4 @@ def test_cta_path_variants_match_golden(cuda, env):
     res = json.loads(line[len("RESULT "):])
     for name, (egr, egl) in res.items():
         assert egr < 1e-10 and egl < 1e-10, (name, egr, egl, env)
+
