@@ -985,6 +985,244 @@ __global__ void __launch_bounds__(T, 512 / T) panel_kernel(SolveParams P, const 
   panel_body<NB, T>(P, t.e, d, blockIdx.y, t.a, sh);
 }
 
+// ---- panel step with ONE CTA barrier per column: T = 32 * ceil(R / 32) threads,
+// one S row per thread in registers.  Per column, every warp reduces its best
+// candidate (max |re|+|im|, lowest position on ties) and the candidate's lane
+// publishes its whole row and the pivot inverse in a per-warp slot (double
+// buffered); after the barrier every thread picks the winning slot and updates
+// its row from it.  Row interchanges are logical positions; rows are written to
+// their final positions at the end.  Same pivots and arithmetic as panel_body.
+template <int NB, int T>
+__global__ void __launch_bounds__(T) panel1_kernel(SolveParams P, const Task* tasks) {
+  constexpr int NW = T / 32;
+  __shared__ double2 cand[2][NW][NB + 1];
+  __shared__ double candv[2][NW];
+  __shared__ int candi[2][NW];
+  __shared__ int s_bad, s_nd;
+  __shared__ double s_scale[NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, j = t.a;
+  const int j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
+  const Scr S = scratch_of(P, d, e, NB);
+  double2* M = S.M;
+  double2* Lst = S.MS + (int64_t)tid * NB;
+  const bool has = tid < R;
+  int pos = tid;
+  double2 row[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) row[c] = (has && c < jb) ? M[(int64_t)(j0 + tid) * n + j0 + c] : cz();
+  if (tid == 0) { s_bad = INT32_MAX; s_nd = 0; }
+  double scale;
+  if (j == 0) {
+    scale = 0.0;
+    for (int q = tid; q < (s + kRowChunk - 1) / kRowChunk; q += T) scale = fmax(scale, S.pmax[q]);
+    for (int o = 16; o; o >>= 1) scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
+    if (lane == 0) s_scale[warp] = scale;
+    __syncthreads();
+    scale = s_scale[0];
+    for (int w = 1; w < NW; ++w) scale = fmax(scale, s_scale[w]);
+    if (tid == 0) {
+      *S.scale = scale;
+      if (scale == 0.0) s_bad = 0;
+    }
+  } else {
+    scale = *reinterpret_cast<volatile double*>(S.scale);
+  }
+#pragma unroll 1
+  for (int jj = 0; jj < jb; ++jj) {
+    const int buf = jj & 1;
+    double v = (has && pos >= jj) ? cabs1(row[0]) : -1.0;
+    int vi = (has && pos >= jj) ? pos : INT32_MAX;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
+      if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
+    }
+    if (has && pos == vi) {  // this warp's candidate: publish its row and pivot inverse
+#pragma unroll
+      for (int c = 0; c < NB; ++c) cand[buf][warp][c] = row[c];
+      cand[buf][warp][NB] = cinv(row[0]);
+    }
+    if (lane == 0) { candv[buf][warp] = v; candi[buf][warp] = vi; }
+    __syncthreads();
+    int wsel = 0;
+    {
+      double bv = candv[buf][0];
+      int bi = candi[buf][0];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) {
+        const double ov = candv[buf][w];
+        const int oi = candi[buf][w];
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; wsel = w; }
+      }
+      vi = bi;
+    }
+    const int pr = vi;
+    const double2* prow = cand[buf][wsel];
+    if (tid == 0) {
+      S.PIV[j0 + jj] = j0 + pr;
+      if (cabs(prow[0]) < P.rtol * scale) s_bad = min(s_bad, j0 + jj);
+    }
+    if (has && pos == pr) pos = -1 - jj;  // pivot row of column jj (final position jj)
+    else if (has && pos == jj) pos = pr;
+    if (has && pos > jj) {
+      const double2 l = cmul(row[0], prow[NB]);
+      Lst[jj] = l;
+#pragma unroll
+      for (int c = 1; c < NB; ++c) row[c - 1] = cfms(row[c], l, prow[c]);
+      row[NB - 1] = cz();
+    }
+  }
+  // final positions: pivot rows (pos = -1 - jj) hold U row jj shifted by jj
+  int fp = pos < 0 ? -1 - pos : pos;
+  if (has) {
+    double2* dst = M + (int64_t)(j0 + fp) * n + j0;
+    const int nl = min(fp, jb);
+#pragma unroll 8
+    for (int c = 0; c < nl; ++c) dst[c] = Lst[c];
+    if (pos < 0) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (fp + c < jb) dst[fp + c] = row[c];
+    }
+    if (fp != tid) {
+      const int k = atomicAdd(&s_nd, 1);
+      S.PERM[1 + k] = tid;
+      S.PERM[1 + 2 * NB + k] = fp;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    S.PERM[0] = s_nd;
+    if (s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
+  }
+}
+
+// ---- panel step, one WARP per (elimination, energy): rows [j0, s) x columns
+// [j0, j0+jb) staged in shared memory (row stride NB+1: conflict-free), physical
+// row interchanges (LAPACK order), no CTA barriers; several panels per CTA.
+// Same pivots (max |re|+|im|, lowest row on ties), same pivot test and the same
+// multiplier / update arithmetic as panel_body.  RPL = rows per lane (R <= 32 RPL).
+__host__ __device__ constexpr size_t warp_panel_bytes(int rmax, int nb) {
+  return ((size_t)rmax * (nb + 1) * sizeof(double2) + (size_t)rmax * sizeof(int) + 15) & ~size_t(15);
+}
+
+template <int NB, int RPL>
+__global__ void __launch_bounds__(256) warp_panel_kernel(SolveParams P, const Task* tasks, int64_t count, int rmax) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int LD = NB + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ti = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (ti >= count) return;  // warp-uniform; the kernel has no CTA barrier
+  const Task t = tasks[ti];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, j = t.a;
+  const int j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
+  const Scr S = scratch_of(P, d, e, NB);
+  unsigned char* base = smem_raw + (size_t)warp * warp_panel_bytes(rmax, NB);
+  double2* A = reinterpret_cast<double2*>(base);
+  int* rowof = reinterpret_cast<int*>(A + (size_t)rmax * LD);  // position -> original panel row
+  const double2* Mp = S.M + (int64_t)j0 * n + j0;
+#pragma unroll 4
+  for (int q = lane; q < R * NB; q += 32) {
+    const int r = q / NB, c = q % NB;
+    A[r * LD + c] = c < jb ? Mp[(int64_t)r * n + c] : cz();
+  }
+  for (int r = lane; r < R; r += 32) rowof[r] = r;
+  double scale;
+  if (j == 0) {
+    scale = 0.0;
+    for (int q = lane; q < (s + kRowChunk - 1) / kRowChunk; q += 32) scale = fmax(scale, S.pmax[q]);
+    for (int o = 16; o; o >>= 1) scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
+    if (lane == 0) *S.scale = scale;
+  } else {
+    scale = *reinterpret_cast<volatile double*>(S.scale);
+  }
+  int bad = (j == 0 && scale == 0.0) ? 0 : INT32_MAX;
+  __syncwarp();
+#pragma unroll 1
+  for (int jj = 0; jj < jb; ++jj) {
+    double v = -1.0;
+    int vi = INT32_MAX;
+    for (int r = jj + lane; r < R; r += 32) {
+      const double a = cabs1(A[r * LD + jj]);
+      if (a > v) { v = a; vi = r; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
+      if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
+    }
+    const int pr = vi;
+    if (pr != jj) {
+      for (int c = lane; c < NB; c += 32) {
+        const double2 x = A[jj * LD + c];
+        A[jj * LD + c] = A[pr * LD + c];
+        A[pr * LD + c] = x;
+      }
+      if (lane == 0) {
+        const int tmp = rowof[jj];
+        rowof[jj] = rowof[pr];
+        rowof[pr] = tmp;
+      }
+    }
+    __syncwarp();
+    const double2 pv = A[jj * LD + jj];
+    if (lane == 0) {
+      S.PIV[j0 + jj] = j0 + pr;
+      if (cabs(pv) < P.rtol * scale) bad = min(bad, j0 + jj);
+    }
+    const double2 uinv = cinv(pv);
+    double2 lv[RPL];
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      const int r = jj + 1 + lane + 32 * k;
+      if (r < R) {
+        lv[k] = cmul(A[r * LD + jj], uinv);
+        A[r * LD + jj] = lv[k];
+      }
+    }
+    for (int c = jj + 1; c < jb; ++c) {
+      const double2 u = A[jj * LD + c];
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        const int r = jj + 1 + lane + 32 * k;
+        if (r < R) A[r * LD + c] = cfms(A[r * LD + c], lv[k], u);
+      }
+    }
+    __syncwarp();
+  }
+  double2* Mw = S.M + (int64_t)j0 * n + j0;
+#pragma unroll 4
+  for (int q = lane; q < R * NB; q += 32) {
+    const int r = q / NB, c = q % NB;
+    if (c < jb) Mw[(int64_t)r * n + c] = A[r * LD + c];
+  }
+  // net row permutation of this panel (rows that moved: <= 2 NB)
+  int nd = 0;
+  for (int b0 = 0; b0 < R; b0 += 32) {
+    const int r = b0 + lane;
+    const bool mv = r < R && rowof[r] != r;
+    const unsigned m = __ballot_sync(0xffffffffu, mv);
+    if (mv) {
+      const int k = nd + __popc(m & ((1u << lane) - 1u));
+      S.PERM[1 + k] = rowof[r];
+      S.PERM[1 + 2 * NB + k] = r;
+    }
+    nd += __popc(m);
+  }
+  if (lane == 0) {
+    S.PERM[0] = nd;
+    if (bad != INT32_MAX) report_bad(P, t.e, e, bad);
+  }
+}
+
 // ---- same panel step with the S-row panel in shared memory (R > 256 rows):
 // 256 threads, row per thread in a strided loop, 2 barriers per column.
 template <int NB>
@@ -1569,6 +1807,9 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(small_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(mid_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(warp_panel_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(warp_panel_kernel<32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(warp_panel_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
 
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -1617,10 +1858,21 @@ int side_init(find_status* st) {
 
 int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE, cudaStream_t stream,
                   find_status* st);
-// register-resident panel rows (default) vs shared-memory panel (FIND_B200_SMEM_PANEL=1)
+// NB = 32 panel steps: register rows with one barrier per column (default),
+// register rows with two barriers per column (FIND_B200_PANEL=reg), one warp per
+// panel in shared memory (FIND_B200_PANEL=warp) or CTA with shared-memory rows
+// (FIND_B200_SMEM_PANEL=1)
 const bool g_reg_panel = [] {
   const char* f = std::getenv("FIND_B200_SMEM_PANEL");
   return !(f && f[0] == '1');
+}();
+const int g_panel_mode = [] {
+  const char* f = std::getenv("FIND_B200_PANEL");
+  if (f && std::string(f) == "reg") return 1;
+  if (f && std::string(f) == "warp") return 3;
+  const char* m = std::getenv("FIND_B200_SMEM_PANEL");
+  if (m && m[0] == '1') return 2;
+  return 0;
 }();
 
 // Fused-LU launches (one CTA per elimination and energy) instead of the
@@ -1747,7 +1999,25 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         case kLGatherS: gather_kernel<true><<<grid, kThreads, 0, stream>>>(prm, tk); break;
         case kLPanel: {
           const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
-          if (L.nb == 32 && g_reg_panel && rmax <= 64) panel_kernel<32, 64><<<grid, 64, 0, stream>>>(prm, tk);
+          if (L.nb == 32 && g_panel_mode == 0) {
+            switch ((std::max(rmax, 1) + 31) / 32) {
+              case 1: panel1_kernel<32, 32><<<grid, 32, 0, stream>>>(prm, tk); break;
+              case 2: panel1_kernel<32, 64><<<grid, 64, 0, stream>>>(prm, tk); break;
+              case 3: panel1_kernel<32, 96><<<grid, 96, 0, stream>>>(prm, tk); break;
+              case 4: panel1_kernel<32, 128><<<grid, 128, 0, stream>>>(prm, tk); break;
+              case 5: panel1_kernel<32, 160><<<grid, 160, 0, stream>>>(prm, tk); break;
+              case 6: panel1_kernel<32, 192><<<grid, 192, 0, stream>>>(prm, tk); break;
+              case 7: panel1_kernel<32, 224><<<grid, 224, 0, stream>>>(prm, tk); break;
+              default: panel1_kernel<32, 256><<<grid, 256, 0, stream>>>(prm, tk); break;
+            }
+          } else if (L.nb == 32 && g_panel_mode == 3) {
+            const size_t pb = warp_panel_bytes(std::max(rmax, 1), 32);
+            const int w = (int)std::max<size_t>(1, std::min<size_t>(8, kMaxSmem / pb));
+            const dim3 wg((unsigned)((L.task_count + w - 1) / w), (unsigned)nE);
+            if (rmax <= 64) warp_panel_kernel<32, 2><<<wg, 32 * w, pb * w, stream>>>(prm, tk, L.task_count, rmax);
+            else if (rmax <= 128) warp_panel_kernel<32, 4><<<wg, 32 * w, pb * w, stream>>>(prm, tk, L.task_count, rmax);
+            else warp_panel_kernel<32, 8><<<wg, 32 * w, pb * w, stream>>>(prm, tk, L.task_count, rmax);
+          } else if (L.nb == 32 && g_reg_panel && rmax <= 64) panel_kernel<32, 64><<<grid, 64, 0, stream>>>(prm, tk);
           else if (L.nb == 32 && g_reg_panel && rmax <= 128) panel_kernel<32, 128><<<grid, 128, 0, stream>>>(prm, tk);
           else if (L.nb == 32 && g_reg_panel) panel_kernel<32, 256><<<grid, 256, 0, stream>>>(prm, tk);
           else if (L.nb == 32)

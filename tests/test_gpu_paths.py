@@ -38,7 +38,8 @@ print("RESULT", json.dumps(out))
 @pytest.mark.parametrize("env", [{"FIND_B200_FUSED": "1"}, {"FIND_B200_FUSED": "0"},
                                  {"FIND_B200_FUSED": "0", "FIND_B200_NB": "16"},
                                  {"FIND_B200_FUSED": "0", "FIND_B200_NB": "8"},
-                                 {"FIND_B200_FUSED": "0", "FIND_B200_SMEM_PANEL": "1"}])
+                                 {"FIND_B200_FUSED": "0", "FIND_B200_SMEM_PANEL": "1"},
+                                 {"FIND_B200_PANEL": "reg"}, {"FIND_B200_PANEL": "warp"}])
 def test_cta_path_variants_match_golden(cuda, env):
     code = SCRIPT.format(root=str(ROOT), tests=str(ROOT / "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
