@@ -487,7 +487,7 @@ struct Builder {
         if (d.n <= kMidMaxN) return 5;
         if (d.s <= 64) return 1;
         if (d.s <= 128) return 2;
-        if (d.s <= 256) return 3;
+        if (d.s <= kRegPanelMaxS) return 3;
         return 4;
       };
       std::stable_sort(P->elims.begin() + begin, P->elims.end(), [&](const ElimDesc& a, const ElimDesc& b) {

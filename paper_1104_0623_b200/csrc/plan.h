@@ -62,17 +62,17 @@ struct LaunchSpec {
   int64_t task_off, task_count;
 };
 
-// Panel width of a group: the S rows of a panel live in registers, ceil(max_s/256)
-// rows per thread, NB complex each (<= 128 doubles per thread).
-// (NB=32: register panel, one row per thread, up to 256 rows; NB=16/8: shared-memory panel)
+// Panel width of a group.  NB = 32: register panel, one S row per thread, up to
+// kRegPanelMaxS rows; NB = 16/8/4: shared-memory panel for larger S.
+constexpr int64_t kRegPanelMaxS = 288;
 inline int pick_nb_host(int64_t max_s) {
   if (const char* f = std::getenv("FIND_B200_NB")) {  // test hook: force the panel width
     const int nb = std::atoi(f);
-    if ((nb == 32 && max_s <= 256) || (nb == 16 && max_s * 17 * 16 <= 220 * 1024) ||
+    if ((nb == 32 && max_s <= kRegPanelMaxS) || (nb == 16 && max_s * 17 * 16 <= 220 * 1024) ||
         (nb == 8 && max_s * 9 * 16 <= 220 * 1024) || (nb == 4 && max_s * 5 * 16 <= 220 * 1024))
       return nb;
   }
-  if (max_s <= 256) return 32;
+  if (max_s <= kRegPanelMaxS) return 32;
   if (max_s * 17 * 16 <= 220 * 1024) return 16;
   if (max_s * 9 * 16 <= 220 * 1024) return 8;
   if (max_s * 5 * 16 <= 220 * 1024) return 4;

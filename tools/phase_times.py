@@ -44,7 +44,8 @@ for rep in range(3):
         e1.record()
         evs.append((e0, e1))
     torch.cuda.synchronize()
-plan.check_status(ws, ne)
+if not os.environ.get("FIND_B200_SKIP"):
+    plan.check_status(ws, ne)
 rows = []
 g = plan.groups
 for k in range(len(bounds) - 1):
