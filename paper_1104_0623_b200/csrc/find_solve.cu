@@ -62,6 +62,12 @@ __device__ __forceinline__ double2 cfma(double2 acc, double2 a, double2 b) {
 }
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }  // LAPACK izamax metric
+// 1 / a as conj(a) / |a|^2: one reciprocal (pivots are far from the overflow / underflow range
+// of |a|^2; tiny pivots are rejected by the pivot test anyway)
+__device__ __forceinline__ double2 crcp(double2 a) {
+  const double r = 1.0 / fma(a.x, a.x, a.y * a.y);
+  return make_double2(a.x * r, -a.y * r);
+}
 __device__ __forceinline__ double cabs(double2 a) { return hypot(a.x, a.y); }
 __device__ __forceinline__ double2 cinv(double2 a) {  // Smith's algorithm
   if (a.x == 0.0 && a.y == 0.0) return cz();
@@ -801,17 +807,17 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(SolveParams P, const T
 //   LOWER (unit L):  [A 0; C B]^-1 = [A^-1 0; -B^-1 C A^-1  B^-1]
 //   upper (U):       [A C; 0 B]^-1 = [A^-1 -A^-1 C B^-1; 0  B^-1]
 // X, W: smem [NB][NB+1]; rows/cols >= jb act as identity.
-template <int NB, bool LOWER>
-__device__ void block_tri_inverse(const double2 (*D)[NB + 1], int jb, double2 (*X)[NB + 1], double2 (*W)[NB + 1]) {
+template <int NB, bool LOWER, int NT>
+__device__ void block_tri_inverse_t(const double2 (*D)[NB + 1], int jb, double2 (*X)[NB + 1], double2 (*W)[NB + 1]) {
   const int tid = threadIdx.x;
-  for (int q = tid; q < NB * NB; q += kThreads) {
+  for (int q = tid; q < NB * NB; q += NT) {
     const int r = q / NB, c = q % NB;
     X[r][c] = r != c ? cz() : ((LOWER || r >= jb) ? make_double2(1.0, 0.0) : cinv(D[r][r]));
   }
   __syncthreads();
 #pragma unroll 1
   for (int bs = 1; bs < NB; bs *= 2) {
-    for (int q = tid; q < (NB / 2) * bs; q += kThreads) {
+    for (int q = tid; q < (NB / 2) * bs; q += NT) {
       const int pair = q / (bs * bs), loc = q % (bs * bs);
       const int k = pair * 2 * bs, a = loc / bs, b = loc % bs;
       double2 acc = cz();
@@ -830,7 +836,7 @@ __device__ void block_tri_inverse(const double2 (*D)[NB + 1], int jb, double2 (*
       }
     }
     __syncthreads();
-    for (int q = tid; q < (NB / 2) * bs; q += kThreads) {
+    for (int q = tid; q < (NB / 2) * bs; q += NT) {
       const int pair = q / (bs * bs), loc = q % (bs * bs);
       const int k = pair * 2 * bs, a = loc / bs, b = loc % bs;
       double2 acc = cz();
@@ -848,6 +854,11 @@ __device__ void block_tri_inverse(const double2 (*D)[NB + 1], int jb, double2 (*
     }
     __syncthreads();
   }
+}
+
+template <int NB, bool LOWER>
+__device__ void block_tri_inverse(const double2 (*D)[NB + 1], int jb, double2 (*X)[NB + 1], double2 (*W)[NB + 1]) {
+  block_tri_inverse_t<NB, LOWER, kThreads>(D, jb, X, W);
 }
 
 // ---- panel LU of the S rows [j0, s) x [j0, j1) with partial pivoting (kernels.py:237-252)
@@ -985,44 +996,15 @@ __global__ void __launch_bounds__(T, 512 / T) panel_kernel(SolveParams P, const 
   panel_body<NB, T>(P, t.e, d, blockIdx.y, t.a, sh);
 }
 
-// Inverse of one triangle of the factored jb x jb diagonal block D (smem, ld
-// NB + 1, identity outside jb) by one warp, lane = column, column kept in
-// registers; written to out[NB][NB] (zeros outside jb).
-//   LOWER (unit L): X[r][c] = delta_rc - sum_{k<r} L[r][k] X[k][c]
-//   upper (U):      X[r][c] = (delta_rc - sum_{k>r} U[r][k] X[k][c]) / U[r][r]
-template <int NB, bool LOWER>
-__device__ void warp_tri_inverse(const double2* D, int jb, double2* out, int lane) {
-  constexpr int LD = NB + 1;
-  double2 x[NB];
-  const int c = lane;
-  if (LOWER) {
-#pragma unroll
-    for (int r = 0; r < NB; ++r) {
-      double2 a0 = make_double2(r == c ? 1.0 : 0.0, 0.0), a1 = cz();
-#pragma unroll
-      for (int k = 0; k < r; ++k) {
-        if (k & 1) a1 = cfms(a1, D[r * LD + k], x[k]);
-        else a0 = cfms(a0, D[r * LD + k], x[k]);
-      }
-      x[r] = make_double2(a0.x + a1.x, a0.y + a1.y);
-    }
-  } else {
-#pragma unroll
-    for (int r = NB - 1; r >= 0; --r) {
-      double2 a0 = make_double2(r == c ? 1.0 : 0.0, 0.0), a1 = cz();
-#pragma unroll
-      for (int k = r + 1; k < NB; ++k) {
-        if (k & 1) a1 = cfms(a1, D[r * LD + k], x[k]);
-        else a0 = cfms(a0, D[r * LD + k], x[k]);
-      }
-      x[r] = cmul(make_double2(a0.x + a1.x, a0.y + a1.y), cinv(D[r * LD + r]));
-    }
-  }
-  if (c < NB) {
-#pragma unroll
-    for (int r = 0; r < NB; ++r) out[r * NB + c] = (r < jb && c < jb) ? x[r] : cz();
-  }
-}
+#ifdef FIND_PANEL_CLOCKS  // tools/panel_bench.cu latency breakdown of one panel CTA
+__device__ long long g_pclk[64][8];
+#define PCLK(k) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && threadIdx.x / 32 == PCLK_WARP && jj < 64) g_pclk[jj][k] = clock64(); } while (0)
+#ifndef PCLK_WARP
+#define PCLK_WARP 0
+#endif
+#else
+#define PCLK(k) do {} while (0)
+#endif
 
 // ---- panel step with ONE CTA barrier per column: T = 32 * ceil(R / 32) threads,
 // one S row per thread in registers.  Per column, every warp reduces its best
@@ -1031,15 +1013,19 @@ __device__ void warp_tri_inverse(const double2* D, int jb, double2* out, int lan
 // buffered); after the barrier every thread picks the winning slot and updates
 // its row from it.  Row interchanges are logical positions; rows are written to
 // their final positions at the end.  Same pivots and arithmetic as panel_body.
-template <int NB, int T, bool INV = false>
-__global__ void __launch_bounds__(T) panel1_kernel(SolveParams P, const Task* tasks) {
+// two or three CTAs per SM up to 192 rows (the panel is latency-bound: throughput comes from
+// concurrent panels); above that the row registers leave room for one without spilling
+template <int NB, int T>
+__global__ void __launch_bounds__(T, (T <= 96 ? 3 : (T <= 192 ? 2 : 1))) panel1_kernel(SolveParams P, const Task* tasks) {
   constexpr int NW = T / 32;
   __shared__ double2 cand[2][NW][NB + 1];
   __shared__ double candv[2][NW];
   __shared__ int candi[2][NW];
   __shared__ int s_bad, s_nd;
   __shared__ double s_scale[NW];
-  __shared__ double2 Dg[NB * (NB + 1)];  // factored diagonal block (for L_jj^-1, U_jj^-1)
+  __shared__ double2 s_pval[NB];         // pivot values (test after the column loop)
+  __shared__ int s_piv[NB];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Task t = tasks[blockIdx.x];
   const int e = blockIdx.y;
@@ -1074,48 +1060,80 @@ __global__ void __launch_bounds__(T) panel1_kernel(SolveParams P, const Task* ta
 #pragma unroll 1
   for (int jj = 0; jj < jb; ++jj) {
     const int buf = jj & 1;
-    double v = (has && pos >= jj) ? cabs1(row[0]) : -1.0;
-    int vi = (has && pos >= jj) ? pos : INT32_MAX;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
-      if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
+    const int rem = jb - jj - 1;  // panel columns right of the pivot column (row[1..rem])
+    const bool act = has && pos >= jj;
+    PCLK(0);
+    // every candidate row's pivot inverse, off the reduction's critical path
+    const double2 rinv = crcp(row[0]);
+    // warp argmax: max |re|+|im| (>= 0, so its IEEE bits order like integers: high word,
+    // then low word), then the lowest position holding it
+    const double v0 = cabs1(row[0]);
+    const double v = v0 >= 0.0 ? v0 : 0.0;  // NaN (after a zero pivot) ranks lowest; the status already failed
+    const int vhi = act ? __double2hiint(v) : -1;
+    const int mhi = __reduce_max_sync(0xffffffffu, vhi);
+    const unsigned vlo = (unsigned)__double2loint(v);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, vhi == mhi ? vlo : 0u);
+    const bool best = act && vhi == mhi && vlo == mlo;
+    const int wpos = (int)__reduce_min_sync(0xffffffffu, (unsigned)(best ? pos : INT32_MAX));
+    PCLK(1);
+    if (lane == 0) {
+      candv[buf][warp] = mhi < 0 ? -1.0 : __hiloint2double(mhi, (int)mlo);
+      candi[buf][warp] = wpos;
     }
-    if (has && pos == vi) {  // this warp's candidate: publish its row and pivot inverse
-#pragma unroll
-      for (int c = 0; c < NB; ++c) cand[buf][warp][c] = row[c];
-      cand[buf][warp][NB] = cinv(row[0]);
-    }
-    if (lane == 0) { candv[buf][warp] = v; candi[buf][warp] = vi; }
+    PCLK(2);
     __syncthreads();
-    int wsel = 0;
-    {
-      double bv = candv[buf][0];
-      int bi = candi[buf][0];
+    PCLK(3);
+    // block argmax over the warp candidates (same rule), lane w looks at warp w
+    const double cvw = lane < NW ? candv[buf][lane] : -1.0;
+    const int ciw = lane < NW ? candi[buf][lane] : INT32_MAX;
+    const int whi = cvw < 0.0 ? -1 : __double2hiint(cvw);
+    const int bhi = __reduce_max_sync(0xffffffffu, whi);
+    const unsigned wlo = (unsigned)__double2loint(cvw);
+    const unsigned blo = __reduce_max_sync(0xffffffffu, whi == bhi ? wlo : 0u);
+    const int pr = (int)__reduce_min_sync(0xffffffffu, (unsigned)((whi == bhi && wlo == blo) ? ciw : INT32_MAX));
+    // only the pivot row is published (live part + its inverse), then a second barrier
+    if (has && pos == pr) {
+      double2* slot = cand[buf][0];
+      slot[NB] = rinv;
 #pragma unroll
-      for (int w = 1; w < NW; ++w) {
-        const double ov = candv[buf][w];
-        const int oi = candi[buf][w];
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; wsel = w; }
-      }
-      vi = bi;
+      for (int c0 = 0; c0 < NB; c0 += 4)
+        if (c0 <= rem) {
+#pragma unroll
+          for (int c = c0; c < c0 + 4; ++c) slot[c] = row[c];
+        }
     }
-    const int pr = vi;
+    __syncthreads();
+    const int wsel = 0;
     const double2* prow = cand[buf][wsel];
+    PCLK(4);
     if (tid == 0) {
-      S.PIV[j0 + jj] = j0 + pr;
-      if (cabs(prow[0]) < P.rtol * scale) s_bad = min(s_bad, j0 + jj);
+      s_piv[jj] = pr;
+      s_pval[jj] = prow[0];
     }
     if (has && pos == pr) pos = -1 - jj;  // pivot row of column jj (final position jj)
     else if (has && pos == jj) pos = pr;
     if (has && pos > jj) {
       const double2 l = cmul(row[0], prow[NB]);
       Lst[jj] = l;
+      // 8-column chunks of the live part: each chunk's shared loads issue together
 #pragma unroll
-      for (int c = 1; c < NB; ++c) row[c - 1] = cfms(row[c], l, prow[c]);
-      row[NB - 1] = cz();
+      for (int c0 = 1; c0 < NB; c0 += 8)
+        if (c0 <= rem) {
+          double2 pv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c0 + q < NB) pv[q] = prow[c0 + q];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c0 + q < NB) row[c0 + q - 1] = cfms(row[c0 + q], l, pv[q]);
+        }
     }
+    PCLK(5);
+  }
+  __syncthreads();
+  for (int k = tid; k < jb; k += T) {  // pivot rows and the pivot test of kernels.py:241 (abs < rtol * scale)
+    S.PIV[j0 + k] = j0 + s_piv[k];
+    if (cabs(s_pval[k]) < P.rtol * scale) atomicMin(&s_bad, j0 + k);
   }
   // final positions: pivot rows (pos = -1 - jj) hold U row jj shifted by jj
   int fp = pos < 0 ? -1 - pos : pos;
@@ -1135,32 +1153,11 @@ __global__ void __launch_bounds__(T) panel1_kernel(SolveParams P, const Task* ta
       S.PERM[1 + 2 * NB + k] = fp;
     }
   }
-  if (!INV) {
-    __syncthreads();
-    if (tid == 0) {
-      S.PERM[0] = s_nd;
-      if (s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
-    }
-    return;
-  }
-  // the diagonal block (identity outside jb) -> L_jj^-1 and U_jj^-1 for the TRSM / X launches
-  for (int q = tid; q < NB * NB; q += T) {
-    const int r = q / NB, c = q % NB;
-    if (r >= jb || c >= jb) Dg[r * (NB + 1) + c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
-  }
-  if (has && fp < jb) {
-    for (int c = 0; c < fp; ++c) Dg[fp * (NB + 1) + c] = Lst[c];
-#pragma unroll
-    for (int c = 0; c < NB; ++c)
-      if (fp + c < jb) Dg[fp * (NB + 1) + fp + c] = row[c];
-  }
   __syncthreads();
   if (tid == 0) {
     S.PERM[0] = s_nd;
     if (s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
   }
-  if (warp == 0) warp_tri_inverse<NB, true>(Dg, jb, S.LINV + (int64_t)j * NB * NB, lane);
-  if (warp == (NW > 1 ? 1 : 0)) warp_tri_inverse<NB, false>(Dg, jb, S.UINV + (int64_t)j * NB * NB, lane);
 }
 
 // ---- panel step, one WARP per (elimination, energy): rows [j0, s) x columns
@@ -1406,7 +1403,7 @@ template <>
 struct TrsmTiles<4> { using U = Tile<1, 8, 1, 1, false>; using L = Tile<8, 1, 1, 1, false>; };
 
 template <int NB>
-__device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, double2* smem, bool inv_ready = false) {
+__device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, double2* smem) {
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s;
   const int j0 = j * NB, jb = min(NB, s - j0);
@@ -1430,8 +1427,8 @@ __device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, dou
     __syncthreads();
     if (t.a == 2) return;
   }
-  if (!inv_ready) {  // the diagonal block's inverse this tile needs (L for U12 tiles, U for L21 tiles), published
-                     // to the elimination's LINV/UINV slot; every tile of the elimination writes the same values
+  {  // the diagonal block's inverse this tile needs (L for U12 tiles, U for L21 tiles), published to the
+     // elimination's LINV/UINV slot; every tile of the elimination writes the same values
     typedef double2 Row[NB + 1];
     Row* Dm = reinterpret_cast<Row*>(smem);
     Row* Xm = Dm + NB;
@@ -1474,9 +1471,9 @@ __device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, dou
 }
 
 template <int NB>
-__global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Task* tasks, int j, int inv_ready) {
+__global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Task* tasks, int j) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  trsm_body<NB>(P, tasks[blockIdx.x], blockIdx.y, j, reinterpret_cast<double2*>(smem_raw), inv_ready != 0);
+  trsm_body<NB>(P, tasks[blockIdx.x], blockIdx.y, j, reinterpret_cast<double2*>(smem_raw));
 }
 
 // ---- trailing update M[j1:, j1:] -= M[j1:, j0:j1] M[j0:j1, j1:]
@@ -1934,6 +1931,7 @@ const int g_force_fused = [] {
 }();
 bool use_fused(const LaunchGroup& G, int nE) {
   if (G.fspec_end <= G.fspec_begin) return false;
+  if (g_force_fused == 2) return G.max_b <= 64;  // experiment: tall-S / small-B groups only
   return g_force_fused == 1 && (G.end - G.begin) * (int64_t)nE >= 2 * 148;
 }
 
@@ -2095,10 +2093,10 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         }
         case kLTrsm:
           if (L.nb == 32)
-            trsm_kernel<32><<<grid, kThreads, trsm_smem<32>(), stream>>>(prm, tk, L.step, 0);
-          else if (L.nb == 16) trsm_kernel<16><<<grid, kThreads, trsm_smem<16>(), stream>>>(prm, tk, L.step, 0);
-          else if (L.nb == 8) trsm_kernel<8><<<grid, kThreads, trsm_smem<8>(), stream>>>(prm, tk, L.step, 0);
-          else trsm_kernel<4><<<grid, kThreads, trsm_smem<4>(), stream>>>(prm, tk, L.step, 0);
+            trsm_kernel<32><<<grid, kThreads, trsm_smem<32>(), stream>>>(prm, tk, L.step);
+          else if (L.nb == 16) trsm_kernel<16><<<grid, kThreads, trsm_smem<16>(), stream>>>(prm, tk, L.step);
+          else if (L.nb == 8) trsm_kernel<8><<<grid, kThreads, trsm_smem<8>(), stream>>>(prm, tk, L.step);
+          else trsm_kernel<4><<<grid, kThreads, trsm_smem<4>(), stream>>>(prm, tk, L.step);
           break;
         case kLTrail: trail_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk, L.step, L.nb); break;
         case kLXSolve:

@@ -142,6 +142,7 @@ int main(int argc, char** argv) {
     const int ncol = v == 4 ? 16 : 32;
     // compare M panel columns, PIV
     size_t diff = 0;
+    double maxrel = 0.0;
     for (int e = 0; e < nE; ++e)
       for (int i = 0; i < count; ++i) {
         const size_t o = (size_t)e * total + (size_t)i * per;
@@ -149,12 +150,27 @@ int main(int argc, char** argv) {
           for (int c = 0; c < ncol; ++c) {
             const double2 x = ref[o + (size_t)r * n + c], y = out[o + (size_t)r * n + c];
             if (std::memcmp(&x, &y, sizeof(x))) ++diff;
+            const double dx = std::hypot(x.x - y.x, x.y - y.y), nx = std::hypot(x.x, x.y);
+            maxrel = std::max(maxrel, dx / std::max(nx, 1e-300));
           }
         const int* p0 = reinterpret_cast<const int*>(ref.data() + o + 2 * (size_t)n * n);
         const int* p1 = reinterpret_cast<const int*>(out.data() + o + 2 * (size_t)n * n);
         for (int k = 0; k < ncol; ++k) diff += p0[k] != p1[k];
       }
-    std::printf("%-22s %9.1f us  mismatches %zu\n", names[v], tv * 1e3, diff);
+    std::printf("%-22s %9.1f us  bit mismatches %zu  max rel diff %.2e\n", names[v], tv * 1e3, diff, maxrel);
   }
+#ifdef FIND_PANEL_CLOCKS
+  {
+    CK(cudaMemcpy(d1, d0, h.size() * sizeof(double2), cudaMemcpyDeviceToDevice));
+    panel1_kernel<32, 160><<<dim3(1, 1), 160>>>(P, dt);
+    CK(cudaDeviceSynchronize());
+    long long c[64][8];
+    CK(cudaMemcpyFromSymbol(c, g_pclk, sizeof(c)));
+    std::printf("one CTA (T=160), warp %d: cycles per stage [argmax, publish, barrier, xwarp, update] per column\n", PCLK_WARP);
+    for (int jj = 0; jj < 32; jj += 4)
+      std::printf("col %2d: %5lld %5lld %5lld %5lld %5lld  | col total %lld\n", jj, c[jj][1] - c[jj][0], c[jj][2] - c[jj][1],
+                  c[jj][3] - c[jj][2], c[jj][4] - c[jj][3], c[jj][5] - c[jj][4], c[jj + 1][0] - c[jj][0]);
+  }
+#endif
   return 0;
 }
