@@ -157,6 +157,9 @@ int find_plan_group_phases(const find_plan* plan, int32_t* phase);
  * recorded launches (writes launch kind as in find_plan_specs, group, ms). */
 void find_solve_timing_enable(int32_t enable);
 int64_t find_solve_timing_read(int32_t* kind, int32_t* group, float* ms, int64_t cap);
+/* Same record as start / end times (ms) relative to the first recorded launch
+ * (a timeline across the side streams). */
+int64_t find_solve_timing_read2(int32_t* kind, int32_t* group, float* t_begin, float* t_end, int64_t cap);
 
 /* Synchronise `stream` and decode the device status of the last find_solve
  * that used `ws`. */

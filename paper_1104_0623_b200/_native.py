@@ -24,7 +24,7 @@ EXPORTED = (
     "find_plan_ledger", "find_ledger_key_name", "find_solve_workspace_bytes", "find_plan_upload", "find_solve",
     "find_solve_groups", "find_plan_groups", "find_solve_status", "find_solve_launch_count",
     "find_schur_sigma_update", "find_plan_exception_slots", "find_plan_specs", "find_solve_timing_enable",
-    "find_solve_timing_read", "find_plan_group_phases",
+    "find_solve_timing_read", "find_plan_group_phases", "find_solve_timing_read2",
 )
 
 
@@ -77,6 +77,7 @@ def lib():
         "find_plan_exception_slots": (i64, [P, i32, pi64, i64]),
         "find_plan_specs": (i32, [P, i32, pi32, pi32, pi32, pi64]),
         "find_plan_group_phases": (i32, [P, pi32]),
+        "find_solve_timing_read2": (i64, [pi32, pi32, C.POINTER(C.c_float), C.POINTER(C.c_float), i64]),
         "find_solve_timing_enable": (None, [i32]),
         "find_solve_timing_read": (i64, [pi32, pi32, C.POINTER(C.c_float), i64]),
         "find_schur_sigma_update": (i32, [i32, i32, P, P, P, P, P, P, P, P, dbl, P, P, P, i32, P, st]),

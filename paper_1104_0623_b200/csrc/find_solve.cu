@@ -62,6 +62,13 @@ __device__ __forceinline__ double2 cfma(double2 acc, double2 a, double2 b) {
 }
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }  // LAPACK izamax metric
+// Programmatic dependent launch: let the next kernel of the stream be scheduled
+// now (its CTAs only take resources this grid has left), then wait until the
+// previous kernel of the stream has completed and its writes are visible.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 // 1 / a as conj(a) / |a|^2: one reciprocal (pivots are far from the overflow / underflow range
 // of |a|^2; tiny pivots are rejected by the pivot test anyway)
 __device__ __forceinline__ double2 crcp(double2 a) {
@@ -210,6 +217,7 @@ __host__ __device__ constexpr int small_warp_elems(int nmax, int ld, int xcap) {
 
 __global__ void __launch_bounds__(kSmallWarps * 32) small_elim_kernel(SolveParams P, int64_t count, int nmax, int ld,
                                                                       int xcap) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t idx = (int64_t)blockIdx.x * kSmallWarps + warp;
@@ -418,6 +426,7 @@ __device__ __forceinline__ void block_max(double& v, double* cv) {
 }
 
 __global__ void __launch_bounds__(kMidThreads) mid_elim_kernel(SolveParams P, int64_t count, int nmax, int xcap) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int NT = kMidThreads;
   __shared__ double cv[2][NT / 32];
@@ -799,6 +808,7 @@ __device__ void gather_body(const SolveParams& P, const Task& t, int e) {
 
 template <bool SIGMA>
 __global__ void __launch_bounds__(kThreads) gather_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
   gather_body<SIGMA>(P, tasks[blockIdx.x], blockIdx.y);
 }
 
@@ -990,6 +1000,7 @@ __device__ void panel_body(const SolveParams& P, int64_t eidx, const ElimDesc& d
 
 template <int NB, int T>
 __global__ void __launch_bounds__(T, 512 / T) panel_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
   __shared__ PanelShared<NB, T> sh;
   const Task t = tasks[blockIdx.x];
   const ElimDesc d = P.elims[t.e];
@@ -1017,6 +1028,7 @@ __device__ long long g_pclk[64][8];
 // concurrent panels); above that the row registers leave room for one without spilling
 template <int NB, int T>
 __global__ void __launch_bounds__(T, (T <= 96 ? 3 : (T <= 192 ? 2 : 1))) panel1_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
   constexpr int NW = T / 32;
   __shared__ double2 cand[2][NW][NB + 1];
   __shared__ double candv[2][NW];
@@ -1171,6 +1183,7 @@ __host__ __device__ constexpr size_t warp_panel_bytes(int rmax, int nb) {
 
 template <int NB, int RPL>
 __global__ void __launch_bounds__(256) warp_panel_kernel(SolveParams P, const Task* tasks, int64_t count, int rmax) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LD = NB + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1285,6 +1298,7 @@ __global__ void __launch_bounds__(256) warp_panel_kernel(SolveParams P, const Ta
 // 256 threads, row per thread in a strided loop, 2 barriers per column.
 template <int NB>
 __global__ void __launch_bounds__(kThreads) panel_smem_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* panel = reinterpret_cast<double2*>(smem_raw);  // [R][NB+1]
   constexpr int PS = NB + 1;
@@ -1472,6 +1486,7 @@ __device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, dou
 
 template <int NB>
 __global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Task* tasks, int j) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   trsm_body<NB>(P, tasks[blockIdx.x], blockIdx.y, j, reinterpret_cast<double2*>(smem_raw));
 }
@@ -1495,6 +1510,7 @@ __device__ void trail_body(const SolveParams& P, const Task& t, int e, int j, in
 }
 
 __global__ void __launch_bounds__(kThreads, 2) trail_kernel(SolveParams P, const Task* tasks, int j, int nb) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   trail_body(P, tasks[blockIdx.x], blockIdx.y, j, nb, reinterpret_cast<double2*>(smem_raw));
 }
@@ -1524,6 +1540,7 @@ __device__ void schur_body(const SolveParams& P, const Task& t, int e, double2* 
 }
 
 __global__ void __launch_bounds__(kThreads, 2) schur_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   schur_body(P, tasks[blockIdx.x], blockIdx.y, reinterpret_cast<double2*>(smem_raw));
 }
@@ -1558,12 +1575,15 @@ __device__ void xsolve_tile(const Scr& S, int n, int s, int j, int r0, double2* 
 
 // ---- X_j = (Y_j - X_{>j} L11[>j, j]) L_jj^-1 for 64 B rows (X in its own buffer; Y stays for the Schur launch)
 template <int NB>
-__global__ void __launch_bounds__(kThreads) xsolve_kernel(SolveParams P, const Task* tasks, int j) {
+__global__ void __launch_bounds__(kThreads) xsolve_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Task t = tasks[blockIdx.x];
   const int e = blockIdx.y;
   const ElimDesc d = P.elims[t.e];
-  xsolve_tile<NB>(scratch_of(P, d, e, NB), d.n, d.s, j, t.a * kTile, reinterpret_cast<double2*>(smem_raw));
+  const Scr S = scratch_of(P, d, e, NB);
+  for (int j = (d.s + NB - 1) / NB - 1; j >= 0; --j)
+    xsolve_tile<NB>(S, d.n, d.s, j, t.a * kTile, reinterpret_cast<double2*>(smem_raw));
 }
 
 // ---- pivot permutation sigma and its inverse (+ L for the unit-test shim)
@@ -1591,6 +1611,7 @@ __device__ void finish_body(const SolveParams& P, int64_t eidx, const ElimDesc& 
 }
 
 __global__ void __launch_bounds__(kThreads) finish_kernel(SolveParams P, const Task* tasks, int nb) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Task t = tasks[blockIdx.x];
   const ElimDesc d = P.elims[t.e];
@@ -1604,6 +1625,7 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SolveParams P, const T
 // Same arithmetic and data layout as the phase launches.
 constexpr int kFusedT = 256;
 __global__ void __launch_bounds__(kFusedT, 2) lu_fused_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
   constexpr int NB = 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw);
@@ -1727,6 +1749,7 @@ __device__ void tgemm_body(const SolveParams& P, const Task& t, int e, int nb, d
 }
 
 __global__ void __launch_bounds__(kThreads, 2) tgemm_kernel(SolveParams P, const Task* tasks, int nb) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   tgemm_body(P, tasks[blockIdx.x], blockIdx.y, nb, reinterpret_cast<double2*>(smem_raw));
 }
@@ -1771,6 +1794,7 @@ __device__ void rgemm_body(const SolveParams& P, const Task& t, int e, int nb, d
 }
 
 __global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const Task* tasks, int nb) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   rgemm_body(P, tasks[blockIdx.x], blockIdx.y, nb, reinterpret_cast<double2*>(smem_raw));
 }
@@ -1792,6 +1816,7 @@ __device__ void final_body_warp(const SolveParams& P, const Task& t, int e, doub
 
 __global__ void __launch_bounds__(kSmallWarps * 32) final_kernel(SolveParams P, const Task* tasks, int64_t count,
                                                                  int cmax) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t idx = (int64_t)blockIdx.x * kSmallWarps + warp;
@@ -1829,6 +1854,29 @@ int fail_status(find_status* st, int code, const char* msg) {
     std::snprintf(st->message, sizeof(st->message), "%s", msg);
   }
   return code;
+}
+
+// Kernel launches, optionally with programmatic stream serialization
+// (FIND_B200_PDL=1; measured neutral on cfg1, so off by default): every kernel
+// starts with pdl_entry(), so a launch may begin while its predecessor in the
+// stream drains; errors surface through cudaGetLastError().
+const bool g_pdl = [] {
+  const char* f = std::getenv("FIND_B200_PDL");
+  return f && f[0] == '1';
+}();
+template <typename... KArgs, typename... Args>
+void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // dynamic budget (static smem of the kernels < 1 KB)
@@ -1879,11 +1927,15 @@ int set_attrs(find_status* st) {
   return FIND_OK;
 }
 
-// Side streams for the concurrent groups of a phase (per device, created once).
+// Side streams for the concurrent groups of a phase (per device, created once):
+// kSideStreams at normal priority and kHiStreams at the device's greatest
+// priority for the groups on the phase's critical path (the longest launch
+// chains), whose CTAs the scheduler then places first.
 constexpr int kSideStreams = 8;
+constexpr int kHiStreams = 4;
 struct SideStreams {
   int device = -1;
-  cudaStream_t s[kSideStreams] = {};
+  cudaStream_t s[kSideStreams + kHiStreams] = {};
   cudaEvent_t fork[64] = {}, join[64] = {};
   int next = 0;
 };
@@ -1893,7 +1945,10 @@ int side_init(find_status* st) {
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   if (g_side.device == dev) return FIND_OK;
-  for (int i = 0; i < kSideStreams; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&g_side.s[i], cudaStreamNonBlocking));
+  int least = 0, greatest = 0;
+  CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  for (int i = 0; i < kSideStreams + kHiStreams; ++i)
+    CUDA_TRY(cudaStreamCreateWithPriority(&g_side.s[i], cudaStreamNonBlocking, i < kSideStreams ? least : greatest));
   for (int i = 0; i < 64; ++i) {
     CUDA_TRY(cudaEventCreateWithFlags(&g_side.fork[i], cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&g_side.join[i], cudaEventDisableTiming));
@@ -1967,6 +2022,12 @@ int timer_mark(cudaStream_t stream, int32_t kind, int32_t group, bool begin, fin
   return FIND_OK;
 }
 
+// critical-path groups on high-priority streams (FIND_B200_PRIO=0 disables)
+const bool g_prio = [] {
+  const char* f = std::getenv("FIND_B200_PRIO");
+  return !(f && f[0] == '0');
+}();
+
 // Enqueue the launches of groups [g_begin, g_end): phase by phase; the groups
 // of a phase fork onto side streams and join back into `stream`.
 int run_groups(const find_plan* P, const SolveParams& prm, int64_t g_begin, int64_t g_end, int nE,
@@ -1981,17 +2042,39 @@ int run_groups(const find_plan* P, const SolveParams& prm, int64_t g_begin, int6
     if (ge - gi == 1) {
       if ((rc = run_one_group(P, prm, gi, nE, stream, st))) return rc;
     } else {
+      // critical groups: launch chains at least 3/4 as long as the phase's longest
+      int64_t longest = 0;
+      for (int64_t g = gi; g < ge; ++g) longest = std::max(longest, P->groups[g].spec_end - P->groups[g].spec_begin);
       const int slot = g_side.next;
       g_side.next = (g_side.next + 1) % 64;
       CUDA_TRY(cudaEventRecord(g_side.fork[slot], stream));
-      const int width = (int)std::min<int64_t>(ge - gi, kSideStreams);
-      for (int k = 0; k < width; ++k) CUDA_TRY(cudaStreamWaitEvent(g_side.s[k], g_side.fork[slot], 0));
-      for (int64_t g = gi; g < ge; ++g)
-        if ((rc = run_one_group(P, prm, g, nE, g_side.s[(g - gi) % kSideStreams], st))) return rc;
-      for (int k = 0; k < width; ++k) {
-        const int js = (slot + 1 + k) % 64;
-        CUDA_TRY(cudaEventRecord(g_side.join[js], g_side.s[k]));
-        CUDA_TRY(cudaStreamWaitEvent(stream, g_side.join[js], 0));
+      bool used[kSideStreams + kHiStreams] = {};
+      int nlo = 0, nhi = 0;
+      std::vector<int> sid((size_t)(ge - gi));
+      for (int64_t g = gi; g < ge; ++g) {
+        const int64_t len = P->groups[g].spec_end - P->groups[g].spec_begin;
+        const bool hi = g_prio && 4 * len >= 3 * longest;
+        sid[(size_t)(g - gi)] = hi ? kSideStreams + (nhi++ % kHiStreams) : (nlo++ % kSideStreams);
+      }
+      for (int64_t g = gi; g < ge; ++g) {
+        const int k = sid[(size_t)(g - gi)];
+        if (!used[k]) {
+          used[k] = true;
+          CUDA_TRY(cudaStreamWaitEvent(g_side.s[k], g_side.fork[slot], 0));
+        }
+      }
+      // critical chains first so their first launches are queued ahead of the rest
+      for (int pass = 0; pass < 2; ++pass)
+        for (int64_t g = gi; g < ge; ++g) {
+          const int k = sid[(size_t)(g - gi)];
+          if ((k >= kSideStreams) != (pass == 0)) continue;
+          if ((rc = run_one_group(P, prm, g, nE, g_side.s[k], st))) return rc;
+        }
+      for (int k = 0, js = 0; k < kSideStreams + kHiStreams; ++k) {
+        if (!used[k]) continue;
+        const int ev = (slot + 1 + js++) % 64;
+        CUDA_TRY(cudaEventRecord(g_side.join[ev], g_side.s[k]));
+        CUDA_TRY(cudaStreamWaitEvent(stream, g_side.join[ev], 0));
       }
     }
     gi = ge;
@@ -2039,8 +2122,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           const int nmax = std::max(1, G.max_n), ld = nmax + 1;
           const int xcap = G.max_b * G.max_s + G.max_b * G.max_b;
           const size_t smem = (size_t)kSmallWarps * small_warp_elems(nmax, ld, xcap) * sizeof(double2);
-          small_elim_kernel<<<dim3((unsigned)((L.task_count + kSmallWarps - 1) / kSmallWarps), (unsigned)nE),
-                              kSmallWarps * 32, smem, stream>>>(p, L.task_count, nmax, ld, xcap);
+          launch_k(small_elim_kernel, dim3((unsigned)((L.task_count + kSmallWarps - 1) / kSmallWarps), (unsigned)nE), kSmallWarps * 32, smem, stream, p, L.task_count, nmax, ld, xcap);
           break;
         }
         case kLMid: {
@@ -2050,72 +2132,72 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           const int nmax = std::max(1, G.max_n);
           const int xcap = G.max_b * G.max_s + G.max_b * G.max_b;
           const size_t smem = (size_t)mid_smem_elems(nmax, xcap) * sizeof(double2);
-          mid_elim_kernel<<<dim3((unsigned)L.task_count, (unsigned)nE), kMidThreads, smem, stream>>>(p, L.task_count, nmax,
+          launch_k(mid_elim_kernel, dim3((unsigned)L.task_count, (unsigned)nE), kMidThreads, smem, stream, p, L.task_count, nmax,
                                                                                                    xcap);
           break;
         }
-        case kLGatherA: gather_kernel<false><<<grid, kThreads, 0, stream>>>(prm, tk); break;
-        case kLGatherS: gather_kernel<true><<<grid, kThreads, 0, stream>>>(prm, tk); break;
+        case kLGatherA: launch_k(gather_kernel<false>, grid, kThreads, 0, stream, prm, tk); break;
+        case kLGatherS: launch_k(gather_kernel<true>, grid, kThreads, 0, stream, prm, tk); break;
         case kLPanel: {
           const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
           if (L.nb == 32 && g_panel_mode == 0) {
             switch ((std::max(rmax, 1) + 31) / 32) {
-              case 1: panel1_kernel<32, 32><<<grid, 32, 0, stream>>>(prm, tk); break;
-              case 2: panel1_kernel<32, 64><<<grid, 64, 0, stream>>>(prm, tk); break;
-              case 3: panel1_kernel<32, 96><<<grid, 96, 0, stream>>>(prm, tk); break;
-              case 4: panel1_kernel<32, 128><<<grid, 128, 0, stream>>>(prm, tk); break;
-              case 5: panel1_kernel<32, 160><<<grid, 160, 0, stream>>>(prm, tk); break;
-              case 6: panel1_kernel<32, 192><<<grid, 192, 0, stream>>>(prm, tk); break;
-              case 7: panel1_kernel<32, 224><<<grid, 224, 0, stream>>>(prm, tk); break;
-              case 8: panel1_kernel<32, 256><<<grid, 256, 0, stream>>>(prm, tk); break;
-              default: panel1_kernel<32, 288><<<grid, 288, 0, stream>>>(prm, tk); break;
+              case 1: launch_k(panel1_kernel<32, 32>, grid, 32, 0, stream, prm, tk); break;
+              case 2: launch_k(panel1_kernel<32, 64>, grid, 64, 0, stream, prm, tk); break;
+              case 3: launch_k(panel1_kernel<32, 96>, grid, 96, 0, stream, prm, tk); break;
+              case 4: launch_k(panel1_kernel<32, 128>, grid, 128, 0, stream, prm, tk); break;
+              case 5: launch_k(panel1_kernel<32, 160>, grid, 160, 0, stream, prm, tk); break;
+              case 6: launch_k(panel1_kernel<32, 192>, grid, 192, 0, stream, prm, tk); break;
+              case 7: launch_k(panel1_kernel<32, 224>, grid, 224, 0, stream, prm, tk); break;
+              case 8: launch_k(panel1_kernel<32, 256>, grid, 256, 0, stream, prm, tk); break;
+              default: launch_k(panel1_kernel<32, 288>, grid, 288, 0, stream, prm, tk); break;
             }
           } else if (L.nb == 32 && rmax > 256) {  // other NB = 32 variants hold <= 256 rows
-            panel_smem_kernel<32><<<grid, kThreads, (size_t)rmax * 33 * sizeof(double2), stream>>>(prm, tk);
+            launch_k(panel_smem_kernel<32>, grid, kThreads, (size_t)rmax * 33 * sizeof(double2), stream, prm, tk);
           } else if (L.nb == 32 && g_panel_mode == 3) {
             const size_t pb = warp_panel_bytes(std::max(rmax, 1), 32);
             const int w = (int)std::max<size_t>(1, std::min<size_t>(8, kMaxSmem / pb));
             const dim3 wg((unsigned)((L.task_count + w - 1) / w), (unsigned)nE);
-            if (rmax <= 64) warp_panel_kernel<32, 2><<<wg, 32 * w, pb * w, stream>>>(prm, tk, L.task_count, rmax);
-            else if (rmax <= 128) warp_panel_kernel<32, 4><<<wg, 32 * w, pb * w, stream>>>(prm, tk, L.task_count, rmax);
-            else warp_panel_kernel<32, 8><<<wg, 32 * w, pb * w, stream>>>(prm, tk, L.task_count, rmax);
-          } else if (L.nb == 32 && g_reg_panel && rmax <= 64) panel_kernel<32, 64><<<grid, 64, 0, stream>>>(prm, tk);
-          else if (L.nb == 32 && g_reg_panel && rmax <= 128) panel_kernel<32, 128><<<grid, 128, 0, stream>>>(prm, tk);
-          else if (L.nb == 32 && g_reg_panel) panel_kernel<32, 256><<<grid, 256, 0, stream>>>(prm, tk);
+            if (rmax <= 64) launch_k(warp_panel_kernel<32, 2>, wg, 32 * w, pb * w, stream, prm, tk, L.task_count, rmax);
+            else if (rmax <= 128) launch_k(warp_panel_kernel<32, 4>, wg, 32 * w, pb * w, stream, prm, tk, L.task_count, rmax);
+            else launch_k(warp_panel_kernel<32, 8>, wg, 32 * w, pb * w, stream, prm, tk, L.task_count, rmax);
+          } else if (L.nb == 32 && g_reg_panel && rmax <= 64) launch_k(panel_kernel<32, 64>, grid, 64, 0, stream, prm, tk);
+          else if (L.nb == 32 && g_reg_panel && rmax <= 128) launch_k(panel_kernel<32, 128>, grid, 128, 0, stream, prm, tk);
+          else if (L.nb == 32 && g_reg_panel) launch_k(panel_kernel<32, 256>, grid, 256, 0, stream, prm, tk);
           else if (L.nb == 32)
-            panel_smem_kernel<32><<<grid, kThreads, (size_t)std::max(rmax, 1) * 33 * sizeof(double2), stream>>>(prm, tk);
+            launch_k(panel_smem_kernel<32>, grid, kThreads, (size_t)std::max(rmax, 1) * 33 * sizeof(double2), stream, prm, tk);
           else if (L.nb == 16)
-            panel_smem_kernel<16><<<grid, kThreads, (size_t)G.max_s * 17 * sizeof(double2), stream>>>(prm, tk);
+            launch_k(panel_smem_kernel<16>, grid, kThreads, (size_t)G.max_s * 17 * sizeof(double2), stream, prm, tk);
           else if (L.nb == 8)
-            panel_smem_kernel<8><<<grid, kThreads, (size_t)G.max_s * 9 * sizeof(double2), stream>>>(prm, tk);
-          else panel_smem_kernel<4><<<grid, kThreads, (size_t)G.max_s * 5 * sizeof(double2), stream>>>(prm, tk);
+            launch_k(panel_smem_kernel<8>, grid, kThreads, (size_t)G.max_s * 9 * sizeof(double2), stream, prm, tk);
+          else launch_k(panel_smem_kernel<4>, grid, kThreads, (size_t)G.max_s * 5 * sizeof(double2), stream, prm, tk);
           break;
         }
         case kLTrsm:
           if (L.nb == 32)
-            trsm_kernel<32><<<grid, kThreads, trsm_smem<32>(), stream>>>(prm, tk, L.step);
-          else if (L.nb == 16) trsm_kernel<16><<<grid, kThreads, trsm_smem<16>(), stream>>>(prm, tk, L.step);
-          else if (L.nb == 8) trsm_kernel<8><<<grid, kThreads, trsm_smem<8>(), stream>>>(prm, tk, L.step);
-          else trsm_kernel<4><<<grid, kThreads, trsm_smem<4>(), stream>>>(prm, tk, L.step);
+            launch_k(trsm_kernel<32>, grid, kThreads, trsm_smem<32>(), stream, prm, tk, L.step);
+          else if (L.nb == 16) launch_k(trsm_kernel<16>, grid, kThreads, trsm_smem<16>(), stream, prm, tk, L.step);
+          else if (L.nb == 8) launch_k(trsm_kernel<8>, grid, kThreads, trsm_smem<8>(), stream, prm, tk, L.step);
+          else launch_k(trsm_kernel<4>, grid, kThreads, trsm_smem<4>(), stream, prm, tk, L.step);
           break;
-        case kLTrail: trail_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk, L.step, L.nb); break;
+        case kLTrail: launch_k(trail_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.step, L.nb); break;
         case kLXSolve:
-          if (L.nb == 32) xsolve_kernel<32><<<grid, kThreads, xsolve_smem<32>(), stream>>>(prm, tk, L.step);
-          else if (L.nb == 16) xsolve_kernel<16><<<grid, kThreads, xsolve_smem<16>(), stream>>>(prm, tk, L.step);
-          else if (L.nb == 8) xsolve_kernel<8><<<grid, kThreads, xsolve_smem<8>(), stream>>>(prm, tk, L.step);
-          else xsolve_kernel<4><<<grid, kThreads, xsolve_smem<4>(), stream>>>(prm, tk, L.step);
+          if (L.nb == 32) launch_k(xsolve_kernel<32>, grid, kThreads, xsolve_smem<32>(), stream, prm, tk);
+          else if (L.nb == 16) launch_k(xsolve_kernel<16>, grid, kThreads, xsolve_smem<16>(), stream, prm, tk);
+          else if (L.nb == 8) launch_k(xsolve_kernel<8>, grid, kThreads, xsolve_smem<8>(), stream, prm, tk);
+          else launch_k(xsolve_kernel<4>, grid, kThreads, xsolve_smem<4>(), stream, prm, tk);
           break;
         case kLFinish:
-          finish_kernel<<<grid, kThreads, std::max<size_t>((size_t)G.max_s * sizeof(int), 16), stream>>>(prm, tk, L.nb);
+          launch_k(finish_kernel, grid, kThreads, std::max<size_t>((size_t)G.max_s * sizeof(int), 16), stream, prm, tk, L.nb);
           break;
-        case kLTGemm: tgemm_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk, L.nb); break;
-        case kLRGemm: rgemm_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk, L.nb); break;
-        case kLSchur: schur_kernel<<<grid, kThreads, Tile64::SMEM, stream>>>(prm, tk); break;
-        case kLLuFused: lu_fused_kernel<<<grid, kFusedT, Tile64::SMEM, stream>>>(prm, tk); break;
+        case kLTGemm: launch_k(tgemm_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.nb); break;
+        case kLRGemm: launch_k(rgemm_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.nb); break;
+        case kLSchur: launch_k(schur_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk); break;
+        case kLLuFused: launch_k(lu_fused_kernel, grid, kFusedT, Tile64::SMEM, stream, prm, tk); break;
         case kLFinal: {
           const int cmax = std::max(1, G.max_b);
           const size_t smem = (size_t)kSmallWarps * 2 * cmax * (cmax + 1) * sizeof(double2);
-          final_kernel<<<dim3((cnt + kSmallWarps - 1) / kSmallWarps, (unsigned)nE), kSmallWarps * 32, smem, stream>>>(
+          launch_k(final_kernel, dim3((cnt + kSmallWarps - 1) / kSmallWarps, (unsigned)nE), kSmallWarps * 32, smem, stream, 
               prm, tk, L.task_count, cmax);
           break;
         }
@@ -2295,6 +2377,22 @@ int64_t find_solve_timing_read(int32_t* kind, int32_t* group, float* ms, int64_t
         cudaEventElapsedTime(&v, g_timer.ev[2 * i], g_timer.ev[2 * i + 1]);
       ms[i] = v;
     }
+  }
+  return n;
+}
+
+int64_t find_solve_timing_read2(int32_t* kind, int32_t* group, float* t_begin, float* t_end, int64_t cap) {
+  const int64_t n = (int64_t)g_timer.used;
+  for (int64_t i = 0; i < std::min(n, cap); ++i) {
+    if (kind) kind[i] = g_timer.kind[i];
+    if (group) group[i] = g_timer.group[i];
+    float a = 0.f, b = 0.f;
+    if (cudaEventSynchronize(g_timer.ev[2 * i + 1]) == cudaSuccess) {
+      cudaEventElapsedTime(&a, g_timer.ev[0], g_timer.ev[2 * i]);
+      cudaEventElapsedTime(&b, g_timer.ev[0], g_timer.ev[2 * i + 1]);
+    }
+    if (t_begin) t_begin[i] = a;
+    if (t_end) t_end[i] = b;
   }
   return n;
 }

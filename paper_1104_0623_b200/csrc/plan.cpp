@@ -146,15 +146,15 @@ void find_build_tasks(find_plan* P) {
         for (int tn = 0; tn < tb; ++tn) push((int32_t)e, tm, tn, 0);
     }
     spec(kLSchur, 0, nb, gi, off);
-    for (int j = steps - 1; j >= 0; --j) {
-      off = (int64_t)P->tasks.size();
-      for (int64_t e = G.begin; e < G.end; ++e) {
-        const ElimDesc& d = P->elims[e];
-        if (d.s <= j * nb || d.b == 0) continue;
-        for (int tm = 0; tm < (d.b + kTile - 1) / kTile; ++tm) push((int32_t)e, tm, 0, 0);
-      }
-      spec(kLXSolve, j, nb, gi, off);
+    // X = Y L11^-1: one task per 64-row tile of B, each walking the block columns right to
+    // left (a row tile depends only on its own rows of X)
+    off = (int64_t)P->tasks.size();
+    for (int64_t e = G.begin; e < G.end; ++e) {
+      const ElimDesc& d = P->elims[e];
+      if (d.s == 0 || d.b == 0) continue;
+      for (int tm = 0; tm < (d.b + kTile - 1) / kTile; ++tm) push((int32_t)e, tm, 0, 0);
     }
+    spec(kLXSolve, -1, nb, gi, off);
     off = (int64_t)P->tasks.size();
     for (int64_t e = G.begin; e < G.end; ++e) push((int32_t)e, 0, 0, 0);
     spec(kLFinish, 0, nb, gi, off);

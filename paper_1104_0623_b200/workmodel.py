@@ -60,7 +60,7 @@ def executed_cmacs(plan, sigma_sym: int = 0) -> dict:
                 acc["panel"] += sum(max(r - jj - 1, 0) for jj in range(jb)) * (nb - 1)
                 acc["trsm"] += jb * jb * (n - j1) + b * jb * jb
                 acc["trail"] += ((n - j1) ** 2 - b * b) * jb
-                acc["xsolve"] += b * jb * (s - j1) + b * jb * (jb - 1) // 2
+                acc["xsolve"] += b * jb * (s - j1) + b * jb * jb  # Z, then Z L_jj^-1 (DMMA)
             acc["schur"] += b * b * s
             acc["tgemm"] += b * s * s
             acc["rgemm"] += 2 * s * (b * (b + 1) // 2 if sym else b * b)
