@@ -131,6 +131,31 @@ int find_solve_groups(find_plan* plan, const void* a_vals, const void* s_vals, i
                       void* gl_out, void* ws, size_t ws_bytes, int64_t g_begin, int64_t g_end,
                       void* stream, find_status* st);
 
+/* ---- off-diagonal extraction (SolverConfig.compute_offdiag, solver.py:454-484,
+ *      637-642, 666-669; the G^< cross blocks of _extended_extraction,
+ *      solver.py:487-507) ---- */
+
+/* Directed adjacent pairs (u, v), u != v in the plan's pattern (a.adjacency(),
+ * operators.py:84-93), in ascending (u, v) order: the index space of the
+ * off_gr / off_gl outputs of find_solve_offdiag.  Builds the per-leaf
+ * extraction lists on first use.  Returns the pair count (writes
+ * min(count, cap) entries; u / v may be NULL), or -1 on failure. */
+int64_t find_plan_offdiag_pairs(find_plan* plan, int64_t* u, int64_t* v, int64_t cap);
+
+/* find_solve that also writes G^r(u, v) (off_gr) and, when compute_gless and
+ * off_gl != NULL, G^<(u, v) (off_gl) for every pair of find_plan_offdiag_pairs:
+ * device arrays [n_energies][n_pairs] complex128.  Each pair is taken from the
+ * extraction of the leaf the reference's downward DFS visits first
+ * (solver.py:666-669).  Leaves of more than 16 nodes are rejected (FIND_EINVAL). */
+int find_solve_offdiag(find_plan* plan, const void* a_vals, const void* s_vals, int32_t s_broadcast,
+                       int32_t n_energies, int32_t compute_gless, double pivot_rtol, void* gr_out,
+                       void* gl_out, void* off_gr, void* off_gl, void* ws, size_t ws_bytes, void* stream,
+                       find_status* st);
+int find_solve_offdiag_groups(find_plan* plan, const void* a_vals, const void* s_vals, int32_t s_broadcast,
+                              int32_t n_energies, int32_t compute_gless, double pivot_rtol, void* gr_out,
+                              void* gl_out, void* off_gr, void* off_gl, void* ws, size_t ws_bytes,
+                              int64_t g_begin, int64_t g_end, void* stream, find_status* st);
+
 /* Launch-group table (find_plan_info out[12] entries): pass (0 upward,
  * 1 downward, 2 final), tree level, path (0 warp-per-elimination, 1 CTA),
  * number of eliminations, and the largest s+b, s, b in the group.  Any
@@ -141,7 +166,7 @@ int find_plan_groups(const find_plan* plan, int32_t* pass, int32_t* level, int32
 /* Kernel-launch table of a find_solve over n_energies points, in issue order
  * (find_solve_launch_count() entries): launch kind (0 warp path, 1 gather A,
  * 2 panel, 3 TRSM, 4 trailing, 5 X solve, 6 finish, 7 gather Sigma, 8 T_S,
- * 9 R, 10 final, 11 Schur, 12 fused LU, 13 mid path), panel step, launch
+ * 9 R, 10 final, 11 Schur, 12 fused LU, 13 mid path, 14 off-diagonal), panel step, launch
  * group, task count.  Any pointer may be NULL. */
 int find_plan_specs(const find_plan* plan, int32_t n_energies, int32_t* kind, int32_t* step, int32_t* group,
                     int64_t* tasks);

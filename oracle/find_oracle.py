@@ -281,6 +281,8 @@ class OracleResult:
     gless_diag: np.ndarray | None
     ledger: OLedger
     timings: dict
+    offdiag: dict | None = None        # G^r on adjacent pairs (solver.py:454-484, 666-669)
+    offdiag_gless: dict | None = None  # G^< on the same pairs (_extended_extraction, solver.py:487-507)
 
 
 class FindOracle:
@@ -323,7 +325,8 @@ class FindOracle:
             rmat = rmat[np.ix_(order, order)]
         return u, rmat
 
-    def solve(self, a: sp.csr_matrix, sigma: sp.csr_matrix | None, compute_gless=True, pivot_rtol=1e-12):
+    def solve(self, a: sp.csr_matrix, sigma: sp.csr_matrix | None, compute_gless=True, pivot_rtol=1e-12,
+              compute_offdiag=False):
         import time
 
         t0 = time.perf_counter()
@@ -352,6 +355,9 @@ class FindOracle:
         gr = np.zeros(self.n, np.complex128)
         gl = np.zeros(self.n, np.complex128) if compute_gless else None
         filled = np.zeros(self.n, bool)
+        self._off = {} if compute_offdiag else None
+        self._offl = {} if (compute_offdiag and compute_gless) else None
+        self._adj = _adjacency(a) if compute_offdiag else None
         # downward_pass, solver.py:311-375 (DFS, negative data freed per subtree)
         neg = {-1: (z, z if compute_gless else None)}
         stack = [(self.root, False)]
@@ -382,7 +388,8 @@ class FindOracle:
         t2 = time.perf_counter()
         if not filled.all():
             raise RuntimeError("extraction did not cover every node")
-        return OracleResult(gr, gl, ledger, {"upward": t1 - t0, "downward_extract": t2 - t1, "total": t2 - t0})
+        return OracleResult(gr, gl, ledger, {"upward": t1 - t0, "downward_extract": t2 - t1, "total": t2 - t0},
+                            self._off, self._offl)
 
     def _leaf(self, leaf, a, sg, negdata, gr, gl, filled, ledger, compute_gless, rtol):
         """solver.py:392-418 (_final_elimination), 383-389 (_invert), 660-669 (sandwich, harvest)."""
@@ -409,6 +416,44 @@ class FindOracle:
             ledger.add("gless_sandwich", 2 * Fraction(g.shape[0]) ** 3)
             gl[nodes[new]] = np.diagonal(gless)[new]
         filled[nodes] = True
+        if self._off is not None:
+            self._leaf_offdiag(leaf, a, sg, ring, nodes, nu, nr, g, ledger)
+
+    def _leaf_offdiag(self, leaf, a, sg, ring, nodes, nu, nr, g, ledger):
+        """leaf_extract_offdiag (solver.py:454-484), first writer wins (solver.py:666-669):
+        pairs inside the leaf from G(C,C); cross pairs by one back-substitution each way.
+        G^< on the same pairs from the ring+leaf system as _extended_extraction does
+        (solver.py:487-507): g_t = M^-1, G^<_t = g_t S_t g_t^H."""
+        adj = self._adj
+        labels = np.concatenate([ring, nodes])
+        t = ring.size
+        gl_t = None
+        if self._offl is not None:
+            m = merge_matrix(a, ring, nodes, nu, extract(a, nodes, nodes))
+            s_t = merge_matrix(sg, ring, nodes, nr, extract(sg, nodes, nodes))
+            g_t = np.linalg.inv(m)
+            gl_t = (g_t @ s_t) @ g_t.conj().T
+
+        def put(i, j, gval, li, lj):
+            key = (int(labels[li]), int(labels[lj]))
+            if key not in self._off:
+                self._off[key] = complex(gval)
+                if gl_t is not None:
+                    self._offl[key] = complex(gl_t[li, lj])
+
+        sub = adj[nodes][:, nodes].tocoo()
+        for i, j in zip(sub.row, sub.col):
+            put(i, j, g[i, j], t + i, t + j)
+        if t:
+            a_bc = extract(a, ring, nodes)
+            a_cb = extract(a, nodes, ring)
+            g_bc = -np.linalg.solve(nu, a_bc @ g)
+            g_cb = -np.linalg.solve(nu.conj().T, (g @ a_cb).conj().T).conj().T
+            ledger.add("offdiag_backsub", 2 * (Fraction(t) ** 2 * nodes.size + t * Fraction(nodes.size) ** 2))
+            cross = adj[ring][:, nodes].tocoo()
+            for i, j in zip(cross.row, cross.col):
+                put(i, j, g_bc[i, j], i, t + j)
+                put(j, i, g_cb[j, i], t + j, i)
 
 
 def dense_gr_diag(a):

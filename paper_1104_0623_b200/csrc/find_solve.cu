@@ -26,6 +26,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <stdexcept>
 #include <vector>
 
 #include "../../include/find_b200.h"
@@ -108,6 +109,13 @@ struct SolveParams {
   unsigned long long* status;  // first failing (elim << 32 | energy << 16 | pos)
   int64_t elim_base;           // global index of elims[0] in the plan
   double2* dbg_l;              // unit-test shim only: L = A(B,S) A(S,S)^-1 (b x s), elimination 0 / energy 0
+  // off-diagonal extraction (find_solve_offdiag): [nE][n_pairs] outputs, items per final elimination
+  double2* off_gr;
+  double2* off_gl;
+  const OffItem* off_items;
+  const int64_t* off_item_off;
+  int64_t n_pairs;
+  int32_t off_sym;  // +1 / -1: Sigma^< exactly Hermitian / skew-Hermitian (then G^< is too), 0 general
 };
 
 __device__ __forceinline__ void report_bad(const SolveParams& P, int64_t elim_global, int e, int pos) {
@@ -1825,6 +1833,308 @@ __global__ void __launch_bounds__(kSmallWarps * 32) final_kernel(SolveParams P, 
                   cmax, lane);
 }
 
+
+// ================================================================== off-diagonal extraction
+// G^r and G^< between each leaf C and its ring r = B_{-C} (solver.py:454-484; the
+// G^< cross blocks as in _extended_extraction, solver.py:487-507, which the
+// reference computes by inverting [[U_r, A_rC], [A_Cr, A_CC]] and sandwiching
+// [[R_r, S_rC], [S_Cr, S_CC]]).  With K = A_rr^-1 A_rC, L = A_Cr A_rr^-1,
+// G = U_f^-1, G^<_CC = G R_f G^H:
+//   G(r, C)   = -K G                       G(C, r) = -G L
+//   G^<(r, C) = A_rr^-1 (S_rC - R_r L^H) G^H - K G^<_CC
+//   G^<(C, r) = [same with Sigma^H]^H   (= +-G^<(r, C)^H when Sigma^< is (skew-)Hermitian)
+// Outputs are written only for the pairs this leaf owns (first in DFS order).
+constexpr int kOffMaxC = 16;
+constexpr int kOffT = 256;
+
+// CTA-path final steps reuse the factorization left in scratch: M[:s,:s] = L11\U11 of
+// P A_rr, M[:s, s:] = U12 = L11^-1 P A_rC, M[s:, s:] = U_f, X = A_Cr U11^-1 L11^-1
+// (L = X P), the inverted diagonal blocks L_jj^-1 / U_jj^-1, and in MS the pivot-
+// permuted Sigma rows of S (P S_rr P^T | P S_rC), T_S and R_f.  Then
+//   P (S_rC - R_r L^H) = MS_SB - MS_SS X^H,  P (S^H_rC - R_r^H L^H) = T_S^H,
+// and A_rr^-1 = U11^-1 L11^-1 P: blocked substitutions with the published inverses.
+__global__ void __launch_bounds__(kOffT) offdiag_cta_kernel(SolveParams P, const Task* tasks, int nb) {
+  pdl_entry();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sm = reinterpret_cast<double2*>(smem_raw);
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y, tid = threadIdx.x;
+  const int64_t it0 = P.off_item_off[t.e], it1 = P.off_item_off[t.e + 1];
+  if (it0 == it1) return;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, c = d.b;
+  const Scr S = scratch_of(P, d, e, nb);
+  const double2* M = S.M;
+  const double2* MS = S.MS;
+  const bool gl = P.off_gl != nullptr;
+  const bool gen = gl && P.off_sym == 0;
+  const int nc = gl ? (gen ? 3 * c : 2 * c) : c;
+  const int ldc = c + 1;
+  double2* G = sm;
+  double2* GL = G + c * ldc;
+  double2* RF = GL + c * ldc;
+  double2* Z = RF + c * ldc;           // [s][nc]: K | x2 | x3
+  double2* TM = Z + (int64_t)s * nc;   // [nb][nc]
+  for (int q = tid; q < c * c; q += kOffT) {
+    const int i = q / c, j = q % c;
+    G[i * ldc + j] = M[(int64_t)(s + i) * n + s + j];
+    RF[i * ldc + j] = gl ? MS[(int64_t)(s + i) * n + s + j] : cz();
+  }
+  __syncthreads();
+  if (tid < 32) {
+    bool sing = false;  // a singular U_f is reported by the final launch
+    warp_gj_inverse(G, ldc, c, tid, &sing);
+  }
+  __syncthreads();
+  if (gl)
+    for (int q = tid; q < c * c; q += kOffT) {
+      const int i = q / c, j = q % c;
+      double2 acc = cz();
+      for (int a = 0; a < c; ++a) {
+        double2 tt = cz();
+        for (int b2 = 0; b2 < c; ++b2) tt = cfma(tt, RF[a * ldc + b2], cconj(G[j * ldc + b2]));
+        acc = cfma(acc, G[i * ldc + a], tt);
+      }
+      GL[i * ldc + j] = acc;
+    }
+  // right-hand sides, rows in pivoted order
+  for (int k = tid; k < s; k += kOffT) {
+    double2* z = Z + (int64_t)k * nc;
+    for (int j = 0; j < c; ++j) z[j] = M[(int64_t)k * n + s + j];
+    if (!gl) continue;
+    double2 v[kOffMaxC];
+    const double2* mr = MS + (int64_t)k * n;
+    for (int j = 0; j < c; ++j) {
+      double2 acc = mr[s + j];
+      const double2* xr = S.X + (int64_t)j * s;
+      for (int m = 0; m < s; ++m) acc = cfms(acc, mr[m], cconj(xr[m]));
+      v[j] = acc;
+    }
+    for (int j = 0; j < c; ++j) {
+      double2 acc = cz();
+      for (int i = 0; i < c; ++i) acc = cfma(acc, v[i], cconj(G[j * ldc + i]));
+      z[c + j] = acc;
+    }
+    if (gen)
+      for (int j = 0; j < c; ++j) {
+        double2 acc = cz();
+        for (int i = 0; i < c; ++i) acc = cfma(acc, cconj(MS[(int64_t)(s + i) * n + k]), cconj(G[j * ldc + i]));
+        z[2 * c + j] = acc;
+      }
+  }
+  __syncthreads();
+  const int nblk = (s + nb - 1) / nb;
+  if (gl) {  // unit-lower L11 on the Sigma columns
+    const int w = nc - c;
+    for (int j = 0; j < nblk; ++j) {
+      const int j0 = j * nb, jb = min(nb, s - j0), j1 = j0 + jb;
+      const double2* Li = S.LINV + (int64_t)j * nb * nb;
+      for (int q = tid; q < jb * w; q += kOffT) {
+        const int r = q / w, col = c + q % w;
+        double2 acc = cz();
+        for (int kk = 0; kk < jb; ++kk) acc = cfma(acc, Li[r * nb + kk], Z[(int64_t)(j0 + kk) * nc + col]);
+        TM[r * nc + col] = acc;
+      }
+      __syncthreads();
+      for (int q = tid; q < jb * w; q += kOffT) {
+        const int r = q / w, col = c + q % w;
+        Z[(int64_t)(j0 + r) * nc + col] = TM[r * nc + col];
+      }
+      __syncthreads();
+      for (int q = tid; q < (s - j1) * w; q += kOffT) {
+        const int i = j1 + q / w, col = c + q % w;
+        double2 acc = Z[(int64_t)i * nc + col];
+        const double2* lr = M + (int64_t)i * n + j0;
+        for (int kk = 0; kk < jb; ++kk) acc = cfms(acc, lr[kk], Z[(int64_t)(j0 + kk) * nc + col]);
+        Z[(int64_t)i * nc + col] = acc;
+      }
+      __syncthreads();
+    }
+  }
+  for (int j = nblk - 1; j >= 0; --j) {  // U11 on every column; rows become merged ring positions
+    const int j0 = j * nb, jb = min(nb, s - j0);
+    const double2* Ui = S.UINV + (int64_t)j * nb * nb;
+    for (int q = tid; q < jb * nc; q += kOffT) {
+      const int r = q / nc, col = q % nc;
+      double2 acc = cz();
+      for (int kk = 0; kk < jb; ++kk) acc = cfma(acc, Ui[r * nb + kk], Z[(int64_t)(j0 + kk) * nc + col]);
+      TM[r * nc + col] = acc;
+    }
+    __syncthreads();
+    for (int q = tid; q < jb * nc; q += kOffT) Z[(int64_t)(j0 + q / nc) * nc + q % nc] = TM[q];
+    __syncthreads();
+    for (int q = tid; q < j0 * nc; q += kOffT) {
+      const int i = q / nc, col = q % nc;
+      double2 acc = Z[(int64_t)i * nc + col];
+      const double2* ur = M + (int64_t)i * n + j0;
+      for (int kk = 0; kk < jb; ++kk) acc = cfms(acc, ur[kk], Z[(int64_t)(j0 + kk) * nc + col]);
+      Z[(int64_t)i * nc + col] = acc;
+    }
+    __syncthreads();
+  }
+  const double sg = P.off_sym < 0 ? -1.0 : 1.0;
+  for (int64_t q = it0 + tid; q < it1; q += kOffT) {
+    const OffItem I = P.off_items[q];
+    double2 gr = cz(), gv = cz();
+    if (I.type == 2) {
+      gr = G[I.r * ldc + I.c];
+      if (gl) gv = GL[I.r * ldc + I.c];
+    } else {
+      const double2* z = Z + (int64_t)I.r * nc;
+      const int cj = I.c;
+      if (I.type == 0) {
+        for (int k = 0; k < c; ++k) gr = cfms(gr, z[k], G[k * ldc + cj]);
+        if (gl) {
+          gv = z[c + cj];
+          for (int k = 0; k < c; ++k) gv = cfms(gv, z[k], GL[k * ldc + cj]);
+        }
+      } else {
+        const int pc = S.ISG[I.r];
+        for (int k = 0; k < c; ++k) gr = cfms(gr, G[cj * ldc + k], S.X[(int64_t)k * s + pc]);
+        if (gl) {
+          double2 v;
+          if (gen) {
+            v = z[2 * c + cj];
+            for (int k = 0; k < c; ++k) v = cfms(v, z[k], cconj(GL[cj * ldc + k]));
+            gv = cconj(v);
+          } else {
+            v = z[c + cj];
+            for (int k = 0; k < c; ++k) v = cfms(v, z[k], GL[k * ldc + cj]);
+            gv = make_double2(sg * v.x, -sg * v.y);
+          }
+        }
+      }
+    }
+    P.off_gr[(int64_t)e * P.n_pairs + I.pair] = gr;
+    if (gl) P.off_gl[(int64_t)e * P.n_pairs + I.pair] = gv;
+  }
+}
+
+// Warp- and mid-path final steps (s + c <= 64): the trailing system
+// M = [[U_r, A_rC], [A_Cr, A_CC]] and its Sigma counterpart are rebuilt in shared
+// memory and M is inverted in place (Gauss-Jordan, partial pivoting), as the
+// reference's _extended_extraction does (solver.py:487-507).
+template <int NMAX>
+__host__ __device__ constexpr size_t offdiag_small_smem() {
+  return (size_t)(2 * NMAX * (NMAX + 1) + 2 * NMAX * kOffMaxC + NMAX) * sizeof(double2);
+}
+
+template <int NMAX, int NT>
+__global__ void __launch_bounds__(NT) offdiag_small_kernel(SolveParams P, int64_t elim_begin) {
+  pdl_entry();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int LD = NMAX + 1;
+  __shared__ int ip[NMAX];
+  __shared__ int piv;
+  const int64_t k = elim_begin + blockIdx.x;
+  const int e = blockIdx.y, tid = threadIdx.x;
+  const int64_t it0 = P.off_item_off[k], it1 = P.off_item_off[k + 1];
+  if (it0 == it1) return;
+  const ElimDesc d = P.elims[k];
+  const int n = d.n, s = d.s, c = d.b;
+  double2* A = reinterpret_cast<double2*>(smem_raw);  // [NMAX][LD]: M, then M^-1
+  double2* SG = A + NMAX * LD;                          // [NMAX][LD]: merged Sigma
+  double2* Q = SG + NMAX * LD;                          // [NMAX][kOffMaxC]: Sigma G(C,:)^H
+  double2* Q2 = Q + NMAX * kOffMaxC;                    // [NMAX][kOffMaxC]: Sigma^H G(C,:)^H
+  double2* F = Q2 + NMAX * kOffMaxC;                    // [NMAX]
+  const bool gl = P.off_gl != nullptr;
+  const bool gen = gl && P.off_sym == 0;
+  const int32_t* map = P.i32 + d.map_off;
+  const SparseEntry* sp = P.sparse + d.sparse_off;
+  for (int sig = 0; sig < (gl ? 2 : 1); ++sig) {
+    double2* dst = sig ? SG : A;
+    const double2* lb = child_block(P, d, e, true, sig != 0);
+    const double2* rb = child_block(P, d, e, false, sig != 0);
+    for (int q = tid; q < n * n; q += NT) dst[(q / n) * LD + q % n] = block_entry(d, lb, rb, map[q / n], map[q % n]);
+    __syncthreads();
+    const double2* vals = sig ? P.s_vals + (P.s_broadcast ? 0 : (int64_t)e * P.nnz) : P.a_vals + (int64_t)e * P.nnz;
+    for (int q = tid; q < d.nsparse; q += NT) {
+      const SparseEntry en = sp[q];
+      dst[en.i * LD + en.j] = ldg2(vals + en.csr);
+    }
+    __syncthreads();
+  }
+  for (int kk = 0; kk < n; ++kk) {
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = kk;
+      for (int i = kk + tid; i < n; i += 32) {
+        const double v = cabs1(A[i * LD + kk]);
+        if (v > best) { best = v; bi = i; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) { piv = bi; ip[kk] = bi; }
+    }
+    __syncthreads();
+    const int p = piv;
+    if (p != kk)
+      for (int j = tid; j < n; j += NT) {
+        const double2 tmp = A[kk * LD + j];
+        A[kk * LD + j] = A[p * LD + j];
+        A[p * LD + j] = tmp;
+      }
+    __syncthreads();
+    const double2 pinv = cinv(A[kk * LD + kk]);
+    for (int i = tid; i < n; i += NT) F[i] = A[i * LD + kk];
+    __syncthreads();
+    for (int j = tid; j < n; j += NT) A[kk * LD + j] = cmul(j == kk ? make_double2(1.0, 0.0) : A[kk * LD + j], pinv);
+    __syncthreads();
+    for (int q = tid; q < n * n; q += NT) {
+      const int i = q / n, j = q % n;
+      if (i == kk) continue;
+      A[i * LD + j] = cfms(j == kk ? cz() : A[i * LD + j], F[i], A[kk * LD + j]);
+    }
+    __syncthreads();
+  }
+  for (int kk = n - 1; kk >= 0; --kk) {
+    const int p = ip[kk];
+    if (p != kk)
+      for (int i = tid; i < n; i += NT) {
+        const double2 tmp = A[i * LD + kk];
+        A[i * LD + kk] = A[i * LD + p];
+        A[i * LD + p] = tmp;
+      }
+    __syncthreads();
+  }
+  if (gl) {
+    for (int q = tid; q < n * c; q += NT) {
+      const int i = q / c, cj = q % c;
+      const double2* grow = A + (s + cj) * LD;
+      double2 a1 = cz(), a2 = cz();
+      for (int m = 0; m < n; ++m) {
+        a1 = cfma(a1, SG[i * LD + m], cconj(grow[m]));
+        if (gen) a2 = cfma(a2, cconj(SG[m * LD + i]), cconj(grow[m]));
+      }
+      Q[i * kOffMaxC + cj] = a1;
+      Q2[i * kOffMaxC + cj] = a2;
+    }
+    __syncthreads();
+  }
+  const double sg = P.off_sym < 0 ? -1.0 : 1.0;
+  for (int64_t q = it0 + tid; q < it1; q += NT) {
+    const OffItem I = P.off_items[q];
+    const int row = I.type == 2 ? s + I.r : I.r;  // G^< row: ring r (types 0, 1) or leaf node a
+    const int cj = I.c;
+    double2 gr, gv = cz();
+    if (I.type == 0) gr = A[I.r * LD + s + cj];
+    else if (I.type == 1) gr = A[(s + cj) * LD + I.r];
+    else gr = A[(s + I.r) * LD + s + cj];
+    if (gl) {
+      const double2* QQ = (I.type == 1 && gen) ? Q2 : Q;
+      double2 acc = cz();
+      for (int m = 0; m < n; ++m) acc = cfma(acc, A[row * LD + m], QQ[m * kOffMaxC + cj]);
+      if (I.type == 1) gv = gen ? cconj(acc) : make_double2(sg * acc.x, -sg * acc.y);
+      else gv = acc;
+    }
+    P.off_gr[(int64_t)e * P.n_pairs + I.pair] = gr;
+    if (gl) P.off_gl[(int64_t)e * P.n_pairs + I.pair] = gv;
+  }
+}
+
 // ================================================================== host side
 #define CUDA_TRY(x)                                                                                   \
   do {                                                                                                \
@@ -1923,6 +2233,11 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<8>()));
   CUDA_TRY(cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(offdiag_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(offdiag_small_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)offdiag_small_smem<32>()));
+  CUDA_TRY(cudaFuncSetAttribute(offdiag_small_kernel<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)offdiag_small_smem<64>()));
   done = true;
   return FIND_OK;
 }
@@ -2206,6 +2521,32 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
       CUDA_TRY(cudaGetLastError());
       if (int rt = timer_mark(stream, L.kind, (int32_t)gi, false, st)) return rt;
     }
+    if (prm.off_gr && G.pass == 2) {  // off-diagonal extraction right after the group's final step
+      if (G.max_b > kOffMaxC) return fail_status(st, FIND_EINVAL, "off-diagonal extraction supports leaves of <= 16 nodes");
+      if (int rt = timer_mark(stream, kLOffdiag, (int32_t)gi, true, st)) return rt;
+      const unsigned ne = (unsigned)nE;
+      if (G.path == 1) {
+        const LaunchSpec* fl = nullptr;
+        for (int64_t si = fused ? G.fspec_begin : G.spec_begin; si < (fused ? G.fspec_end : G.spec_end); ++si)
+          if (P->specs[si].kind == kLFinal) fl = &P->specs[si];
+        if (!fl) return fail_status(st, FIND_EINVAL, "final group without a final launch");
+        const bool gl = prm.off_gl != nullptr, gen = gl && prm.off_sym == 0;
+        const int c = G.max_b, nc = gl ? (gen ? 3 * c : 2 * c) : c;
+        const size_t smem = ((size_t)3 * c * (c + 1) + (size_t)G.max_s * nc + (size_t)G.nb * nc) * sizeof(double2);
+        if (smem > kMaxSmem) return fail_status(st, FIND_EINVAL, "leaf ring too large for off-diagonal extraction");
+        launch_k(offdiag_cta_kernel, dim3((unsigned)fl->task_count, ne), kOffT, smem, stream, prm, dtasks + fl->task_off,
+                 G.nb);
+      } else if (G.max_n <= 32) {
+        launch_k(offdiag_small_kernel<32, 64>, dim3((unsigned)(G.end - G.begin), ne), 64, offdiag_small_smem<32>(), stream,
+                 prm, G.begin);
+      } else {
+        if (G.max_n > 64) return fail_status(st, FIND_EINVAL, "unexpected final group size");
+        launch_k(offdiag_small_kernel<64, 128>, dim3((unsigned)(G.end - G.begin), ne), 128, offdiag_small_smem<64>(),
+                 stream, prm, G.begin);
+      }
+      CUDA_TRY(cudaGetLastError());
+      if (int rt = timer_mark(stream, kLOffdiag, (int32_t)gi, false, st)) return rt;
+    }
   }
   return FIND_OK;
 }
@@ -2251,7 +2592,11 @@ void find_plan_free_device(find_plan* P) {
   if (P->d_i32) cudaFree(P->d_i32);
   if (P->d_sparse) cudaFree(P->d_sparse);
   if (P->d_tasks) cudaFree(P->d_tasks);
+  if (P->d_off_items) cudaFree(P->d_off_items);
+  if (P->d_off_item_off) cudaFree(P->d_off_item_off);
   P->d_elims = P->d_i32 = P->d_sparse = P->d_tasks = nullptr;
+  P->d_off_items = P->d_off_item_off = nullptr;
+  P->off_device = -1;
   P->device = -1;
 }
 
@@ -2299,16 +2644,41 @@ int find_plan_group_phases(const find_plan* P, int32_t* phase) {
   return FIND_OK;
 }
 
-int find_solve_groups(find_plan* P, const void* a_vals, const void* s_vals, int32_t s_broadcast, int32_t nE,
-                      int32_t compute_gless, double rtol, void* gr_out, void* gl_out, void* ws, size_t ws_bytes,
-                      int64_t g_begin, int64_t g_end, void* stream_, find_status* st) {
+int find_plan_offdiag_build(find_plan* P);  // plan.cpp
+
+int find_solve_offdiag_groups(find_plan* P, const void* a_vals, const void* s_vals, int32_t s_broadcast, int32_t nE,
+                              int32_t compute_gless, double rtol, void* gr_out, void* gl_out, void* off_gr,
+                              void* off_gl, void* ws, size_t ws_bytes, int64_t g_begin, int64_t g_end, void* stream_,
+                              find_status* st) {
   status_ok(st);
   if (!P || !a_vals || !gr_out || !ws || nE < 1) return fail_status(st, FIND_EINVAL, "invalid argument");
   if (compute_gless && (!s_vals || !gl_out)) return fail_status(st, FIND_EINVAL, "compute_gless needs s_vals and gl_out");
   if (nE > 0xffff) return fail_status(st, FIND_EINVAL, "too many energy points in one call");
   if (ws_bytes < find_solve_workspace_bytes(P, nE, compute_gless)) return fail_status(st, FIND_ENOMEM, "workspace too small");
+  if (off_gl && !compute_gless) return fail_status(st, FIND_EINVAL, "off_gl needs compute_gless");
   int rc = find_plan_upload(P, st);
   if (rc) return rc;
+  if (off_gr) {
+    try {
+      if (find_plan_offdiag_build(P) != FIND_OK) return fail_status(st, FIND_EINVAL, "off-diagonal plan failed");
+    } catch (const std::exception& ex) {
+      return fail_status(st, FIND_ENOMEM, ex.what());
+    }
+    if (P->off_device != P->device) {
+      if (P->d_off_items) cudaFree(P->d_off_items);
+      if (P->d_off_item_off) cudaFree(P->d_off_item_off);
+      P->d_off_items = P->d_off_item_off = nullptr;
+      const size_t bi = std::max<size_t>(16, P->off_items.size() * sizeof(OffItem));
+      const size_t bo = P->off_item_off.size() * sizeof(int64_t);
+      CUDA_TRY(cudaMalloc(&P->d_off_items, bi));
+      CUDA_TRY(cudaMalloc(&P->d_off_item_off, bo));
+      if (!P->off_items.empty())
+        CUDA_TRY(cudaMemcpy(P->d_off_items, P->off_items.data(), P->off_items.size() * sizeof(OffItem),
+                            cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(P->d_off_item_off, P->off_item_off.data(), bo, cudaMemcpyHostToDevice));
+      P->off_device = P->device;
+    }
+  }
   cudaStream_t stream = (cudaStream_t)stream_;
   SolveParams prm = make_params(P, ws, nE);
   prm.a_vals = (const double2*)a_vals;
@@ -2319,10 +2689,32 @@ int find_solve_groups(find_plan* P, const void* a_vals, const void* s_vals, int3
   prm.rtol = rtol;
   prm.gr_out = (double2*)gr_out;
   prm.gl_out = (double2*)gl_out;
+  if (off_gr) {
+    prm.off_gr = (double2*)off_gr;
+    prm.off_gl = (double2*)off_gl;
+    prm.off_items = (const OffItem*)P->d_off_items;
+    prm.off_item_off = (const int64_t*)P->d_off_item_off;
+    prm.n_pairs = (int64_t)P->off_u.size();
+    prm.off_sym = prm.rsym;
+  }
   if (g_begin < 0) g_begin = 0;
   if (g_end < 0 || g_end > (int64_t)P->groups.size()) g_end = (int64_t)P->groups.size();
   if (g_begin == 0) CUDA_TRY(cudaMemsetAsync(ws, 0xff, 8, stream));
   return run_groups(P, prm, g_begin, g_end, nE, stream, st);
+}
+
+int find_solve_offdiag(find_plan* P, const void* a_vals, const void* s_vals, int32_t s_broadcast, int32_t nE,
+                       int32_t compute_gless, double rtol, void* gr_out, void* gl_out, void* off_gr, void* off_gl,
+                       void* ws, size_t ws_bytes, void* stream_, find_status* st) {
+  return find_solve_offdiag_groups(P, a_vals, s_vals, s_broadcast, nE, compute_gless, rtol, gr_out, gl_out, off_gr,
+                                   off_gl, ws, ws_bytes, 0, -1, stream_, st);
+}
+
+int find_solve_groups(find_plan* P, const void* a_vals, const void* s_vals, int32_t s_broadcast, int32_t nE,
+                      int32_t compute_gless, double rtol, void* gr_out, void* gl_out, void* ws, size_t ws_bytes,
+                      int64_t g_begin, int64_t g_end, void* stream_, find_status* st) {
+  return find_solve_offdiag_groups(P, a_vals, s_vals, s_broadcast, nE, compute_gless, rtol, gr_out, gl_out, nullptr,
+                                   nullptr, ws, ws_bytes, g_begin, g_end, stream_, st);
 }
 
 int find_solve(find_plan* P, const void* a_vals, const void* s_vals, int32_t s_broadcast, int32_t nE,

@@ -781,6 +781,96 @@ int find_plan_ledger(const find_plan* P, int32_t kernel, int32_t compute_gless, 
   return FIND_OK;
 }
 
+// ---- off-diagonal extraction plan (solver.py:454-484, 644-669) ----
+// Every directed adjacent pair (u, v), u != v in A's pattern (operators.py:84-93),
+// ascending.  The reference harvests pairs leaf by leaf in the downward DFS
+// order, first writer wins (solver.py:666-669): a pair inside one leaf comes
+// from that leaf's block G(C, C); a pair across two leaves from the leaf that
+// is visited first, as G(ring, C) or G(C, ring) of its extraction.
+int find_plan_offdiag_build(find_plan* P) {
+  if (P->off_ready) return FIND_OK;
+  const int64_t n = P->n, ne = (int64_t)P->elims.size();
+  std::vector<int32_t> leaf_elim((size_t)n, -1), pos((size_t)n, -1);
+  std::vector<int64_t> dfs((size_t)ne, -1);
+  for (int64_t k = 0; k < ne; ++k) {
+    const ElimDesc& d = P->elims[k];
+    if (d.kind != kFinal) continue;
+    auto it = std::lower_bound(P->label_keys.begin(), P->label_keys.end(), d.label);
+    if (it == P->label_keys.end() || *it != d.label) return FIND_EINVAL;
+    dfs[k] = P->label_index[it - P->label_keys.begin()];  // preorder index = DFS leaf order
+    for (int32_t j = 0; j < d.b; ++j) {
+      const int32_t node = P->i32[d.rank_off + j];
+      leaf_elim[node] = (int32_t)k;
+      pos[node] = j;
+    }
+  }
+  for (int64_t v = 0; v < n; ++v)
+    if (leaf_elim[v] < 0) return FIND_EINVAL;
+  P->off_u.clear();
+  P->off_v.clear();
+  std::vector<int32_t> owner;
+  for (int64_t u = 0; u < n; ++u)
+    for (int64_t q = P->indptr[u]; q < P->indptr[u + 1]; ++q) {
+      const int64_t v = P->indices[q];
+      if (v == u) continue;
+      P->off_u.push_back(u);
+      P->off_v.push_back(v);
+      const int32_t lu = leaf_elim[u], lv = leaf_elim[v];
+      owner.push_back(dfs[lu] <= dfs[lv] ? lu : lv);
+    }
+  const int64_t np = (int64_t)P->off_u.size();
+  P->off_item_off.assign((size_t)ne + 1, 0);
+  for (int64_t p = 0; p < np; ++p) P->off_item_off[owner[p] + 1]++;
+  for (int64_t k = 0; k < ne; ++k) P->off_item_off[k + 1] += P->off_item_off[k];
+  P->off_items.assign((size_t)np, OffItem{0, 0, 0, 0, 0});
+  std::vector<int64_t> fill(P->off_item_off.begin(), P->off_item_off.end() - 1);
+  for (int64_t p = 0; p < np; ++p) {
+    const int64_t u = P->off_u[p], v = P->off_v[p];
+    const int32_t k = owner[p];
+    OffItem it{0, 0, 0, 0, p};
+    if (leaf_elim[u] == leaf_elim[v]) {
+      it.type = 2; it.r = pos[u]; it.c = pos[v];
+    } else if (leaf_elim[v] == k) {
+      it.type = 0; it.r = (int32_t)u; it.c = pos[v];  // r resolved below (ring node id -> S position)
+    } else {
+      it.type = 1; it.r = (int32_t)v; it.c = pos[u];
+    }
+    P->off_items[fill[k]++] = it;
+  }
+  std::vector<int32_t> rp((size_t)n, -1);
+  for (int64_t k = 0; k < ne; ++k) {
+    const int64_t b0 = P->off_item_off[k], b1 = P->off_item_off[k + 1];
+    if (b0 == b1) continue;
+    const ElimDesc& d = P->elims[k];
+    for (int32_t q = 0; q < d.s; ++q) rp[P->slabels[d.slabel_off + q]] = q;
+    for (int64_t t = b0; t < b1; ++t) {
+      OffItem& it = P->off_items[t];
+      if (it.type == 2) continue;
+      const int32_t r = rp[it.r];
+      if (r < 0) return FIND_EINVAL;  // not in the leaf's ring: cannot happen for a symmetric pattern
+      it.r = r;
+    }
+    for (int32_t q = 0; q < d.s; ++q) rp[P->slabels[d.slabel_off + q]] = -1;
+  }
+  P->off_ready = true;
+  return FIND_OK;
+}
+
+int64_t find_plan_offdiag_pairs(find_plan* P, int64_t* u, int64_t* v, int64_t cap) {
+  if (!P) return -1;
+  try {
+    if (find_plan_offdiag_build(P) != FIND_OK) return -1;
+  } catch (const std::exception&) {
+    return -1;
+  }
+  const int64_t np = (int64_t)P->off_u.size();
+  for (int64_t p = 0; p < std::min(np, cap); ++p) {
+    if (u) u[p] = P->off_u[p];
+    if (v) v[p] = P->off_v[p];
+  }
+  return np;
+}
+
 void find_plan_free_device(find_plan* P);  // find_solve.cu
 
 void find_plan_destroy(find_plan* P) {

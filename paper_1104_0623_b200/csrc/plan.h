@@ -53,6 +53,7 @@ enum LaunchKind : int32_t {
   kLSchur = 11,    // U = A_BB - Y U12 (K = s), stored sorted  tasks {e, tm, tn}
   kLLuFused = 12,  // whole blocked LU + X + sigma in one CTA    tasks {e}
   kLMid = 13,      // CTA-per-elimination smem kernel (32 < s+b <= 64)
+  kLOffdiag = 14,  // off-diagonal G^r / G^< of a final group (after its final launch)
 };
 
 struct Task { int32_t e, a, b, c; };
@@ -100,6 +101,15 @@ struct SparseEntry {  // merged (row, col) <- csr value slot
   int64_t csr;
 };
 
+// One off-diagonal output of a final leaf step (solver.py:454-484): the directed
+// adjacent pair `pair` is read from this leaf's extraction as
+//   type 0: G(ring r, leaf node c)   type 1: G(leaf node c, ring r)   type 2: G(leaf a=r, leaf b=c)
+// with r the merged S position of the ring node (type 0/1) or the leaf position (type 2).
+struct OffItem {
+  int32_t type, r, c, pad;
+  int64_t pair;
+};
+
 struct Cluster {
   int64_t label;
   int32_t x0, y0, w, h, level;
@@ -130,6 +140,14 @@ struct find_plan {
   int64_t ws_elems = 0;
   int32_t max_n = 0, max_s = 0, max_b = 0, depth = 0, n_leaves = 0;
   int32_t n_levels_up = 0, n_levels_down = 0;
+  // off-diagonal extraction (built on first request, find_plan_offdiag_pairs)
+  bool off_ready = false;
+  std::vector<int64_t> off_u, off_v;        // directed adjacent pairs, (u, v) ascending
+  std::vector<findb200::OffItem> off_items; // grouped by final elimination
+  std::vector<int64_t> off_item_off;        // [n_elims + 1]
+  void* d_off_items = nullptr;
+  void* d_off_item_off = nullptr;
+  int off_device = -1;
   // device copies (owned), set by find_plan_upload
   int device = -1;
   void* d_elims = nullptr;

@@ -132,7 +132,23 @@ class Plan:
         return int(_native.lib().find_solve_launch_count(self._h, int(n_energies)))
 
     KIND_NAMES = ("warp", "gatherA", "panel", "trsm", "trail", "xsolve", "finish", "gatherS", "tgemm", "rgemm", "final",
-                  "schur", "lu_fused", "mid")
+                  "schur", "lu_fused", "mid", "offdiag")
+
+    def offdiag_pairs(self) -> np.ndarray:
+        """Directed adjacent pairs [n_pairs, 2] (u, v), u != v, ascending: the index space of the
+        off-diagonal outputs (a.adjacency(), operators.py:84-93; solver.py:454-484)."""
+        pr = self.cache.get("offdiag_pairs")
+        if pr is None:
+            L = _native.lib()
+            k = L.find_plan_offdiag_pairs(self._h, None, None, 0)
+            if k < 0:
+                raise NativeLibraryError("find_plan_offdiag_pairs failed")
+            u = np.zeros(max(k, 1), np.int64)
+            v = np.zeros(max(k, 1), np.int64)
+            L.find_plan_offdiag_pairs(self._h, _i64p(u), _i64p(v), k)
+            pr = np.stack([u[:k], v[:k]], axis=1)
+            self.cache["offdiag_pairs"] = pr
+        return pr
 
     def group_phases(self) -> np.ndarray:
         """Phase of every launch group (groups of a phase are independent; phases run in order)."""
@@ -188,11 +204,13 @@ class Plan:
             return self._ws
 
     def run(self, a_dev, s_dev, gr_dev, gl_dev, compute_gless=True, pivot_rtol=1e-12, s_broadcast=True, ws=None,
-            stream=None, groups=(0, -1), check=True, sigma_sym=0):
+            stream=None, groups=(0, -1), check=True, sigma_sym=0, off_gr=None, off_gl=None):
         """Enqueue the solve on `stream` for a_dev [nE, nnz] (torch complex128, CUDA).
 
         sigma_sym: +1 if Sigma^< is exactly Hermitian, -1 if exactly skew-Hermitian
-        (then every R block is too and only its lower triangle is computed)."""
+        (then every R block is too and only its lower triangle is computed).
+        off_gr / off_gl: optional CUDA complex128 [nE, n_pairs] outputs of G^r / G^< on
+        offdiag_pairs() (find_solve_offdiag)."""
         import torch
 
         L = _native.lib()
@@ -204,11 +222,17 @@ class Plan:
         if stream is None:
             stream = torch.cuda.current_stream(a_dev.device)
         st = _native.FindStatus()
-        rc = L.find_solve_groups(
-            self._h, C.c_void_p(a_dev.data_ptr()), C.c_void_p(s_dev.data_ptr() if s_dev is not None else 0),
-            int(s_broadcast), n_e, (0 if not compute_gless else {1: 2, -1: 3}.get(int(sigma_sym), 1)), float(pivot_rtol), C.c_void_p(gr_dev.data_ptr()),
-            C.c_void_p(gl_dev.data_ptr() if gl_dev is not None else 0), C.c_void_p(ws.data_ptr()), ws.numel(),
-            int(groups[0]), int(groups[1]), C.c_void_p(stream.cuda_stream), C.byref(st))
+        cg = 0 if not compute_gless else {1: 2, -1: 3}.get(int(sigma_sym), 1)
+        head = (self._h, C.c_void_p(a_dev.data_ptr()), C.c_void_p(s_dev.data_ptr() if s_dev is not None else 0),
+                int(s_broadcast), n_e, cg, float(pivot_rtol), C.c_void_p(gr_dev.data_ptr()),
+                C.c_void_p(gl_dev.data_ptr() if gl_dev is not None else 0))
+        tail = (C.c_void_p(ws.data_ptr()), ws.numel(), int(groups[0]), int(groups[1]), C.c_void_p(stream.cuda_stream),
+                C.byref(st))
+        if off_gr is None:
+            rc = L.find_solve_groups(*head, *tail)
+        else:
+            rc = L.find_solve_offdiag_groups(*head, C.c_void_p(off_gr.data_ptr()),
+                                             C.c_void_p(off_gl.data_ptr() if off_gl is not None else 0), *tail)
         if rc != _native.FIND_OK:
             if rc == _native.FIND_EINVAL:
                 raise ValueError(st.text)

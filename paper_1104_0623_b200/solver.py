@@ -52,6 +52,9 @@ class SelectedInverse:
     ledger: FlopLedger
     timings: dict = field(default_factory=dict)
     stats: dict = field(default_factory=dict)
+    # beyond the reference fields: G^< on the same adjacent pairs as ``offdiag`` (the
+    # reference computes these only inside _extended_extraction, solver.py:487-507)
+    offdiag_gless: dict | None = None
 
 
 @dataclass
@@ -63,6 +66,9 @@ class SelectedInverseBatch:
     ledger: FlopLedger  # per energy point
     timings: dict = field(default_factory=dict)
     stats: dict = field(default_factory=dict)
+    offdiag_pairs: np.ndarray | None = None  # [n_pairs, 2] directed adjacent pairs (u, v), ascending
+    offdiag_gr: np.ndarray | None = None     # [nE, n_pairs] G^r(u, v)
+    offdiag_gless: np.ndarray | None = None  # [nE, n_pairs] G^<(u, v)
 
 
 def _csr_sorted(m) -> sp.csr_matrix:
@@ -166,9 +172,6 @@ def _validate(mesh, a, sigma, config, plan_cache: dict | None = None):
             raise ValueError("ldlt kernel requires a (complex-)symmetric operator")
     elif config.use_symmetry and not is_hermitian(a.matrix):
         raise ValueError("use_symmetry requires a Hermitian operator")
-    if config.compute_offdiag or config.tiling != "full-leaves":
-        raise NotImplementedError(
-            "off-diagonal extraction and half-leaves tiling are not in this build (SURVEY.md §8(f) row 1)")
 
 
 def _device():
@@ -180,12 +183,14 @@ def _device():
 
 
 def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, compute_gless=True, pivot_rtol=1e-12,
-                 sigma_sym=0, max_chunk: int | None = None):
+                 sigma_sym=0, max_chunk: int | None = None, compute_offdiag=False, offdiag_out: dict | None = None):
     """Run the plan on host value arrays a_vals [nE, nnz], s_vals [nnz] or [nE, nnz].
 
     Energy points are processed in chunks sized to the free device memory (one
     find_solve per chunk); per chunk: host -> device copies, the level-batched
     kernels, status check, device -> host copy of the diagonals.
+    With compute_offdiag, G^r (and G^< when compute_gless) on plan.offdiag_pairs() are
+    stored into offdiag_out["gr"] / ["gl"] ([nE, n_pairs]).
     Returns (gr, gl, device_seconds_up, device_seconds_down)."""
     import torch
 
@@ -198,6 +203,8 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
         s_b = s_vals.ndim == 1
     per_energy = plan.workspace_bytes(2, compute_gless) - plan.workspace_bytes(1, compute_gless)
     per_energy += (plan.nnz + 2 * plan.n) * 16
+    n_pairs = plan.offdiag_pairs().shape[0] if compute_offdiag else 0
+    per_energy += 2 * n_pairs * 16
     free, _ = torch.cuda.mem_get_info(dev)
     held = plan._ws.numel() if plan._ws is not None and plan._ws.device == dev else 0
     chunk = max(1, min(n_e, int((0.85 * (free + held) - plan.workspace_bytes(1, compute_gless) + per_energy) // per_energy)))
@@ -208,6 +215,9 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
     gl = np.empty((n_e, plan.n), np.complex128) if compute_gless else None
     s_all = torch.from_numpy(s_vals).to(dev, non_blocking=True) if (compute_gless and s_b) else None
     a_host = plan.pinned_tensor(a_vals) if plan.is_pinned_view(a_vals) else torch.from_numpy(a_vals)
+    if compute_offdiag:
+        offdiag_out["gr"] = np.empty((n_e, n_pairs), np.complex128)
+        offdiag_out["gl"] = np.empty((n_e, n_pairs), np.complex128) if compute_gless else None
     t_up = t_down = 0.0
     for k0 in range(0, n_e, chunk):
         k1 = min(n_e, k0 + chunk)
@@ -215,13 +225,17 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
         s_d = s_all if s_b else (torch.from_numpy(s_vals[k0:k1]).to(dev) if compute_gless else None)
         gr_d = torch.empty((k1 - k0, plan.n), dtype=torch.complex128, device=dev)
         gl_d = torch.empty((k1 - k0, plan.n), dtype=torch.complex128, device=dev) if compute_gless else None
+        og_d = ol_d = None
+        if compute_offdiag:
+            og_d = torch.empty((k1 - k0, max(n_pairs, 1)), dtype=torch.complex128, device=dev)
+            ol_d = torch.empty_like(og_d) if compute_gless else None
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
         ws = plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, stream=stream,
                       groups=(0, plan.first_down_group), sigma_sym=sigma_sym)
         ev[1].record(stream)
         plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, ws=ws, stream=stream,
-                 groups=(plan.first_down_group, -1), sigma_sym=sigma_sym)
+                 groups=(plan.first_down_group, -1), sigma_sym=sigma_sym, off_gr=og_d, off_gl=ol_d)
         ev[2].record(stream)
         out_h = plan.host_outputs(k1 - k0, compute_gless)
         out_h[0].copy_(gr_d, non_blocking=True)
@@ -236,6 +250,10 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
         gr[k0:k1] = out_h[0].numpy()
         if compute_gless:
             gl[k0:k1] = out_h[1].numpy()
+        if compute_offdiag:
+            offdiag_out["gr"][k0:k1] = og_d[:, :n_pairs].cpu().numpy()
+            if compute_gless:
+                offdiag_out["gl"][k0:k1] = ol_d[:, :n_pairs].cpu().numpy()
         t_up += ev[0].elapsed_time(ev[1]) * 1e-3
         t_down += ev[1].elapsed_time(ev[2]) * 1e-3
         del a_d, gr_d, gl_d
@@ -249,13 +267,78 @@ def _stats(plan: Plan, a_data: np.ndarray) -> dict:
     }
 
 
+def _leaf_table(plan: Plan):
+    """(final-step indices, leaf rectangles [x0, y0, w, h]) in plan order, cached."""
+    t = plan.cache.get("leaf_table")
+    if t is None:
+        fin = np.nonzero(plan.kind == 3)[0]
+        rect = np.zeros((fin.size, 4), np.int64)
+        for i, k in enumerate(fin):
+            nodes = plan.cluster_set(int(plan.label[k]), 0)
+            x, y = nodes % plan.nx, nodes // plan.nx
+            rect[i] = (x.min(), y.min(), x.max() - x.min() + 1, y.max() - y.min() + 1)
+        t = (fin, rect)
+        plan.cache["leaf_table"] = t
+    return t
+
+
+def half_leaves_selection(plan: Plan):
+    """select_tiling(tree, "half-leaves") (solver.py:522-556): boolean mask over the final
+    steps, or None when the reference falls back to full-leaves (with its warning)."""
+    import warnings
+
+    fin, rect = _leaf_table(plan)
+    shapes = {(int(w), int(h)) for w, h in rect[:, 2:]}
+    if len(shapes) != 1:
+        warnings.warn("non-uniform leaves; falling back to full-leaves tiling")
+        return None
+    lw, lh = shapes.pop()
+    if max(lw, lh) > 2:
+        warnings.warn("half-leaves tiling needs leaves of side <= 2; using full-leaves")
+        return None
+    ntx, nty = plan.nx // lw, plan.ny // lh
+    ti, tj = rect[:, 0] // lw, rect[:, 1] // lh
+    on_edge = (ti == 0) | (tj == 0) | (ti == ntx - 1) | (tj == nty - 1)
+    return on_edge | ((ti + tj) % 2 == 0)
+
+
 def _ledger_cached(plan: Plan, config, sigma_herm: bool) -> FlopLedger:
-    key = ("ledger", config.kernel, bool(config.compute_gless), bool(sigma_herm), config.sigma_mode)
+    """The reference's FlopLedger for this config: merges as charged by the kernel
+    dispatch; leaf extraction as full-leaves (final step, inverse, sandwich and, with
+    compute_offdiag, offdiag_backsub, solver.py:475) or half-leaves (one dense inverse
+    and sandwich of ring+leaf per selected leaf, solver.py:487-507)."""
+    half = config.tiling == "half-leaves"
+    key = ("ledger", config.kernel, bool(config.compute_gless), bool(sigma_herm), config.sigma_mode,
+           bool(config.compute_offdiag), half)
     led = plan.cache.get(key)
     if led is None:
-        led = plan.ledger(config.kernel, config.compute_gless, sigma_herm, config.sigma_mode)
+        sel = half_leaves_selection(plan) if half else None
+        if sel is None:
+            led = plan.ledger(config.kernel, config.compute_gless, sigma_herm, config.sigma_mode)
+            if config.compute_offdiag:
+                fin = plan.kind == 3
+                t = plan.s[fin].astype(object)
+                c = plan.b[fin].astype(object)
+                m = t > 0
+                if m.any():
+                    led.add("offdiag_backsub", 2 * int(np.sum(t[m] ** 2 * c[m] + t[m] * c[m] ** 2)))
+        else:
+            from .ledger import plan_ledger
+
+            nf = plan.kind != 3
+            led = plan_ledger(plan.kind[nf], plan.s[nf], plan.b[nf], config.kernel, config.compute_gless, sigma_herm,
+                              config.sigma_mode)
+            fin, _ = _leaf_table(plan)
+            m = (plan.s[fin] + plan.b[fin])[sel].astype(object)
+            led.add("dense_inverse", int(np.sum(m ** 3)))
+            if config.compute_gless:
+                led.add("gless_sandwich", 2 * int(np.sum(m ** 3)))
         plan.cache[key] = led
     return FlopLedger(led.multiplications, dict(led.by_kernel))
+
+
+def _offdiag_dict(pairs: np.ndarray, vals: np.ndarray) -> dict:
+    return dict(zip(map(tuple, pairs.tolist()), vals.tolist()))
 
 
 def _prepare(mesh, a_list, sigma, config):
@@ -287,15 +370,25 @@ def solve(mesh, a, sigma, config: SolverConfig) -> SelectedInverse:
     t0 = time.perf_counter()
     plan, am, vals, s_vals, ssym, sherm = _prepare(mesh, [a], sigma, config)
     t1 = time.perf_counter()
-    gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol, ssym)
+    off = {}
+    gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol, ssym,
+                                        compute_offdiag=config.compute_offdiag, offdiag_out=off)
+    led = _ledger_cached(plan, config, sherm)
+    offd = offl = None
+    if config.compute_offdiag:
+        pairs = plan.offdiag_pairs()
+        offd = _offdiag_dict(pairs, off["gr"][0])
+        if off.get("gl") is not None:
+            offl = _offdiag_dict(pairs, off["gl"][0])
     t3 = time.perf_counter()
     return SelectedInverse(
         gr_diag=gr[0],
         gless_diag=gl[0] if gl is not None else None,
-        offdiag=None,
-        ledger=_ledger_cached(plan, config, sherm),
+        offdiag=offd,
+        ledger=led,
         timings={"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},
         stats=_stats(plan, am.data),
+        offdiag_gless=offl,
     )
 
 
@@ -305,8 +398,15 @@ def solve_batch(mesh, a_list, sigma, config: SolverConfig) -> SelectedInverseBat
     t0 = time.perf_counter()
     plan, am0, vals, s_vals, ssym, sherm = _prepare(mesh, list(a_list), sigma, config)
     t1 = time.perf_counter()
-    gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol, ssym)
+    off = {}
+    gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol, ssym,
+                                        compute_offdiag=config.compute_offdiag, offdiag_out=off)
     t3 = time.perf_counter()
-    return SelectedInverseBatch(gr, gl, _ledger_cached(plan, config, sherm),
-                                {"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},
-                                _stats(plan, am0.data))
+    res = SelectedInverseBatch(gr, gl, _ledger_cached(plan, config, sherm),
+                               {"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},
+                               _stats(plan, am0.data))
+    if config.compute_offdiag:
+        res.offdiag_pairs = plan.offdiag_pairs()
+        res.offdiag_gr = off["gr"]
+        res.offdiag_gless = off.get("gl")
+    return res

@@ -142,7 +142,90 @@ def set_cases():
         print("wrote", name)
 
 
+def _ref_extended_gless(mesh, a, s, leaf_max):
+    """G^< on every directed adjacent pair, from the reference's own ring+leaf
+    extraction (_extended_extraction, solver.py:487-507) run on each leaf in the
+    downward DFS, keeping the pairs full-leaves extraction owns (first writer,
+    solver.py:666-669): pairs inside the leaf and between the leaf and its ring."""
+    from find_selinv import solver as rs
+
+    cfg = ref.SolverConfig(kernel="naive", compute_gless=True, leaf_max=leaf_max)
+    tree = build_cluster_tree(mesh, leaf_max)
+    adj = a.adjacency()
+    annotate_boundaries(tree, adj)
+    comps = complement_boundary_sets(tree, adj)
+    led = ref.FlopLedger()
+    engine = rs._Engine(a, s, tree, comps, cfg, led)
+    pos = rs.upward_pass(tree, a, s, cfg, engine=engine)
+    out = {}
+
+    def on_leaf(leaf, neg):
+        g_t, gl_t, labels = rs._extended_extraction(engine, leaf, neg, True)
+        t = labels.size - leaf.nodes.size
+        region = adj[labels][:, labels].tocoo()
+        for i, j in zip(region.row, region.col):
+            if i < t and j < t:
+                continue  # ring-ring pairs belong to other leaves under full-leaves
+            key = (int(labels[i]), int(labels[j]))
+            if key not in out:
+                out[key] = complex(gl_t[i, j])
+
+    rs.downward_pass(tree, a, s, pos, cfg, engine=engine, leaf_callback=on_leaf, keep_all=False)
+    return out
+
+
+def offdiag_cases():
+    """Off-diagonal G^r (reference solve, compute_offdiag, both tilings) and G^< (reference
+    _extended_extraction) on contact-style and general-Sigma problems."""
+    cases = {
+        "off_c5_10x8": (build_problem(10, 8, [0.9, 2.2], seed=21, stencil=5), 2, False),
+        "off_c9_9x7": (build_problem(9, 7, [1.7], seed=22, stencil=9), 2, False),
+        "off_c5_7x9_lm3": (build_problem(7, 9, [1.1], seed=23, stencil=5), 3, False),
+        "off_gen_8x8": (build_problem(8, 8, [1.4], seed=24, stencil=5), 2, True),
+    }
+    for name, (p, lm, general) in cases.items():
+        mesh = ref.Mesh(p.nx, p.ny)
+        s_csr = p.sigma_csr()
+        if general:  # a non-Hermitian Sigma on the same pattern: exercises the general G^< path
+            rng = np.random.default_rng(99)
+            s_csr = s_csr.copy()
+            s_csr.data = s_csr.data + 0.3 * (rng.standard_normal(s_csr.nnz) + 1j * rng.standard_normal(s_csr.nnz))
+        pairs = None
+        gr_full, gr_half, gl_ext = [], [], []
+        led = {}
+        for k in range(p.energies.size):
+            a_op = SparseOperator(p.a_csr(k))
+            s_op = SparseOperator(s_csr)
+            rf = ref.solve(mesh, a_op, s_op, ref.SolverConfig(kernel="naive", compute_gless=True, compute_offdiag=True,
+                                                              leaf_max=lm))
+            rh = ref.solve(mesh, a_op, s_op, ref.SolverConfig(kernel="naive", compute_gless=True, compute_offdiag=True,
+                                                              tiling="half-leaves", leaf_max=lm))
+            if pairs is None:
+                pairs = np.array(sorted(rf.offdiag), dtype=np.int64)
+                led = {"W_full": frac(rf.ledger.multiplications), "W_half": frac(rh.ledger.multiplications)}
+            gr_full.append([rf.offdiag[tuple(q)] for q in pairs.tolist()])
+            gr_half.append([rh.offdiag[tuple(q)] for q in pairs.tolist()])
+            ext = _ref_extended_gless(mesh, a_op, s_op, lm)
+            gl_ext.append([ext[tuple(q)] for q in pairs.tolist()])
+            A = a_op.to_dense()
+            G = np.linalg.inv(A)
+            GL = G @ s_op.to_dense() @ G.conj().T
+            print(name, k, "ref gr vs dense", np.abs(np.array(gr_full[-1]) - G[pairs[:, 0], pairs[:, 1]]).max(),
+                  "ext gl vs dense", np.abs(np.array(gl_ext[-1]) - GL[pairs[:, 0], pairs[:, 1]]).max())
+        np.savez_compressed(HERE / f"{name}.npz", nx=p.nx, ny=p.ny, leaf_max=lm, indptr=p.indptr, indices=p.indices,
+                            h_vals=p.h_vals, diag_pos=p.diag_pos, s_data=s_csr.data, s_indices=s_csr.indices,
+                            s_indptr=s_csr.indptr, energies=p.energies, pairs=pairs, gr_full=np.array(gr_full),
+                            gr_half=np.array(gr_half), gl_ext=np.array(gl_ext), allow_pickle=True, **led)
+        print("wrote", name, pairs.shape[0], "pairs")
+
+
 if __name__ == "__main__":
-    set_cases()
-    stencil_cases()
-    contact_cases()
+    import sys as _sys
+
+    if "offdiag" in _sys.argv:
+        offdiag_cases()
+    else:
+        set_cases()
+        stencil_cases()
+        contact_cases()
+        offdiag_cases()
