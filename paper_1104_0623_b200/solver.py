@@ -120,8 +120,21 @@ def _transpose_slots(plan: Plan) -> np.ndarray:
 
 def _sigma_prepare(plan: Plan, am: sp.csr_matrix, sigma) -> tuple[np.ndarray, int, bool]:
     """Sigma on A's pattern, its exact (skew-)Hermitian symmetry, and the reference's
-    tolerance-based is_hermitian (operators.py:98-103), with pattern maps cached per plan."""
+    tolerance-based is_hermitian (operators.py:98-103).  The result of the last call is
+    reused when Sigma's pattern and values are bit-identical (three memcmp-speed
+    comparisons), as in an energy sweep that passes the same Sigma every time."""
     sm = _csr_sorted(sigma.matrix)
+    last = plan.cache.get("sigma_last")
+    if (last is not None and last[0].size == sm.indptr.size and last[1].size == sm.indices.size
+            and np.array_equal(last[0], sm.indptr) and np.array_equal(last[1], sm.indices)
+            and np.array_equal(last[2], sm.data)):
+        return last[3]
+    out = _sigma_prepare_full(plan, sm)
+    plan.cache["sigma_last"] = (sm.indptr.copy(), sm.indices.copy(), sm.data.copy(), out)
+    return out
+
+
+def _sigma_prepare_full(plan: Plan, sm: sp.csr_matrix) -> tuple[np.ndarray, int, bool]:
     import hashlib
 
     h = hashlib.sha1(np.ascontiguousarray(sm.indptr, np.int64).tobytes())
@@ -261,9 +274,16 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
 
 
 def _stats(plan: Plan, a_data: np.ndarray) -> dict:
+    """solver.py:186, 217-219: structure-exception entries of A that are nonzero."""
+    occ = plan.cache.get("exception_occ")
+    if occ is None:  # how often each CSR slot is an exception entry, per pass
+        occ = tuple(np.bincount(plan.exception_slots(k), minlength=plan.nnz).astype(np.int64) for k in (0, 1))
+        plan.cache["exception_occ"] = occ
+    f = a_data.view(np.float64)
+    nz = (f[0::2] != 0) | (f[1::2] != 0)
     return {
-        "upward_exception_entries": int(np.count_nonzero(a_data[plan.exception_slots(0)])),
-        "downward_exception_entries": int(np.count_nonzero(a_data[plan.exception_slots(1)])),
+        "upward_exception_entries": int(np.dot(nz, occ[0])),
+        "downward_exception_entries": int(np.dot(nz, occ[1])),
     }
 
 
