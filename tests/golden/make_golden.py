@@ -219,13 +219,39 @@ def offdiag_cases():
         print("wrote", name, pairs.shape[0], "pairs")
 
 
+def io_cases():
+    """Matrix Market files written by the reference (operators.py:222-230) and its CSV
+    exports (solver.py:709-734) of one reference result, for byte-level format checks."""
+    from find_selinv.operators import write_matrix_market
+    from find_selinv.solver import diag_to_csv, offdiag_to_csv
+
+    p = build_problem(6, 5, [1.2], seed=41, stencil=5)
+    mesh = ref.Mesh(p.nx, p.ny)
+    a = SparseOperator(p.a_csr(0))
+    s = SparseOperator(p.sigma_csr())
+    write_matrix_market(HERE / "io_a_mesh.mtx", a, mesh)
+    write_matrix_market(HERE / "io_a_plain.mtx", a)
+    r = ref.solve(mesh, a, s, ref.SolverConfig(compute_gless=True, compute_offdiag=True))
+    keys = np.array(sorted(r.offdiag), dtype=np.int64)
+    np.savez_compressed(HERE / "io_csv.npz", nx=p.nx, ny=p.ny, gr=r.gr_diag, gl=r.gless_diag, off_keys=keys,
+                        off_vals=np.array([r.offdiag[tuple(k)] for k in keys.tolist()]),
+                        diag_csv=np.array(diag_to_csv(r, mesh)), offdiag_csv=np.array(offdiag_to_csv(r)))
+    r2 = ref.solve(mesh, a, None, ref.SolverConfig(compute_gless=False))
+    np.savez_compressed(HERE / "io_csv_nogless.npz", gr=r2.gr_diag, diag_csv=np.array(diag_to_csv(r2, mesh)),
+                        offdiag_csv=np.array(offdiag_to_csv(r2)))
+    print("wrote io cases")
+
+
 if __name__ == "__main__":
     import sys as _sys
 
-    if "offdiag" in _sys.argv:
+    if "io" in _sys.argv:
+        io_cases()
+    elif "offdiag" in _sys.argv:
         offdiag_cases()
     else:
         set_cases()
         stencil_cases()
         contact_cases()
         offdiag_cases()
+        io_cases()
