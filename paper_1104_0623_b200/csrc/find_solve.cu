@@ -792,16 +792,24 @@ __device__ void gather_body(const SolveParams& P, const Task& t, int e) {
   }
   __syncthreads();
   const SparseEntry* sp = P.sparse + d.sparse_off;
-  for (int ri = 0; ri < nr; ++ri) {
+  // rows in merged order (A, and the B rows of Sigma) own one contiguous range of the
+  // sparse list: one flat loop; pivot-permuted Sigma S rows one range per row
+  const int flat0 = SIGMA ? max(r0, min(s, r0 + nr)) : r0;
+  for (int ri = 0; ri < flat0 - r0; ++ri) {
     const int i = r0 + ri;
-    const int mr = (SIGMA && i < s) ? S.SIG[i] : i;
+    const int mr = S.SIG[i];
     for (int q = rowoff[mr] + threadIdx.x; q < rowoff[mr + 1]; q += kThreads) {
       const SparseEntry en = sp[q];
-      const int j = (SIGMA && en.j < s) ? S.ISG[en.j] : en.j;
+      const int j = en.j < s ? S.ISG[en.j] : en.j;
       dst[(int64_t)i * n + j] = ldg2(vals + en.csr);
     }
   }
-  if (!SIGMA) {  // partial pivot scale max |A(S,S)| of these rows (kernels.py:241)
+  for (int q = rowoff[flat0] + threadIdx.x; q < rowoff[r0 + nr]; q += kThreads) {
+    const SparseEntry en = sp[q];
+    const int j = (SIGMA && en.j < s) ? S.ISG[en.j] : en.j;
+    dst[(int64_t)en.i * n + j] = ldg2(vals + en.csr);
+  }
+  if (!SIGMA && r0 < s) {  // partial pivot scale max |A(S,S)| of these rows (kernels.py:241)
     __shared__ double cv[kThreads / 32];
     __shared__ int ci[kThreads / 32];
     __syncthreads();
@@ -2246,8 +2254,8 @@ int set_attrs(find_status* st) {
 // kSideStreams at normal priority and kHiStreams at the device's greatest
 // priority for the groups on the phase's critical path (the longest launch
 // chains), whose CTAs the scheduler then places first.
-constexpr int kSideStreams = 8;
-constexpr int kHiStreams = 4;
+constexpr int kSideStreams = 16;
+constexpr int kHiStreams = 8;
 struct SideStreams {
   int device = -1;
   cudaStream_t s[kSideStreams + kHiStreams] = {};

@@ -218,7 +218,12 @@ namespace {
 
 constexpr int32_t kSmallMaxN = 32;  // warp-per-elimination path up to this merged size
 constexpr int32_t kMidMaxN = 64;    // CTA-per-elimination shared-memory path up to this merged size
-constexpr int32_t kLanes = 4;       // concurrent sub-groups per blocked-path size class
+constexpr int32_t kLanesDefault = 4;  // concurrent sub-groups per blocked-path size class
+int32_t lanes_setting() {  // FIND_B200_LANES overrides (tuning experiments)
+  const char* f = std::getenv("FIND_B200_LANES");
+  const int v = f ? std::atoi(f) : 0;
+  return v >= 1 && v <= 16 ? v : kLanesDefault;
+}
 
 struct Builder {
   find_plan* P;
@@ -531,7 +536,7 @@ struct Builder {
         // streams, so one lane's latency-bound panel steps overlap another lane's DMMA
         // tiles); each lane further split so one group's scratch stays under the cap
         const int64_t cnt = ce - cb;
-        const int lanes = (int)std::min<int64_t>(kLanes, std::max<int64_t>(1, cnt / 2));
+        const int lanes = (int)std::min<int64_t>(lanes_setting(), std::max<int64_t>(1, cnt / 2));
         if (lanes > 1) {
           std::vector<ElimDesc> tmp(P->elims.begin() + cb, P->elims.begin() + ce);
           int64_t w = cb;
