@@ -166,7 +166,7 @@ int find_plan_groups(const find_plan* plan, int32_t* pass, int32_t* level, int32
 /* Kernel-launch table of a find_solve over n_energies points, in issue order
  * (find_solve_launch_count() entries): launch kind (0 warp path, 1 gather A,
  * 2 panel, 3 TRSM, 4 trailing, 5 X solve, 6 finish, 7 gather Sigma, 8 T_S,
- * 9 R, 10 final, 11 Schur, 12 fused LU, 13 mid path, 14 off-diagonal), panel step, launch
+ * 9 R, 10 final, 11 Schur, 12 fused LU, 13 mid path, 14 off-diagonal, 15 panel inverses), panel step, launch
  * group, task count.  Any pointer may be NULL. */
 int find_plan_specs(const find_plan* plan, int32_t n_energies, int32_t* kind, int32_t* step, int32_t* group,
                     int64_t* tasks);

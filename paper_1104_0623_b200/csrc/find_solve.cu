@@ -1433,7 +1433,7 @@ template <>
 struct TrsmTiles<4> { using U = Tile<1, 8, 1, 1, false>; using L = Tile<8, 1, 1, 1, false>; };
 
 template <int NB>
-__device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, double2* smem) {
+__device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, double2* smem, bool inv_ready = false) {
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s;
   const int j0 = j * NB, jb = min(NB, s - j0);
@@ -1457,8 +1457,8 @@ __device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, dou
     __syncthreads();
     if (t.a == 2) return;
   }
-  {  // the diagonal block's inverse this tile needs (L for U12 tiles, U for L21 tiles), published to the
-     // elimination's LINV/UINV slot; every tile of the elimination writes the same values
+  if (!inv_ready) {  // the diagonal block's inverse this tile needs (L for U12 tiles, U for L21 tiles),
+     // published to the elimination's LINV/UINV slot; every tile of the elimination writes the same values
     typedef double2 Row[NB + 1];
     Row* Dm = reinterpret_cast<Row*>(smem);
     Row* Xm = Dm + NB;
@@ -1501,10 +1501,43 @@ __device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, dou
 }
 
 template <int NB>
-__global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Task* tasks, int j) {
+__global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Task* tasks, int j, int inv_ready) {
   pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  trsm_body<NB>(P, tasks[blockIdx.x], blockIdx.y, j, reinterpret_cast<double2*>(smem_raw));
+  trsm_body<NB>(P, tasks[blockIdx.x], blockIdx.y, j, reinterpret_cast<double2*>(smem_raw), inv_ready != 0);
+}
+
+// ---- L_jj^-1 and U_jj^-1 of panel j, once per (elimination, energy), published to LINV / UINV
+template <int NB>
+__global__ void __launch_bounds__(kThreads) panel_inv_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y, j = t.a;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s;
+  const int j0 = j * NB, jb = min(NB, s - j0);
+  const Scr S = scratch_of(P, d, e, NB);
+  typedef double2 Row[NB + 1];
+  Row* Dm = reinterpret_cast<Row*>(smem_raw);
+  Row* Xm = Dm + NB;
+  Row* Wm = Xm + NB;
+  for (int q = threadIdx.x; q < NB * NB; q += kThreads) {
+    const int r = q / NB, c = q % NB;
+    Dm[r][c] = (r < jb && c < jb) ? S.M[(int64_t)(j0 + r) * n + j0 + c] : cz();
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 0) block_tri_inverse<NB, true>(Dm, jb, Xm, Wm);
+    else block_tri_inverse<NB, false>(Dm, jb, Xm, Wm);
+    double2* out = (pass == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
+    for (int q = threadIdx.x; q < NB * NB; q += kThreads) {
+      const int r = q / NB, c = q % NB;
+      out[q] = (r < jb && c < jb) ? Xm[r][c] : cz();
+    }
+    __syncthreads();
+  }
 }
 
 // ---- trailing update M[j1:, j1:] -= M[j1:, j0:j1] M[j0:j1, j1:]
@@ -2227,6 +2260,8 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<4>()));
+  CUDA_TRY(cudaFuncSetAttribute(panel_inv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(3 * 32 * 33 * sizeof(double2))));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<4>()));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<32>()));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<16>()));
@@ -2297,6 +2332,13 @@ const int g_panel_mode = [] {
   const char* m = std::getenv("FIND_B200_SMEM_PANEL");
   if (m && m[0] == '1') return 2;
   return 0;
+}();
+
+// Diagonal-block inverses once per (elimination, panel) in their own launch (default), or
+// recomputed by every TRSM tile that needs one (FIND_B200_INV_LAUNCH=0).
+const bool g_inv_launch = [] {
+  const char* f = std::getenv("FIND_B200_INV_LAUNCH");
+  return !(f && f[0] == '0');
 }();
 
 // Fused-LU launches (one CTA per elimination and energy) instead of the
@@ -2433,6 +2475,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
     for (int64_t si = fused ? G.fspec_begin : G.spec_begin; si < (fused ? G.fspec_end : G.spec_end); ++si) {
       const LaunchSpec& L = P->specs[si];
       if (!prm.compute_gless && (L.kind == kLGatherS || L.kind == kLTGemm)) continue;
+      if (L.kind == kLPanelInv && !g_inv_launch) continue;
       const Task* tk = dtasks + L.task_off;
       const unsigned cnt = (unsigned)L.task_count;
       const dim3 grid(cnt, (unsigned)nE);
@@ -2496,13 +2539,21 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           else launch_k(panel_smem_kernel<4>, grid, kThreads, (size_t)G.max_s * 5 * sizeof(double2), stream, prm, tk);
           break;
         }
-        case kLTrsm:
-          if (L.nb == 32)
-            launch_k(trsm_kernel<32>, grid, kThreads, trsm_smem<32>(), stream, prm, tk, L.step);
-          else if (L.nb == 16) launch_k(trsm_kernel<16>, grid, kThreads, trsm_smem<16>(), stream, prm, tk, L.step);
-          else if (L.nb == 8) launch_k(trsm_kernel<8>, grid, kThreads, trsm_smem<8>(), stream, prm, tk, L.step);
-          else launch_k(trsm_kernel<4>, grid, kThreads, trsm_smem<4>(), stream, prm, tk, L.step);
+        case kLPanelInv:
+          if (L.nb == 32) launch_k(panel_inv_kernel<32>, grid, kThreads, 3 * 32 * 33 * sizeof(double2), stream, prm, tk);
+          else if (L.nb == 16) launch_k(panel_inv_kernel<16>, grid, kThreads, 3 * 16 * 17 * sizeof(double2), stream, prm, tk);
+          else if (L.nb == 8) launch_k(panel_inv_kernel<8>, grid, kThreads, 3 * 8 * 9 * sizeof(double2), stream, prm, tk);
+          else launch_k(panel_inv_kernel<4>, grid, kThreads, 3 * 4 * 5 * sizeof(double2), stream, prm, tk);
           break;
+        case kLTrsm: {
+          const int ir = g_inv_launch ? 1 : 0;  // inverses published by the kLPanelInv launch
+          if (L.nb == 32)
+            launch_k(trsm_kernel<32>, grid, kThreads, trsm_smem<32>(), stream, prm, tk, L.step, ir);
+          else if (L.nb == 16) launch_k(trsm_kernel<16>, grid, kThreads, trsm_smem<16>(), stream, prm, tk, L.step, ir);
+          else if (L.nb == 8) launch_k(trsm_kernel<8>, grid, kThreads, trsm_smem<8>(), stream, prm, tk, L.step, ir);
+          else launch_k(trsm_kernel<4>, grid, kThreads, trsm_smem<4>(), stream, prm, tk, L.step, ir);
+          break;
+        }
         case kLTrail: launch_k(trail_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.step, L.nb); break;
         case kLXSolve:
           if (L.nb == 32) launch_k(xsolve_kernel<32>, grid, kThreads, xsolve_smem<32>(), stream, prm, tk);
@@ -2564,8 +2615,10 @@ template <class F>
 void for_each_launch(const find_plan* P, int nE, F f) {
   for (const LaunchGroup& G : P->groups) {
     const bool fu = use_fused(G, nE);
-    for (int64_t si = fu ? G.fspec_begin : G.spec_begin; si < (fu ? G.fspec_end : G.spec_end); ++si)
+    for (int64_t si = fu ? G.fspec_begin : G.spec_begin; si < (fu ? G.fspec_end : G.spec_end); ++si) {
+      if (P->specs[si].kind == kLPanelInv && !g_inv_launch) continue;
       f(P->specs[si].kind, P->specs[si].step, P->specs[si].group, P->specs[si].task_count);
+    }
   }
 }
 

@@ -115,6 +115,11 @@ void find_build_tasks(find_plan* P) {
       for (int64_t e = G.begin; e < G.end; ++e)
         if (P->elims[e].s > j * nb) push((int32_t)e, j, 0, 0);
       spec(kLPanel, j, nb, gi, off);
+      {  // the diagonal block's inverses, once per (elimination, panel), for the TRSM and X-solve tiles
+        LaunchSpec L = P->specs.back();
+        L.kind = kLPanelInv;
+        P->specs.push_back(L);
+      }
       off = (int64_t)P->tasks.size();
       for (int64_t e = G.begin; e < G.end; ++e) {
         const ElimDesc& d = P->elims[e];

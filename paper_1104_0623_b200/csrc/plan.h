@@ -54,6 +54,7 @@ enum LaunchKind : int32_t {
   kLLuFused = 12,  // whole blocked LU + X + sigma in one CTA    tasks {e}
   kLMid = 13,      // CTA-per-elimination smem kernel (32 < s+b <= 64)
   kLOffdiag = 14,  // off-diagonal G^r / G^< of a final group (after its final launch)
+  kLPanelInv = 15, // diagonal-block inverses L_jj^-1, U_jj^-1 of panel j  tasks {e, j}
 };
 
 struct Task { int32_t e, a, b, c; };

@@ -132,7 +132,7 @@ class Plan:
         return int(_native.lib().find_solve_launch_count(self._h, int(n_energies)))
 
     KIND_NAMES = ("warp", "gatherA", "panel", "trsm", "trail", "xsolve", "finish", "gatherS", "tgemm", "rgemm", "final",
-                  "schur", "lu_fused", "mid", "offdiag")
+                  "schur", "lu_fused", "mid", "offdiag", "panel_inv")
 
     def offdiag_pairs(self) -> np.ndarray:
         """Directed adjacent pairs [n_pairs, 2] (u, v), u != v, ascending: the index space of the

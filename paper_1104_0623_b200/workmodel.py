@@ -12,7 +12,7 @@ from __future__ import annotations
 import numpy as np
 
 KINDS = ("warp", "gatherA", "panel", "trsm", "trail", "xsolve", "finish", "gatherS", "tgemm", "rgemm", "final",
-         "schur", "lu_fused", "mid")
+         "schur", "lu_fused", "mid", "offdiag", "panel_inv")
 TENSOR_KINDS = ("trsm", "trail", "xsolve", "tgemm", "rgemm", "schur")
 
 
