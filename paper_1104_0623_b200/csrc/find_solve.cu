@@ -509,24 +509,40 @@ __global__ void __launch_bounds__(kMidThreads) mid_elim_kernel(SolveParams P, in
       MA[(k + 1 + r) * ld + k] = l;
     }
     __syncthreads();
-    for (int q = tid; q < rows * rows; q += NT) {
-      const int r = q / rows, c = q % rows;
-      double2* p = MA + (k + 1 + r) * ld + k + 1 + c;
-      *p = cfms(*p, LC[r], MA[k * ld + k + 1 + c]);
+    {  // rank-1 update: warp = row (stride 4), lane = column (rows <= 63: two columns per lane)
+      const int warp = tid >> 5, lane = tid & 31;
+      const double2* pr_row = MA + k * ld + k + 1;
+      const double2 u0 = lane < rows ? pr_row[lane] : cz();
+      const double2 u1 = lane + 32 < rows ? pr_row[lane + 32] : cz();
+      for (int r = warp; r < rows; r += NT / 32) {
+        double2* row = MA + (k + 1 + r) * ld + k + 1;
+        const double2 l = LC[r];
+        if (lane < rows) row[lane] = cfms(row[lane], l, u0);
+        if (lane + 32 < rows) row[lane + 32] = cfms(row[lane + 32], l, u1);
+      }
     }
     __syncthreads();
   }
   if (tid == 0 && s_bad != INT32_MAX) report_bad(P, elim_global, e, s_bad);
 
-  // ---- X = Y L11^-1 (row per thread) -> XC [b][s] ----
-  for (int i = tid; i < b; i += NT) {
-    double2* rw = MA + (s + i) * ld;
-    for (int k = s - 1; k >= 0; --k) {
-      double2 acc = rw[k];
-      for (int m = k + 1; m < s; ++m) acc = cfms(acc, rw[m], MA[m * ld + k]);
-      rw[k] = acc;
+  // ---- X = Y L11^-1 -> XC [b][s]: warp per B row, lane = column (s <= 63: two per lane);
+  // column-oriented back substitution, x_k broadcast by shuffle from its owner lane
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int i = warp; i < b; i += NT / 32) {
+      const double2* rw = MA + (s + i) * ld;
+      double2 x0 = lane < s ? rw[lane] : cz();
+      double2 x1 = lane + 32 < s ? rw[lane + 32] : cz();
+      for (int k = s - 1; k >= 0; --k) {
+        const double2 own = k < 32 ? x0 : x1;
+        const double2 xk = make_double2(__shfl_sync(0xffffffffu, own.x, k & 31), __shfl_sync(0xffffffffu, own.y, k & 31));
+        const double2* lk = MA + k * ld;  // L11[k][m], m < k
+        if (lane < k) x0 = cfms(x0, xk, lk[lane]);
+        if (lane + 32 < k) x1 = cfms(x1, xk, lk[lane + 32]);
+      }
+      if (lane < s) XC[i * s + lane] = x0;
+      if (lane + 32 < s) XC[i * s + lane + 32] = x1;
     }
-    for (int k = 0; k < s; ++k) XC[i * s + k] = rw[k];
   }
   if (tid == 0) {
     for (int k = 0; k < s; ++k) sig[k] = k;
@@ -567,12 +583,17 @@ __global__ void __launch_bounds__(kMidThreads) mid_elim_kernel(SolveParams P, in
       MS[isg[en.i] * ld + isg[en.j]] = ldg2(sv + en.csr);
     }
     __syncthreads();
-    // T_S = S'_BS - X S'_SS
+    // T_S = S'_BS - X S'_SS (two accumulators: half-length dependent chains)
     for (int q = tid; q < b * s; q += NT) {
       const int i = q / s, c = q % s;
-      double2 acc = MS[(s + i) * ld + c];
-      for (int m = 0; m < s; ++m) acc = cfms(acc, XC[i * s + m], MS[m * ld + c]);
-      MS[(s + i) * ld + c] = acc;
+      double2 acc = MS[(s + i) * ld + c], acc2 = cz();
+      int m = 0;
+      for (; m + 1 < s; m += 2) {
+        acc = cfms(acc, XC[i * s + m], MS[m * ld + c]);
+        acc2 = cfma(acc2, XC[i * s + m + 1], MS[(m + 1) * ld + c]);
+      }
+      if (m < s) acc = cfms(acc, XC[i * s + m], MS[m * ld + c]);
+      MS[(s + i) * ld + c] = csub(acc, acc2);
     }
     __syncthreads();
     // R = S'_BB - X S'_SB - T_S X^H
@@ -584,11 +605,12 @@ __global__ void __launch_bounds__(kMidThreads) mid_elim_kernel(SolveParams P, in
     for (int q = tid; q < b * b; q += NT) {
       const int i = q / b, j = q % b;
       if (mirror && j > i) continue;
-      double2 acc = MS[(s + i) * ld + s + j];
+      double2 acc = MS[(s + i) * ld + s + j], acc2 = cz();
       for (int m = 0; m < s; ++m) {
         acc = cfms(acc, XC[i * s + m], MS[m * ld + s + j]);
-        acc = cfms(acc, MS[(s + i) * ld + m], cconj(XC[j * s + m]));
+        acc2 = cfma(acc2, MS[(s + i) * ld + m], cconj(XC[j * s + m]));
       }
+      acc = csub(acc, acc2);
       if (!store) {
         MS[(s + i) * ld + s + j] = acc;
       } else {
