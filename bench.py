@@ -258,19 +258,22 @@ def run_b200(args):
     ms_per_step = dev_ms / args.steps
     value = world * n_e * args.steps / (dev_ms * 1e-3)
 
-    # ---- per-launch timing (one extra instrumented step, library CUDA events around every launch)
-    #      -> roofline of the dominant kernel kind, live
+    # ---- per-launch timing: one extra instrumented step with every launch group run ALONE
+    #      (groups in plan order on the solve stream, so each launch's CUDA-event duration is
+    #      its own, not shared with concurrent groups) -> per-kind roofline, live
     import ctypes as C
 
     from paper_1104_0623_b200 import _native
     from paper_1104_0623_b200.workmodel import KINDS, TENSOR_KINDS, executed_cmacs
 
     lib = _native.lib()
+    ngroups = len(plan.groups["count"])
     with torch.cuda.stream(stream):
         flush.fill_(1)
         torch.cuda.synchronize()
         lib.find_solve_timing_enable(1)
-        step()
+        for gi in range(ngroups):
+            plan.run(a_d, s_d, gr_d, gl_d, ws=ws, stream=stream, sigma_sym=ssym, groups=(gi, gi + 1))
         torch.cuda.synchronize()
         lib.find_solve_timing_enable(0)
     nl = int(lib.find_solve_timing_read(None, None, None, 0))
@@ -280,29 +283,52 @@ def run_b200(args):
     lib.find_solve_timing_read(kk, gg, ms, nl)
     work = executed_cmacs(plan, ssym)
     per_kind = {}
+    per_group_ms = np.zeros(ngroups)
     for i in range(nl):
         name = KINDS[kk[i]]
         d = per_kind.setdefault(name, {"ms": 0.0, "launches": 0, "cmacs": 0.0, "groups": set()})
         d["ms"] += ms[i]
         d["launches"] += 1
         d["groups"].add(gg[i])
+        per_group_ms[gg[i]] += ms[i]
     for name, d in per_kind.items():
         d["cmacs"] = sum(work.get((gi, name), 0.0) for gi in d["groups"]) * n_e
     tot_ms = sum(d["ms"] for d in per_kind.values())
-    kernels = {name: {"ms_per_step": round(d["ms"], 3), "share": round(d["ms"] / tot_ms, 4), "launches": d["launches"],
-                      "tflops": (round(8 * d["cmacs"] / (d["ms"] * 1e-3) / 1e12, 3) if d["cmacs"] and d["ms"] else None)}
-               for name, d in sorted(per_kind.items(), key=lambda kv: -kv[1]["ms"])}
+
+    def kind_line(d):
+        tf = 8 * d["cmacs"] / (d["ms"] * 1e-3) / 1e12 if d["cmacs"] and d["ms"] else None
+        return {"ms_per_step_serialized": round(d["ms"], 3), "share": round(d["ms"] / tot_ms, 4),
+                "launches": d["launches"], "tflops": round(tf, 3) if tf else None,
+                "frac_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4) if tf else None}
+
+    kernels = {name: kind_line(d) for name, d in sorted(per_kind.items(), key=lambda kv: -kv[1]["ms"])}
     dom = max((k for k in per_kind if k in TENSOR_KINDS), key=lambda k: per_kind[k]["ms"])
     dk = per_kind[dom]
     achieved = 8 * dk["cmacs"] / (dk["ms"] * 1e-3) / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "r01_ncu_kernels.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get(f"{dom}_kernel", {}).get("dram_bytes_per_launch")
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-        "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+        "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
         "kernel": f"{dom}_kernel", "launches_per_step": dk["launches"], "share_of_step": dk["ms"] / tot_ms,
         "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_fp64_probe.txt); cuBLAS ZGEMM 37.02",
-        "work": "executed complex MACs x 8 of those launches (paper_1104_0623_b200/workmodel.py), ÷ their summed "
-                "CUDA-event durations in one instrumented step (concurrent streams: durations overlap)",
+        "work": "executed complex MACs x 8 of those launches (paper_1104_0623_b200/workmodel.py) / their CUDA-event "
+                "durations with each launch group run alone (serialized instrumented step); dominant = the FP64 "
+                "tensor-core (DMMA) kind with the largest serialized device time; traffic = ncu dram bytes per launch "
+                "of that kernel (profiles/r01_ncu_kernels.json)",
     }
+    # north-star target: FP64 fraction on the near-root levels (upward levels 1-4, downward 1-4)
+    g = plan.groups
+    wl = {}
+    for (gi, kname), v in work.items():
+        wl[gi] = wl.get(gi, 0.0) + v
+    near = [gi for gi in range(ngroups) if int(g["level"][gi]) <= 4 and int(g["pass"][gi]) in (0, 1)]
+    near_ms = float(per_group_ms[near].sum())
+    near_tf = 8 * sum(wl.get(gi, 0.0) for gi in near) * n_e / (near_ms * 1e-3) / 1e12 if near_ms else 0.0
+    near_root = {"levels": "upward 1-4 + downward 1-4", "groups": len(near), "ms_serialized": round(near_ms, 3),
+                 "tflops": round(near_tf, 3), "frac_fp64_peak": round(near_tf / FP64_PEAK_TFLOPS, 4)}
     if args.levels and rank == 0:
         Path(args.levels).write_text(json.dumps({"kernels": kernels, "launches": [
             {"kind": KINDS[kk[i]], "group": int(gg[i]), "ms": float(ms[i])} for i in range(nl)]}, indent=1))
@@ -312,22 +338,24 @@ def run_b200(args):
     ops = [SparseOperator(p.a_csr(k)) for k in range(n_e)]
     sig = SparseOperator(p.sigma_csr())
     conf = SolverConfig()
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(3, min(args.steps, 8))
+    per_step = []
     with torch.cuda.stream(stream):
         solve_batch(mesh, ops, sig, conf)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            res = solve_batch(mesh, ops, sig, conf)
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            res = solve_batch(mesh, ops, sig, conf)  # returns host arrays: D2H + sync inside
+            per_step.append(time.perf_counter() - t0)
+    e2e_s = float(np.median(per_step))
     t_e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
     e2e_s = float(t_e.item())
-    e2e = {"value": world * n_e * e2e_steps / e2e_s, "unit": UNIT,
+    e2e = {"value": world * n_e / e2e_s, "unit": UNIT, "steps": e2e_steps,
+           "timing": "host wall clock per solve_batch call, median over the steps (max over ranks)",
            "h2d_bytes_per_step": int(n_e * plan.nnz * 16 + plan.nnz * 16),
            "d2h_bytes_per_step": int(2 * n_e * plan.n * 16),
            "api": "paper_1104_0623_b200.solve_batch(mesh, [SparseOperator]*16, Sigma, SolverConfig())"}
@@ -345,6 +373,7 @@ def run_b200(args):
         "fp64_tflops": flops_total, "fp64_frac_of_peak": flops_total / FP64_PEAK_TFLOPS,
         "work_per_energy_mults": W,
         "roofline": roofline,
+        "near_root": near_root,
         "kernels": kernels,
         "e2e": e2e,
         "gpu_launches": int(plan.launch_count(n_e) * args.steps),

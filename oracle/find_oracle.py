@@ -300,6 +300,7 @@ class FindOracle:
         annotate(self.by_label, adj, nx)
         self.comps = complement_sets(self.root, self.by_label, adj, nx)
         self.bottom_up = sorted(self.by_label.values(), key=lambda c: (-c.level, c.label))
+        self._off = self._offl = self._adj = None  # off-diagonal harvest state (solve(compute_offdiag=True))
 
     # solver.py:188-232
     def _eliminate(self, a, sg, left, right, ul, ur, rl, rr, s_set, label, want_sigma, ledger, rtol):

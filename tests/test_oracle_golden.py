@@ -40,3 +40,15 @@ def test_oracle_matches_dense_small():
     r = o.solve(a.matrix, s.matrix)
     assert np.max(np.abs(r.gr_diag - dense_gr_diag(a.to_dense())) / np.abs(g["dense_gr"])) < 1e-10
     assert np.max(np.abs(r.gless_diag - dense_gless_diag(a.to_dense(), s.to_dense())) / np.abs(g["dense_gl"])) < 1e-10
+
+
+def test_cpu_baseline_estimator_runs():
+    """bench.py's cpu_baseline / --impl reference leg (oracle/cpu_baseline.py) on a tiny mesh."""
+    from oracle.cpu_baseline import estimate_seconds_per_energy
+    from oracle.find_oracle import FindOracle
+    from paper_1104_0623_b200.configs import build_problem
+
+    p = build_problem(12, 10, [1.0], seed=2)
+    o = FindOracle(p.nx, p.ny, p.a_csr(0))
+    r = estimate_seconds_per_energy(o, p.a_csr(0), p.sigma_csr(), fraction=0.5, seed=0)
+    assert r["seconds_per_energy"] > 0 and r["sampled_eliminations"] > 0
