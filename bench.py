@@ -340,6 +340,7 @@ def run_b200(args):
     conf = SolverConfig()
     e2e_steps = max(3, min(args.steps, 8))
     per_step = []
+    parts = []
     with torch.cuda.stream(stream):
         solve_batch(mesh, ops, sig, conf)
         torch.cuda.synchronize()
@@ -349,6 +350,8 @@ def run_b200(args):
             t0 = time.perf_counter()
             res = solve_batch(mesh, ops, sig, conf)  # returns host arrays: D2H + sync inside
             per_step.append(time.perf_counter() - t0)
+            parts.append((res.timings["tree"], res.timings["upward"] + res.timings["downward_extract"],
+                          res.timings["total"]))
     e2e_s = float(np.median(per_step))
     t_e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
@@ -356,6 +359,9 @@ def run_b200(args):
     e2e_s = float(t_e.item())
     e2e = {"value": world * n_e / e2e_s, "unit": UNIT, "steps": e2e_steps,
            "timing": "host wall clock per solve_batch call, median over the steps (max over ranks)",
+           "median_host_prepare_ms": round(1e3 * float(np.median([x[0] for x in parts])), 3),
+           "median_device_ms": round(1e3 * float(np.median([x[1] for x in parts])), 3),
+           "median_call_ms": round(1e3 * float(np.median([x[2] for x in parts])), 3),
            "h2d_bytes_per_step": int(n_e * plan.nnz * 16 + plan.nnz * 16),
            "d2h_bytes_per_step": int(2 * n_e * plan.n * 16),
            "api": "paper_1104_0623_b200.solve_batch(mesh, [SparseOperator]*16, Sigma, SolverConfig())"}

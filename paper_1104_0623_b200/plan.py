@@ -200,7 +200,11 @@ class Plan:
         with self._lock:
             if self._ws is None or self._ws.numel() < need or self._ws.device != device:
                 self._ws = None
-                self._ws = torch.empty(need, dtype=torch.uint8, device=device)
+                try:
+                    self._ws = torch.empty(need, dtype=torch.uint8, device=device)
+                except torch.OutOfMemoryError:
+                    release_workspaces(keep=self)  # workspaces cached by other plans
+                    self._ws = torch.empty(need, dtype=torch.uint8, device=device)
             return self._ws
 
     def run(self, a_dev, s_dev, gr_dev, gl_dev, compute_gless=True, pivot_rtol=1e-12, s_broadcast=True, ws=None,
@@ -256,6 +260,19 @@ class Plan:
 
 _CACHE: dict = {}
 _CACHE_LOCK = threading.Lock()
+
+
+def release_workspaces(keep: "Plan | None" = None) -> None:
+    """Drop the device workspaces cached by every plan except ``keep`` and return the memory."""
+    import torch
+
+    with _CACHE_LOCK:
+        plans = list(_CACHE.values())
+    for p in plans:
+        if p is not keep:
+            p._ws = None
+    if torch.cuda.is_available():
+        torch.cuda.empty_cache()
 
 
 _LAST: list = []  # (nx, ny, leaf_max, indptr, indices, plan) of the last lookup: memcmp fast path

@@ -218,8 +218,13 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
     per_energy += (plan.nnz + 2 * plan.n) * 16
     n_pairs = plan.offdiag_pairs().shape[0] if compute_offdiag else 0
     per_energy += 2 * n_pairs * 16
-    free, _ = torch.cuda.mem_get_info(dev)
+    free, total = torch.cuda.mem_get_info(dev)
     held = plan._ws.numel() if plan._ws is not None and plan._ws.device == dev else 0
+    if free + held < 0.5 * total:  # other plans' cached workspaces crowd this solve out
+        from .plan import release_workspaces
+
+        release_workspaces(keep=plan)
+        free, total = torch.cuda.mem_get_info(dev)
     chunk = max(1, min(n_e, int((0.85 * (free + held) - plan.workspace_bytes(1, compute_gless) + per_energy) // per_energy)))
     if max_chunk:
         chunk = min(chunk, max_chunk)
