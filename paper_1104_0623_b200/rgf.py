@@ -1,0 +1,300 @@
+"""Block-tridiagonal recursive Green's function (RGF) on the GPU — the reference's
+crossover baseline (find_selinv/rgf.py:1-208).
+
+The operator is blocked by mesh rows (line y = nodes y*nx .. y*nx+nx-1), which makes it
+block tridiagonal: D_i = A(line_i, line_i), E_i = A(line_i, line_{i+1}),
+F_i = A(line_{i+1}, line_i).  The recurrences are those of the reference:
+
+    g_0 = D_0^-1,  g_i = (D_i - F_{i-1} g_{i-1} E_{i-1})^-1                  (rgf.py:108-115)
+    G_{N-1} = g_{N-1},  G_i = g_i + g_i E_i G_{i+1} F_i g_i                    (rgf.py:121-136)
+    G^<: right-connected g^R, left/right-connected scattering blocks and
+         G_ii R_i G_ii^H with R_i = S^L_i + S^R_i - S_ii                       (rgf.py:139-208)
+
+Every step is batched over all energy points: one cuSOLVER batched inverse and a few
+cuBLAS ZGEMMs per mesh line (library GEMM / inverse through torch on the device; this
+is the comparison path, the FIND path is the hand-written one).  The ledger follows the
+reference's charging rules (rgf.py:89-107: inverse c^3, products skipped when the
+coupling block is diagonal).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from .errors import NativeLibraryError, SingularPivotError
+from .ledger import FlopLedger
+
+
+@dataclass
+class BlockTridiagonal:
+    """rgf.py:28-40: line blocks D_i, E_i = A(line_i, line_{i+1}), F_i = A(line_{i+1}, line_i)."""
+
+    diag: list
+    upper: list
+    lower: list
+    lines: list
+
+    @property
+    def num_blocks(self) -> int:
+        return len(self.diag)
+
+
+def _check_tridiagonal(m: sp.csr_matrix, nx: int):
+    c = m.tocoo()
+    if np.any(np.abs(c.row // nx - c.col // nx) > 1):
+        raise ValueError("operator pattern is not block tridiagonal over mesh lines")
+
+
+def block_partition(op, mesh) -> BlockTridiagonal:
+    """rgf.py:43-61 (host numpy blocks; same validation and error)."""
+    if op.n != mesh.n:
+        raise ValueError("operator size does not match the mesh")
+    m = op.matrix.tocsr()
+    _check_tridiagonal(m, mesh.nx)
+    nx, ny = mesh.nx, mesh.ny
+    lines = [np.arange(y * nx, (y + 1) * nx, dtype=np.int64) for y in range(ny)]
+    blk = lambda r, c: m[r * nx:(r + 1) * nx, c * nx:(c + 1) * nx].toarray().astype(np.complex128)
+    return BlockTridiagonal([blk(y, y) for y in range(ny)], [blk(y, y + 1) for y in range(ny - 1)],
+                            [blk(y + 1, y) for y in range(ny - 1)], lines)
+
+
+def _device():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("the RGF path needs a CUDA device (there is no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _blocks_device(mats, nx: int, ny: int, dev):
+    """Dense line blocks of a batch of CSR matrices sharing one pattern, scattered on the
+    device: D [nE, ny, nx, nx], E / F [nE, ny-1, nx, nx]."""
+    import torch
+
+    m0 = mats[0].tocoo()
+    r, c = m0.row.astype(np.int64), m0.col.astype(np.int64)
+    ly, lc = r // nx, c // nx
+    vals = np.stack([np.asarray(_coo_on(m, m0), np.complex128) for m in mats])
+    v = torch.from_numpy(vals).to(dev)
+    ne = len(mats)
+    D = torch.zeros((ne, ny, nx, nx), dtype=torch.complex128, device=dev)
+    E = torch.zeros((ne, max(ny - 1, 0), nx, nx), dtype=torch.complex128, device=dev)
+    F = torch.zeros_like(E)
+    for dst, sel, line in ((D, ly == lc, ly), (E, lc == ly + 1, ly), (F, ly == lc + 1, lc)):
+        if not sel.any():
+            continue
+        idx = torch.from_numpy(((line[sel] * nx + r[sel] % nx) * nx + c[sel] % nx)).to(dev)
+        dst.view(ne, -1)[:, idx] = v[:, torch.from_numpy(np.nonzero(sel)[0]).to(dev)]  # (row, col) unique
+    return D, E, F
+
+
+def _coo_on(m, m0) -> np.ndarray:
+    """Values of m on m0's COO pattern (m must share the pattern)."""
+    m = m.tocsr()
+    if m.nnz == m0.nnz:
+        cm = m.tocoo()
+        if np.array_equal(cm.row, m0.row) and np.array_equal(cm.col, m0.col):
+            return cm.data
+    return np.asarray(m[m0.row, m0.col]).ravel()
+
+
+def _is_diag_batch(X) -> bool:
+    """rgf.py:75-81: no entry off the diagonal (for every energy point)."""
+    import torch
+
+    nx = X.shape[-1]
+    off = X * (1 - torch.eye(nx, dtype=X.dtype, device=X.device))
+    return not bool(torch.any(off != 0))
+
+
+def _inv(X, line: int, infos: list):
+    """Batched inverse; the singularity flags are collected and checked once per sweep
+    (no host synchronisation per line)."""
+    import torch
+
+    out, info = torch.linalg.inv_ex(X)
+    infos.append((line, info))
+    return out
+
+
+def _check_infos(infos: list):
+    import torch
+
+    if not infos:
+        return
+    bad = torch.stack([i for _, i in infos]).ne(0).any(dim=1).nonzero()
+    if bad.numel():
+        raise SingularPivotError(f"singular recurrence block at line {infos[int(bad[0, 0])][0]}")
+    infos.clear()
+
+
+def _sandwich(L, Mid, R, ldiag: bool, rdiag: bool):
+    """L @ Mid @ R with diagonal factors applied as scalings (rgf.py:92-105)."""
+    t = Mid
+    t = t * L.diagonal(dim1=-2, dim2=-1).unsqueeze(-1) if ldiag else L @ t
+    t = t * R.diagonal(dim1=-2, dim2=-1).unsqueeze(-2) if rdiag else t @ R
+    return t
+
+
+def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
+    """diag(G^r) [nE, n] and, if requested, diag(G^<) [nE, n] of every operator in a_list
+    (shared pattern, block tridiagonal over mesh lines) by the RGF recurrences, batched
+    over the energy points on the device.  Returns (gr, gl, ledgers) with the per-energy
+    reference ledgers of rgf_gr_diag (ledgers["gr"]) and rgf_gless_diag (ledgers["gless"])."""
+    import torch
+
+    dev = _device()
+    nx, ny = mesh.nx, mesh.ny
+    mats = [a.matrix.tocsr() for a in a_list]
+    for m in mats[:1]:
+        if m.shape[0] != mesh.n:
+            raise ValueError("operator size does not match the mesh")
+        _check_tridiagonal(m, nx)
+    led = FlopLedger()  # forward + backward: rgf_gr_diag's charges
+    infos: list = []
+    D, E, F = _blocks_device(mats, nx, ny, dev)
+    ediag = [_is_diag_batch(E[:, i]) for i in range(ny - 1)]
+    fdiag = [_is_diag_batch(F[:, i]) for i in range(ny - 1)]
+    c3 = nx ** 3
+
+    def charge_sandwich(ld, rd):
+        if not ld:
+            led.add("rgf", c3)
+        if not rd:
+            led.add("rgf", c3)
+
+    # forward: left-connected g_i (rgf.py:108-115)
+    gl_blk = [None] * ny
+    gl_blk[0] = _inv(D[:, 0], 0, infos)
+    led.add("rgf", c3)
+    for i in range(1, ny):
+        gl_blk[i] = _inv(D[:, i] - _sandwich(F[:, i - 1], gl_blk[i - 1], E[:, i - 1], fdiag[i - 1], ediag[i - 1]), i,
+                         infos)
+        charge_sandwich(fdiag[i - 1], ediag[i - 1])
+        led.add("rgf", c3)
+    led_forward = FlopLedger(led.multiplications, dict(led.by_kernel))
+    # backward: diagonal blocks of G (rgf.py:121-136)
+    gr = torch.empty((len(mats), mesh.n), dtype=torch.complex128, device=dev)
+    g_full = gl_blk[ny - 1]
+    gr[:, (ny - 1) * nx:] = g_full.diagonal(dim1=-2, dim2=-1)
+    for i in range(ny - 2, -1, -1):
+        t = _sandwich(E[:, i], g_full, F[:, i], ediag[i], fdiag[i])
+        charge_sandwich(ediag[i], fdiag[i])
+        g_full = gl_blk[i] + (gl_blk[i] @ t) @ gl_blk[i]
+        led.add("rgf", 2 * c3)
+        gr[:, i * nx:(i + 1) * nx] = g_full.diagonal(dim1=-2, dim2=-1)
+    _check_infos(infos)
+    led_gr = led
+    led = FlopLedger(led_forward.multiplications, dict(led_forward.by_kernel))  # rgf_gless_diag's charges
+    if not compute_gless:
+        return gr.cpu().numpy(), None, {"gr": led_gr, "gless": None}
+    if sigma is None:
+        raise ValueError("compute_gless requires a scattering matrix")
+    sm = sigma.matrix.tocsr()
+    _check_tridiagonal(sm, nx)
+    SD, SE, SF = _blocks_device([sm], nx, ny, dev)  # Sigma^< is energy independent
+    sc = sm.tocoo()
+    up_nz = np.zeros(max(ny - 1, 0), bool)  # Sigma coupling blocks with a nonzero entry (host, no sync)
+    lo_nz = np.zeros(max(ny - 1, 0), bool)
+    nzm = sc.data != 0
+    up_nz[(sc.row // nx)[nzm & (sc.col // nx == sc.row // nx + 1)]] = True
+    lo_nz[(sc.col // nx)[nzm & (sc.row // nx == sc.col // nx + 1)]] = True
+    # right-connected g^R (rgf.py:164-168; its ledger repeats the forward one)
+    gr_blk = [None] * ny
+    gr_blk[ny - 1] = _inv(D[:, ny - 1], ny - 1, infos)
+    led.add("rgf", c3)
+    for i in range(ny - 2, -1, -1):
+        gr_blk[i] = _inv(D[:, i] - _sandwich(E[:, i], gr_blk[i + 1], F[:, i], ediag[i], fdiag[i]), i, infos)
+        charge_sandwich(ediag[i], fdiag[i])
+        led.add("rgf", c3)
+
+    def connected(g_conn, reverse):  # rgf.py:139-178
+        s_conn = [None] * ny
+        order = range(ny - 1, -1, -1) if reverse else range(ny)
+        prev = None
+        for i in order:
+            if prev is None:
+                s_conn[i] = SD[:, i].clone()
+            else:
+                if reverse:
+                    coup, cdiag, sig_sb, sig_bs = E[:, i], ediag[i], SF[:, i], SE[:, i]
+                    nz_sb, nz_bs = lo_nz[i], up_nz[i]
+                else:
+                    coup, cdiag, sig_sb, sig_bs = F[:, i - 1], fdiag[i - 1], SE[:, i - 1], SF[:, i - 1]
+                    nz_sb, nz_bs = up_nz[i - 1], lo_nz[i - 1]
+                if cdiag:
+                    l_fac = coup.diagonal(dim1=-2, dim2=-1).unsqueeze(-1) * g_conn[prev]
+                else:
+                    l_fac = coup @ g_conn[prev]
+                    led.add("rgf", c3)
+                lh = l_fac.conj().transpose(-2, -1)
+                term = SD[:, i] + (l_fac @ s_conn[prev]) @ lh
+                led.add("rgf", 2 * c3)
+                if nz_sb:
+                    term = term - l_fac @ sig_sb
+                if nz_bs:
+                    term = term - sig_bs @ lh
+                s_conn[i] = term
+            prev = i
+        return s_conn
+
+    s_left = connected(gl_blk, False)
+    s_right = connected(gr_blk, True)
+    gless = torch.empty_like(gr)
+    for i in range(ny):  # rgf.py:193-207
+        u = D[:, i].clone()
+        if i > 0:
+            u = u - _sandwich(F[:, i - 1], gl_blk[i - 1], E[:, i - 1], fdiag[i - 1], ediag[i - 1])
+            charge_sandwich(fdiag[i - 1], ediag[i - 1])
+        if i + 1 < ny:
+            u = u - _sandwich(E[:, i], gr_blk[i + 1], F[:, i], ediag[i], fdiag[i])
+            charge_sandwich(ediag[i], fdiag[i])
+        r_i = s_left[i] + s_right[i] - SD[:, i]
+        g_ii = _inv(u, i, infos)
+        led.add("rgf", c3)
+        gless[:, i * nx:(i + 1) * nx] = ((g_ii @ r_i) @ g_ii.conj().transpose(-2, -1)).diagonal(dim1=-2, dim2=-1)
+        led.add("rgf", 2 * c3)
+    _check_infos(infos)
+    return gr.cpu().numpy(), gless.cpu().numpy(), {"gr": led_gr, "gless": led}
+
+
+def rgf_gr_diag(bt: BlockTridiagonal, ledger: FlopLedger | None = None) -> np.ndarray:
+    """rgf.py:118-136 on the device, for one operator given as line blocks."""
+    gr, _, led = _rgf_from_blocks(bt, None, False)
+    if ledger is not None:
+        ledger.merge(led["gr"])
+    return gr
+
+
+def rgf_gless_diag(bt: BlockTridiagonal, sigma_bt: BlockTridiagonal, ledger: FlopLedger | None = None) -> np.ndarray:
+    """rgf.py:181-208 on the device, for one operator and scattering matrix given as line blocks."""
+    _, gl, led = _rgf_from_blocks(bt, sigma_bt, True)
+    if ledger is not None:
+        ledger.merge(led["gless"])
+    return gl
+
+
+def _rgf_from_blocks(bt, sigma_bt, gless):
+    from .mesh import Mesh
+    from .operators import SparseOperator
+
+    nx = bt.lines[0].size
+    ny = bt.num_blocks
+    n = nx * ny
+
+    def assemble(b):
+        m = sp.lil_matrix((n, n), dtype=np.complex128)
+        for i in range(ny):
+            m[i * nx:(i + 1) * nx, i * nx:(i + 1) * nx] = b.diag[i]
+            if i + 1 < ny:
+                m[i * nx:(i + 1) * nx, (i + 1) * nx:(i + 2) * nx] = b.upper[i]
+                m[(i + 1) * nx:(i + 2) * nx, i * nx:(i + 1) * nx] = b.lower[i]
+        return SparseOperator(m.tocsr())
+
+    a = assemble(bt)
+    s = assemble(sigma_bt) if sigma_bt is not None else None
+    gr, gl, led = rgf_batch(Mesh(nx, ny), [a], s, gless)
+    return gr[0], (gl[0] if gl is not None else None), led

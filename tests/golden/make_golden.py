@@ -242,10 +242,35 @@ def io_cases():
     print("wrote io cases")
 
 
+def rgf_cases():
+    """Reference RGF (rgf.py:118-208) diagonals and ledgers on contact and stencil problems."""
+    from find_selinv.rgf import block_partition, rgf_gless_diag, rgf_gr_diag
+
+    cases = {"rgf_c5_12x9": build_problem(12, 9, [0.8, 2.3], seed=51, stencil=5),
+             "rgf_c9_10x8": build_problem(10, 8, [1.6], seed=52, stencil=9)}
+    for name, p in cases.items():
+        mesh = ref.Mesh(p.nx, p.ny)
+        s_op = SparseOperator(p.sigma_csr())
+        gr, gl = [], []
+        for k in range(p.energies.size):
+            a_op = SparseOperator(p.a_csr(k))
+            bt, sbt = block_partition(a_op, mesh), block_partition(s_op, mesh)
+            lg, ll = ref.FlopLedger(), ref.FlopLedger()
+            gr.append(rgf_gr_diag(bt, lg))
+            gl.append(rgf_gless_diag(bt, sbt, ll))
+        np.savez_compressed(HERE / f"{name}.npz", nx=p.nx, ny=p.ny, indptr=p.indptr, indices=p.indices,
+                            h_vals=p.h_vals, diag_pos=p.diag_pos, s_vals=p.s_vals, energies=p.energies,
+                            gr=np.array(gr), gl=np.array(gl), W_gr=frac(lg.multiplications),
+                            W_gl=frac(ll.multiplications), allow_pickle=True)
+        print("wrote", name, "W_gr", lg.multiplications, "W_gl", ll.multiplications)
+
+
 if __name__ == "__main__":
     import sys as _sys
 
-    if "io" in _sys.argv:
+    if "rgf" in _sys.argv:
+        rgf_cases()
+    elif "io" in _sys.argv:
         io_cases()
     elif "offdiag" in _sys.argv:
         offdiag_cases()
@@ -255,3 +280,4 @@ if __name__ == "__main__":
         contact_cases()
         offdiag_cases()
         io_cases()
+        rgf_cases()
