@@ -2528,7 +2528,9 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         case kLGatherS: launch_k(gather_kernel<true>, grid, kThreads, 0, stream, prm, tk); break;
         case kLPanel: {
           const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
-          if (L.nb == 32 && g_panel_mode == 0) {
+          if (L.nb == 32 && rmax > (int)kRegPanelMaxS) {  // more rows than the register panel holds
+            launch_k(panel_smem_kernel<32>, grid, kThreads, (size_t)rmax * 33 * sizeof(double2), stream, prm, tk);
+          } else if (L.nb == 32 && g_panel_mode == 0) {
             switch ((std::max(rmax, 1) + 31) / 32) {
               case 1: launch_k(panel1_kernel<32, 32>, grid, 32, 0, stream, prm, tk); break;
               case 2: launch_k(panel1_kernel<32, 64>, grid, 64, 0, stream, prm, tk); break;

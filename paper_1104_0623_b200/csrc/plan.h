@@ -70,11 +70,12 @@ constexpr int64_t kRegPanelMaxS = 288;
 inline int pick_nb_host(int64_t max_s) {
   if (const char* f = std::getenv("FIND_B200_NB")) {  // test hook: force the panel width
     const int nb = std::atoi(f);
-    if ((nb == 32 && max_s <= kRegPanelMaxS) || (nb == 16 && max_s * 17 * 16 <= 220 * 1024) ||
+    if ((nb == 32 && max_s * 33 * 16 <= 220 * 1024) || (nb == 16 && max_s * 17 * 16 <= 220 * 1024) ||
         (nb == 8 && max_s * 9 * 16 <= 220 * 1024) || (nb == 4 && max_s * 5 * 16 <= 220 * 1024))
       return nb;
   }
   if (max_s <= kRegPanelMaxS) return 32;
+  if (max_s * 33 * 16 <= 220 * 1024) return 32;  // shared-memory rows (panel_smem_kernel<32>): K = 32 updates
   if (max_s * 17 * 16 <= 220 * 1024) return 16;
   if (max_s * 9 * 16 <= 220 * 1024) return 8;
   if (max_s * 5 * 16 <= 220 * 1024) return 4;
