@@ -20,6 +20,7 @@
 //     resident) workspace; panel LU in shared memory with CTA-wide argmax
 //     pivot search; all O(n^3) work as FP64 tensor-core tiles (mma.sync
 //     m8n8k4 f64 -> SASS DMMA.8x8x4; B200 has no tcgen05 f64 kind).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -1443,6 +1444,163 @@ __global__ void __launch_bounds__(kThreads) panel_smem_kernel(SolveParams P, con
 }
 
 // ---- U12 = L_jj^-1 A12 (type 0, 64-column tiles) and L21 = A21 U_jj^-1 (type 1, 64-row tiles), DMMA
+
+// ---- NB = 32 panel step over a thread-block CLUSTER (S rows beyond one CTA's shared
+// memory, s > 426): the R panel rows are split into CS contiguous chunks, one per CTA of
+// the cluster, in shared memory.  Per column (two cluster barriers): every CTA posts its
+// best candidate to every CTA (DSMEM stores); after the barrier all pick the same winner
+// (max |re|+|im|, lowest row on ties, as panel_smem_kernel); the winner's owner broadcasts
+// the pivot row and 1/u, the owner of row jj sends that row to the winner's owner; after
+// the second barrier rows jj / pr are exchanged (LAPACK order) and every CTA updates its
+// rows.  Same pivots, multipliers and outputs (M rows, PIV, PERM) as panel_smem_kernel<32>.
+constexpr int kClusterMax = 8;
+constexpr int kClusterRows = 384;  // rows per CTA: 384 * 33 * 16 B = 198 KB
+__host__ __device__ constexpr size_t cluster_panel_smem() {
+  return ((size_t)kClusterRows * 33 + 2 * 33) * sizeof(double2);
+}
+
+__global__ void __launch_bounds__(kThreads) panel_cluster_kernel(SolveParams P, const Task* tasks) {
+  namespace cg = cooperative_groups;
+  constexpr int NB = 32, PS = NB + 1;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CS = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* panel = reinterpret_cast<double2*>(smem_raw);  // [chunk][PS]
+  double2* prow = panel + (size_t)kClusterRows * PS;       // pivot row (+ 1/u in [NB])
+  double2* srow = prow + PS;                               // row jj, sent to the pivot row's owner
+  __shared__ double cand_v[2][kClusterMax];
+  __shared__ int cand_i[2][kClusterMax];
+  __shared__ double wv[kThreads / 32];
+  __shared__ int wi[kThreads / 32];
+  __shared__ int lpiv[NB], dsrc[2 * NB], ddst[2 * NB];
+  __shared__ int s_bad, s_nd;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Task t = tasks[blockIdx.x / CS];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s;
+  const int j = t.a, j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
+  const int chunk = (R + CS - 1) / CS;
+  const int r_lo = min(R, rank * chunk), r_hi = min(R, r_lo + chunk), nloc = r_hi - r_lo;
+  const Scr S = scratch_of(P, d, e, NB);
+  double2* M = S.M;
+  if (tid == 0) s_bad = INT32_MAX;
+  for (int q = tid; q < nloc * jb; q += kThreads) {
+    const int r = q / jb, c = q % jb;
+    panel[r * PS + c] = M[(int64_t)(j0 + r_lo + r) * n + j0 + c];
+  }
+  double scale = 0.0;
+  if (rank == 0) {
+    if (j == 0) {
+      for (int q = tid; q < (s + kRowChunk - 1) / kRowChunk; q += kThreads) scale = fmax(scale, S.pmax[q]);
+      int dummy = 0;
+      block_argmax<kThreads>(scale, dummy, wv, wi);
+      if (tid == 0) {
+        *S.scale = scale;
+        if (scale == 0.0) s_bad = 0;
+      }
+    } else {
+      scale = *reinterpret_cast<volatile double*>(S.scale);
+    }
+  }
+  cluster.sync();
+  for (int jj = 0; jj < jb; ++jj) {
+    const int buf = jj & 1;
+    // local candidate
+    double v = -1.0;
+    int vi = INT32_MAX;
+    for (int r = max(jj - r_lo, 0) + tid; r < nloc; r += kThreads) {
+      const double a = cabs1(panel[r * PS + jj]);
+      if (a > v) { v = a; vi = r_lo + r; }
+    }
+    block_argmax<kThreads>(v, vi, wv, wi);
+    if (tid < CS) {  // post to every CTA of the cluster
+      double* rv = cluster.map_shared_rank(&cand_v[buf][rank], tid);
+      int* ri = cluster.map_shared_rank(&cand_i[buf][rank], tid);
+      *rv = v;
+      *ri = vi;
+    }
+    cluster.sync();
+    double bv = -1.0;
+    int pr = INT32_MAX;
+    for (int k = 0; k < CS; ++k) {
+      const double ov = cand_v[buf][k];
+      const int oi = cand_i[buf][k];
+      if (ov > bv || (ov == bv && oi < pr)) { bv = ov; pr = oi; }
+    }
+    const int own_pr = pr / chunk, own_jj = jj / chunk;
+    if (rank == own_pr) {  // broadcast the pivot row and 1/u
+      const double2* src = panel + (pr - r_lo) * PS;
+      for (int q = tid; q < CS * (NB + 1); q += kThreads) {
+        const int dst = q / (NB + 1), c = q % (NB + 1);
+        double2* pd = cluster.map_shared_rank(prow, dst);
+        pd[c] = c < NB ? src[c] : cinv(src[jj]);
+      }
+      if (tid == 0 && cabs(src[jj]) < P.rtol * *reinterpret_cast<volatile double*>(S.scale))
+        atomicMin(&s_bad, j0 + jj);
+    }
+    if (rank == own_jj && pr != jj) {  // row jj goes to the pivot row's owner
+      const double2* src = panel + (jj - r_lo) * PS;
+      double2* sd = cluster.map_shared_rank(srow, own_pr);
+      for (int c = tid; c < NB; c += kThreads) sd[c] = src[c];
+    }
+    if (tid == 0) lpiv[jj] = pr;
+    cluster.sync();
+    if (pr != jj) {
+      if (rank == own_jj)
+        for (int c = tid; c < NB; c += kThreads) panel[(jj - r_lo) * PS + c] = prow[c];
+      if (rank == own_pr)
+        for (int c = tid; c < NB; c += kThreads) panel[(pr - r_lo) * PS + c] = srow[c];
+    }
+    __syncthreads();
+    const double2 uinv = prow[NB];
+    for (int r = max(jj + 1 - r_lo, 0) + tid; r < nloc; r += kThreads) {
+      double2* rw = panel + r * PS;
+      const double2 l = cmul(rw[jj], uinv);
+      rw[jj] = l;
+#pragma unroll
+      for (int c = 1; c < NB; ++c)
+        if (c > jj && c < jb) rw[c] = cfms(rw[c], l, prow[c]);
+    }
+  }
+  cluster.sync();
+  for (int q = tid; q < nloc * jb; q += kThreads) {
+    const int r = q / jb, c = q % jb;
+    M[(int64_t)(j0 + r_lo + r) * n + j0 + c] = panel[r * PS + c];
+  }
+  if (tid == 0 && s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);  // pivot test of the rows this CTA owned
+  if (rank != 0) return;
+  for (int k = tid; k < jb; k += kThreads) S.PIV[j0 + k] = j0 + lpiv[k];
+  if (tid == 0) {
+    int key[2 * NB], val[2 * NB], cnt = 0;
+    for (int jj = 0; jj < jb; ++jj) {
+      if (lpiv[jj] == jj) continue;
+      int ia = -1, ib = -1;
+      for (int k = 0; k < cnt; ++k) {
+        if (key[k] == jj) ia = k;
+        if (key[k] == lpiv[jj]) ib = k;
+      }
+      if (ia < 0) { key[cnt] = jj; val[cnt] = jj; ia = cnt++; }
+      if (ib < 0) { key[cnt] = lpiv[jj]; val[cnt] = lpiv[jj]; ib = cnt++; }
+      const int tmp = val[ia];
+      val[ia] = val[ib];
+      val[ib] = tmp;
+    }
+    int nd = 0;
+    for (int k = 0; k < cnt; ++k)
+      if (key[k] != val[k]) { ddst[nd] = key[k]; dsrc[nd] = val[k]; ++nd; }
+    s_nd = nd;
+  }
+  __syncthreads();
+  const int nd = s_nd;
+  if (tid == 0) S.PERM[0] = nd;
+  for (int k = tid; k < nd; k += kThreads) {
+    S.PERM[1 + k] = dsrc[k];
+    S.PERM[1 + 2 * NB + k] = ddst[k];
+  }
+}
+
 template <int NB>
 struct TrsmTiles;
 template <>
@@ -2252,6 +2410,24 @@ void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStrea
   cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
+template <typename... KArgs, typename... Args>
+void launch_cluster(void (*k)(KArgs...), dim3 grid, dim3 block, unsigned cs, size_t smem, cudaStream_t st,
+                    Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // dynamic budget (static smem of the kernels < 1 KB)
 size_t ws_header_bytes() { return 256; }
 
@@ -2299,6 +2475,8 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(offdiag_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)cluster_panel_smem()));
   CUDA_TRY(cudaFuncSetAttribute(offdiag_small_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)offdiag_small_smem<32>()));
   CUDA_TRY(cudaFuncSetAttribute(offdiag_small_kernel<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2528,7 +2706,12 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         case kLGatherS: launch_k(gather_kernel<true>, grid, kThreads, 0, stream, prm, tk); break;
         case kLPanel: {
           const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
-          if (L.nb == 32 && rmax > (int)kRegPanelMaxS) {  // more rows than the register panel holds
+          if (L.nb == 32 && rmax > (int)kSmemPanelMaxS32) {  // rows over a thread-block cluster
+            const unsigned cs = (unsigned)((rmax + kClusterRows - 1) / kClusterRows);
+            if (cs > (unsigned)kClusterMax) return fail_status(st, FIND_EINVAL, "panel too tall for one cluster");
+            launch_cluster(panel_cluster_kernel, dim3(cnt * cs, (unsigned)nE), kThreads, cs, cluster_panel_smem(), stream,
+                           prm, tk);
+          } else if (L.nb == 32 && rmax > (int)kRegPanelMaxS) {  // more rows than the register panel holds
             launch_k(panel_smem_kernel<32>, grid, kThreads, (size_t)rmax * 33 * sizeof(double2), stream, prm, tk);
           } else if (L.nb == 32 && g_panel_mode == 0) {
             switch ((std::max(rmax, 1) + 31) / 32) {

@@ -67,15 +67,16 @@ struct LaunchSpec {
 // Panel width of a group.  NB = 32: register panel, one S row per thread, up to
 // kRegPanelMaxS rows; NB = 16/8/4: shared-memory panel for larger S.
 constexpr int64_t kRegPanelMaxS = 288;
+constexpr int64_t kSmemPanelMaxS32 = 426;     // NB = 32 rows in one CTA's shared memory (426 * 33 * 16 B)
+constexpr int64_t kClusterPanelMaxS = 8 * 384;  // NB = 32 rows over a cluster of <= 8 CTAs (panel_cluster_kernel)
 inline int pick_nb_host(int64_t max_s) {
   if (const char* f = std::getenv("FIND_B200_NB")) {  // test hook: force the panel width
     const int nb = std::atoi(f);
-    if ((nb == 32 && max_s * 33 * 16 <= 220 * 1024) || (nb == 16 && max_s * 17 * 16 <= 220 * 1024) ||
+    if ((nb == 32 && max_s <= kClusterPanelMaxS) || (nb == 16 && max_s * 17 * 16 <= 220 * 1024) ||
         (nb == 8 && max_s * 9 * 16 <= 220 * 1024) || (nb == 4 && max_s * 5 * 16 <= 220 * 1024))
       return nb;
   }
-  if (max_s <= kRegPanelMaxS) return 32;
-  if (max_s * 33 * 16 <= 220 * 1024) return 32;  // shared-memory rows (panel_smem_kernel<32>): K = 32 updates
+  if (max_s <= kClusterPanelMaxS) return 32;  // register / shared-memory / cluster panels: K = 32 updates
   if (max_s * 17 * 16 <= 220 * 1024) return 16;
   if (max_s * 9 * 16 <= 220 * 1024) return 8;
   if (max_s * 5 * 16 <= 220 * 1024) return 4;

@@ -18,7 +18,7 @@ TENSOR_KINDS = ("trsm", "trail", "xsolve", "tgemm", "rgemm", "schur")
 
 def pick_nb(max_s: int) -> int:
     """Mirror of pick_nb_host (csrc/plan.h)."""
-    if max_s <= 288 or max_s * 33 * 16 <= 220 * 1024:
+    if max_s <= 8 * 384:  # register / shared-memory / cluster panels (csrc/plan.h pick_nb_host)
         return 32
     for nb, w in ((16, 17), (8, 9), (4, 5)):
         if max_s * w * 16 <= 220 * 1024:
