@@ -856,14 +856,23 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(SolveParams P, const T
 //   LOWER (unit L):  [A 0; C B]^-1 = [A^-1 0; -B^-1 C A^-1  B^-1]
 //   upper (U):       [A C; 0 B]^-1 = [A^-1 -A^-1 C B^-1; 0  B^-1]
 // X, W: smem [NB][NB+1]; rows/cols >= jb act as identity.
+// Barrier over the NT threads [bar_base, bar_base + NT) of the CTA (named barrier bar_id when
+// NT is not the whole CTA, so two halves can run independent inverses).
+template <int NT>
+__device__ __forceinline__ void part_sync(int bar_id) {
+  if (NT == kThreads) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(NT) : "memory");
+}
+
 template <int NB, bool LOWER, int NT>
-__device__ void block_tri_inverse_t(const double2 (*D)[NB + 1], int jb, double2 (*X)[NB + 1], double2 (*W)[NB + 1]) {
-  const int tid = threadIdx.x;
+__device__ void block_tri_inverse_t(const double2 (*D)[NB + 1], int jb, double2 (*X)[NB + 1], double2 (*W)[NB + 1],
+                                    int tid = -1, int bar_id = 0) {
+  if (tid < 0) tid = threadIdx.x;
   for (int q = tid; q < NB * NB; q += NT) {
     const int r = q / NB, c = q % NB;
     X[r][c] = r != c ? cz() : ((LOWER || r >= jb) ? make_double2(1.0, 0.0) : cinv(D[r][r]));
   }
-  __syncthreads();
+  part_sync<NT>(bar_id);
 #pragma unroll 1
   for (int bs = 1; bs < NB; bs *= 2) {
     for (int q = tid; q < (NB / 2) * bs; q += NT) {
@@ -884,7 +893,7 @@ __device__ void block_tri_inverse_t(const double2 (*D)[NB + 1], int jb, double2 
         W[i][jc] = acc;
       }
     }
-    __syncthreads();
+    part_sync<NT>(bar_id);
     for (int q = tid; q < (NB / 2) * bs; q += NT) {
       const int pair = q / (bs * bs), loc = q % (bs * bs);
       const int k = pair * 2 * bs, a = loc / bs, b = loc % bs;
@@ -901,7 +910,7 @@ __device__ void block_tri_inverse_t(const double2 (*D)[NB + 1], int jb, double2 
         X[i][jc] = make_double2(-acc.x, -acc.y);
       }
     }
-    __syncthreads();
+    part_sync<NT>(bar_id);
   }
 }
 
@@ -1707,16 +1716,18 @@ __global__ void __launch_bounds__(kThreads) panel_inv_kernel(SolveParams P, cons
     Dm[r][c] = (r < jb && c < jb) ? S.M[(int64_t)(j0 + r) * n + j0 + c] : cz();
   }
   __syncthreads();
-#pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {
-    if (pass == 0) block_tri_inverse<NB, true>(Dm, jb, Xm, Wm);
-    else block_tri_inverse<NB, false>(Dm, jb, Xm, Wm);
-    double2* out = (pass == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
-    for (int q = threadIdx.x; q < NB * NB; q += kThreads) {
-      const int r = q / NB, c = q % NB;
-      out[q] = (r < jb && c < jb) ? Xm[r][c] : cz();
-    }
-    __syncthreads();
+  // L_jj^-1 on threads [0, 128), U_jj^-1 on [128, 256), concurrently (named barriers 1 and 2)
+  constexpr int H = kThreads / 2;
+  const bool lower = threadIdx.x < H;
+  const int ht = lower ? threadIdx.x : threadIdx.x - H;
+  Row* Xh = lower ? Xm : Wm + NB;
+  Row* Wh = lower ? Wm : Wm + 2 * NB;
+  if (lower) block_tri_inverse_t<NB, true, H>(Dm, jb, Xh, Wh, ht, 1);
+  else block_tri_inverse_t<NB, false, H>(Dm, jb, Xh, Wh, ht, 2);
+  double2* out = (lower ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
+  for (int q = ht; q < NB * NB; q += H) {
+    const int r = q / NB, c = q % NB;
+    out[q] = (r < jb && c < jb) ? Xh[r][c] : cz();
   }
 }
 
@@ -2459,7 +2470,7 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<4>()));
   CUDA_TRY(cudaFuncSetAttribute(panel_inv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(3 * 32 * 33 * sizeof(double2))));
+                                (int)(5 * 32 * 33 * sizeof(double2))));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<4>()));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<32>()));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<16>()));
@@ -2747,10 +2758,10 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           break;
         }
         case kLPanelInv:
-          if (L.nb == 32) launch_k(panel_inv_kernel<32>, grid, kThreads, 3 * 32 * 33 * sizeof(double2), stream, prm, tk);
-          else if (L.nb == 16) launch_k(panel_inv_kernel<16>, grid, kThreads, 3 * 16 * 17 * sizeof(double2), stream, prm, tk);
-          else if (L.nb == 8) launch_k(panel_inv_kernel<8>, grid, kThreads, 3 * 8 * 9 * sizeof(double2), stream, prm, tk);
-          else launch_k(panel_inv_kernel<4>, grid, kThreads, 3 * 4 * 5 * sizeof(double2), stream, prm, tk);
+          if (L.nb == 32) launch_k(panel_inv_kernel<32>, grid, kThreads, 5 * 32 * 33 * sizeof(double2), stream, prm, tk);
+          else if (L.nb == 16) launch_k(panel_inv_kernel<16>, grid, kThreads, 5 * 16 * 17 * sizeof(double2), stream, prm, tk);
+          else if (L.nb == 8) launch_k(panel_inv_kernel<8>, grid, kThreads, 5 * 8 * 9 * sizeof(double2), stream, prm, tk);
+          else launch_k(panel_inv_kernel<4>, grid, kThreads, 5 * 4 * 5 * sizeof(double2), stream, prm, tk);
           break;
         case kLTrsm: {
           const int ir = g_inv_launch ? 1 : 0;  // inverses published by the kLPanelInv launch
