@@ -631,6 +631,7 @@ struct Scr {
   int* SIG;     // pivoted position -> merged position      [s]
   int* ISG;     // merged position -> pivoted position      [s]
   int* PERM;    // current panel's net row interchange: {nd, src[64], dst[64]}
+  int* PERM2;   // the first panel's PERM of a wide (two-panel) block, saved for the wide TRSM
   double* scale;
   double* pmax;   // per gather row chunk: max |A(S,S)| over its rows   [ceil(n/16)]
   double2* LINV;  // per panel j: L_jj^-1  [NB][NB]   (valid when nb > 0)
@@ -647,7 +648,8 @@ __device__ __forceinline__ Scr scratch_of(const SolveParams& P, const ElimDesc& 
   r.SIG = r.PIV + d.s;
   r.ISG = r.SIG + d.s;
   r.PERM = r.ISG + d.s;
-  const int64_t ints = (3 * d.s + 132 + 3) / 4;
+  r.PERM2 = r.PERM + 132;
+  const int64_t ints = (3 * d.s + 264 + 3) / 4;
   r.scale = reinterpret_cast<double*>(r.M + 2 * nn + ints);
   r.pmax = r.scale + 2;
   r.LINV = r.M + 2 * nn + ints + 1 + (d.n + 31) / 32;
@@ -1621,6 +1623,59 @@ struct TrsmTiles<8> { using U = Tile<1, 8, 1, 1, false>; using L = Tile<8, 1, 1,
 template <>
 struct TrsmTiles<4> { using U = Tile<1, 8, 1, 1, false>; using L = Tile<8, 1, 1, 1, false>; };
 
+// ---- wide (two-panel) block TRSM for columns [c0, c0+64) right of the block [J0, J0+2NB):
+// both panels' row interchanges in order (PERM2 of panel j-1 at J0, PERM of panel j at
+// J0+NB), then U12 = L_JJ^-1 A12 as top = L1^-1 A_top, A_bot -= L21 top, bot = L2^-1 A_bot.
+template <int NB>
+__device__ void wide_trsm_tile(const Scr& S, int n, int s, int j, int c0, double2* smem) {
+  using TT = typename TrsmTiles<NB>::U;
+  double2* M = S.M;
+  const int J0 = (j - 1) * NB, jb2 = min(NB, s - j * NB);
+  const int cn = min(kTile, n - c0);
+  double2* st = smem;  // [2 NB][64] staging of the moved rows
+  for (int pass = 0; pass < 2; ++pass) {
+    const int* perm = pass == 0 ? S.PERM2 : S.PERM;
+    const int base = pass == 0 ? J0 : J0 + NB;
+    const int nd = perm[0];
+    for (int q = threadIdx.x; q < nd * kTile; q += kThreads) {
+      const int k = q / kTile, c = q % kTile;
+      if (c < cn) st[q] = M[(int64_t)(base + perm[1 + k]) * n + c0 + c];
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nd * kTile; q += kThreads) {
+      const int k = q / kTile, c = q % kTile;
+      if (c < cn) M[(int64_t)(base + perm[1 + 2 * NB + k]) * n + c0 + c] = st[q];
+    }
+    __syncthreads();
+  }
+  double2* top = M + (int64_t)J0 * n + c0;
+  double2* bot = M + (int64_t)(J0 + NB) * n + c0;
+  {
+    TT T;
+    T.zero();
+    T.mma(S.LINV + (int64_t)(j - 1) * NB * NB, NB, top, n, NB, cn, NB, smem);
+    T.for_each([&](int r, int c, double2 v) {
+      if (r < NB && c < cn) top[(int64_t)r * n + c] = v;
+    });
+  }
+  __syncthreads();
+  {
+    TT T;
+    T.zero();
+    T.mma(M + (int64_t)(J0 + NB) * n + J0, n, top, n, jb2, cn, NB, smem);
+    T.for_each([&](int r, int c, double2 v) {
+      if (r < jb2 && c < cn) bot[(int64_t)r * n + c] = csub(bot[(int64_t)r * n + c], v);
+    });
+  }
+  __syncthreads();
+  TT T;
+  T.zero();
+  T.mma(S.LINV + (int64_t)j * NB * NB, NB, bot, n, jb2, cn, jb2, smem);
+  T.for_each([&](int r, int c, double2 v) {
+    if (r < jb2 && c < cn) bot[(int64_t)r * n + c] = v;
+  });
+}
+
 template <int NB>
 __device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, double2* smem, bool inv_ready = false) {
   const ElimDesc d = P.elims[t.e];
@@ -1628,10 +1683,18 @@ __device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, dou
   const int j0 = j * NB, jb = min(NB, s - j0);
   const Scr S = scratch_of(P, d, e, NB);
   double2* M = S.M;
+  if (t.a == 5) {  // wide block: keep the first panel's interchanges for the wide TRSM
+    for (int k = threadIdx.x; k < 1 + 4 * NB; k += kThreads) S.PERM2[k] = S.PERM[k];
+    return;
+  }
+  if (t.a == 3) {  // wide TRSM: this is the block's second panel j; columns [c0, c0+64) right of it
+    wide_trsm_tile<NB>(S, n, s, j, t.b, smem);
+    return;
+  }
   if (t.a != 1) {
-    // this panel's row interchanges on columns [c0, c0+64) (solver-side zgetrf laswp):
-    // all moved rows are read before any is written
-    const int c0 = t.b, cn = min(kTile, (t.a == 2 ? j0 : n) - c0);
+    // this panel's row interchanges on columns [c0, c0+64) (solver-side zgetrf laswp), or the
+    // t.c-wide strip of the next panel of a wide block: all moved rows are read before any is written
+    const int c0 = t.b, cn = min(t.c > 0 ? t.c : kTile, (t.a == 2 ? j0 : n) - c0);
     const int nd = S.PERM[0];
     double2* st = smem;  // [2 NB][64]
     for (int q = threadIdx.x; q < nd * kTile; q += kThreads) {
@@ -1672,9 +1735,10 @@ __device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, dou
     double2* B = M + (int64_t)j0 * n + c0;
     TT T;
     T.zero();
-    T.mma(S.LINV + (int64_t)j * NB * NB, NB, B, n, jb, min(kTile, n - c0), jb, smem);
+    const int cn = min(t.c > 0 ? t.c : kTile, n - c0);
+    T.mma(S.LINV + (int64_t)j * NB * NB, NB, B, n, jb, cn, jb, smem);
     T.for_each([&](int r, int c, double2 v) {
-      if (r < jb && c0 + c < n) B[(int64_t)r * n + c] = v;
+      if (r < jb && c < cn) B[(int64_t)r * n + c] = v;
     });
   } else {
     using TT = typename TrsmTiles<NB>::L;
@@ -1732,17 +1796,20 @@ __global__ void __launch_bounds__(kThreads) panel_inv_kernel(SolveParams P, cons
 }
 
 // ---- trailing update M[j1:, j1:] -= M[j1:, j0:j1] M[j0:j1, j1:]
+// t.c: 0 the full trailing update of panel j; 2 only the next panel's columns (the strip of
+// a wide block); 1 the wide block's update, K = both panels (j-1, j)
 __device__ void trail_body(const SolveParams& P, const Task& t, int e, int j, int nb, double2* smem) {
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s;
-  const int j0 = j * nb, jb = min(nb, s - j0), j1 = j0 + jb;
+  const int j0 = (t.c == 1 ? j - 1 : j) * nb, j1 = min(s, (j + 1) * nb), jb = j1 - j0;
   double2* M = scratch_of(P, d, e).M;
   const int r0 = j1 + t.a * kTile, c0 = j1 + t.b * kTile;
+  const int cw = t.c == 2 ? min(nb, s - j1) : kTile;
   Tile64 T;
   T.zero();
-  T.mma(M + (int64_t)r0 * n + j0, n, M + (int64_t)j0 * n + c0, n, min(kTile, n - r0), min(kTile, n - c0), jb, smem);
+  T.mma(M + (int64_t)r0 * n + j0, n, M + (int64_t)j0 * n + c0, n, min(kTile, n - r0), min(cw, n - c0), jb, smem);
   T.for_each([&](int r, int c, double2 v) {
-    if (r0 + r < n && c0 + c < n && (r0 + r < s || c0 + c < s)) {
+    if (r0 + r < n && c < cw && c0 + c < n && (r0 + r < s || c0 + c < s)) {
       double2* p = M + (int64_t)(r0 + r) * n + c0 + c;
       *p = csub(*p, v);
     }

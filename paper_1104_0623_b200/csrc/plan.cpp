@@ -46,7 +46,7 @@ void set_status(find_status* st, int code, const char* msg) {
 // the inverted diagonal blocks L_jj^-1, U_jj^-1 of every panel (nb x nb).
 // Must match scratch_of() in find_solve.cu.
 int64_t find_scratch_elems(int64_t n, int64_t s, int nb) {
-  int64_t e = 2 * n * n + (3 * s + 132 + 3) / 4 + 1 + (n + 31) / 32;
+  int64_t e = 2 * n * n + (3 * s + 264 + 3) / 4 + 1 + (n + 31) / 32;
   if (nb > 0) e += 2 * ((s + nb - 1) / nb) * (int64_t)nb * nb + (n - s) * s;  // + X [b][s]
   return (e + 1) & ~int64_t(1);
 }
@@ -79,6 +79,12 @@ void find_assign_phases(find_plan* P) {
 }
 
 // Flattened task lists of every phase launch (see LaunchKind).
+// Groups whose largest S exceeds this use wide (K = 64) trailing updates (FIND_B200_WIDE_MIN_S).
+int wide_min_s() {
+  const char* f = std::getenv("FIND_B200_WIDE_MIN_S");
+  return f ? std::atoi(f) : 288;
+}
+
 void find_build_tasks(find_plan* P) {
   P->tasks.clear();
   P->specs.clear();
@@ -110,6 +116,13 @@ void find_build_tasks(find_plan* P) {
     }
     spec(kLGatherA, 0, nb, gi, off);
     const int steps = nb ? (G.max_s + nb - 1) / nb : 0;
+    // Wide blocks (large S, NB = 32): panels (2k, 2k+1) of an elimination share one trailing
+    // update with K = 64.  After panel 2k only the next panel's columns (the strip) get its
+    // interchanges, U12 and update; after panel 2k+1 a wide TRSM applies both panels'
+    // interchanges and L_JJ^-1 to the columns right of the block, then one K = 64 update.
+    const bool wide = nb == 32 && G.max_s > wide_min_s();
+    auto first_of_wide = [&](const ElimDesc& d, int j) { return wide && j % 2 == 0 && d.s > (j + 1) * nb; };
+    auto second_of_wide = [&](const ElimDesc& d, int j) { return wide && j % 2 == 1 && d.s > j * nb; };
     for (int j = 0; j < steps; ++j) {
       off = (int64_t)P->tasks.size();
       for (int64_t e = G.begin; e < G.end; ++e)
@@ -125,9 +138,21 @@ void find_build_tasks(find_plan* P) {
         const ElimDesc& d = P->elims[e];
         if (d.s <= j * nb) continue;
         const int j1 = std::min(d.s, (j + 1) * nb);
-        for (int c0 = j1; c0 < d.n; c0 += kTile) push((int32_t)e, 0, c0, 0);
+        if (first_of_wide(d, j)) {
+          push((int32_t)e, 0, j1, std::min(nb, d.s - j1));  // the strip: next panel's columns
+          push((int32_t)e, 5, 0, 0);                        // keep this panel's interchanges
+        } else if (!second_of_wide(d, j)) {
+          for (int c0 = j1; c0 < d.n; c0 += kTile) push((int32_t)e, 0, c0, 0);
+        }
         for (int r0 = 0; r0 < d.b; r0 += kTile) push((int32_t)e, 1, r0, 0);
         for (int c0 = 0; c0 < j * nb; c0 += kTile) push((int32_t)e, 2, c0, 0);  // interchanges on L columns
+      }
+      spec(kLTrsm, j, nb, gi, off);
+      off = (int64_t)P->tasks.size();
+      for (int64_t e = G.begin; e < G.end; ++e) {  // wide TRSM, columns right of the block
+        const ElimDesc& d = P->elims[e];
+        if (!second_of_wide(d, j)) continue;
+        for (int c0 = std::min(d.s, (j + 1) * nb); c0 < d.n; c0 += kTile) push((int32_t)e, 3, c0, 0);
       }
       spec(kLTrsm, j, nb, gi, off);
       off = (int64_t)P->tasks.size();
@@ -136,9 +161,14 @@ void find_build_tasks(find_plan* P) {
         if (d.s <= j * nb) continue;
         const int j1 = std::min(d.s, (j + 1) * nb), m = d.n - j1;
         const int t = (m + kTile - 1) / kTile;
+        if (first_of_wide(d, j)) {  // strip columns only, every row below the panel
+          for (int tm = 0; tm < t; ++tm) push((int32_t)e, tm, 0, 2);
+          continue;
+        }
+        const int mode = second_of_wide(d, j) ? 1 : 0;
         for (int tm = 0; tm < t; ++tm)
           for (int tn = 0; tn < t; ++tn)  // the B x B block is updated once, by the Schur launch
-            if (j1 + tm * kTile < d.s || j1 + tn * kTile < d.s) push((int32_t)e, tm, tn, 0);
+            if (j1 + tm * kTile < d.s || j1 + tn * kTile < d.s) push((int32_t)e, tm, tn, mode);
       }
       spec(kLTrail, j, nb, gi, off);
     }

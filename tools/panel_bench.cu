@@ -9,7 +9,7 @@
 using namespace findb200;
 
 static int64_t scratch_elems(int64_t n, int64_t s, int nb) {  // find_scratch_elems (plan.cpp)
-  int64_t e = 2 * n * n + (3 * s + 132 + 3) / 4 + 1 + (n + 31) / 32;
+  int64_t e = 2 * n * n + (3 * s + 264 + 3) / 4 + 1 + (n + 31) / 32;
   if (nb > 0) e += 2 * ((s + nb - 1) / nb) * (int64_t)nb * nb + (n - s) * s;
   return (e + 1) & ~int64_t(1);
 }
@@ -46,7 +46,7 @@ int main(int argc, char** argv) {
     for (int i = 0; i < count; ++i) {
       double2* M = h.data() + (size_t)e * total + (size_t)i * per;
       const int64_t nn = (int64_t)n * n;
-      const int64_t ints = (3 * s + 132 + 3) / 4;
+      const int64_t ints = (3 * s + 264 + 3) / 4;
       double* scale = reinterpret_cast<double*>(M + 2 * nn + ints);
       for (int q = 0; q < (n + 31) / 32 * 2; ++q) scale[2 + q] = 1.0;
     }
