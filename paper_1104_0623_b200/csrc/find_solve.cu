@@ -100,8 +100,8 @@ struct SolveParams {
   int32_t compute_gless;
   int32_t rsym;  // 0 general; +1 Sigma (hence every R) Hermitian; -1 skew-Hermitian
   double rtol;
-  double2* arena[3];
-  int64_t arena_elems[3];
+  double2* arena[kNumArenas];
+  int64_t arena_elems[kNumArenas];
   double2* scratch;
   int64_t scratch_elems;
   double2* gr_out;  // [nE][n]
@@ -2574,6 +2574,8 @@ struct SideStreams {
   cudaStream_t s[kSideStreams + kHiStreams] = {};
   cudaEvent_t fork[64] = {}, join[64] = {};
   int next = 0;
+  cudaStream_t joiner = nullptr;     // dependency scheduling: per-phase join events are recorded here
+  std::vector<cudaEvent_t> gev, jev;  // per launch group / per phase completion
 };
 SideStreams g_side;
 
@@ -2589,6 +2591,7 @@ int side_init(find_status* st) {
     CUDA_TRY(cudaEventCreateWithFlags(&g_side.fork[i], cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&g_side.join[i], cudaEventDisableTiming));
   }
+  CUDA_TRY(cudaStreamCreateWithFlags(&g_side.joiner, cudaStreamNonBlocking));
   g_side.device = dev;
   return FIND_OK;
 }
@@ -2671,6 +2674,64 @@ const bool g_prio = [] {
   return !(f && f[0] == '0');
 }();
 
+// Dependency scheduling (plans built with dag): every group waits only for the groups that
+// produce its input blocks and for every group two or more phases back (the scratch half and
+// the down arena it reuses), so a phase's tail overlaps the next phase's first launches.
+// FIND_B200_DAG=0 falls back to phase barriers.
+const bool g_dag = [] {
+  const char* f = std::getenv("FIND_B200_DAG");
+  return !(f && f[0] == '0');
+}();
+
+int grow_events(std::vector<cudaEvent_t>& v, size_t n, find_status* st) {
+  while (v.size() < n) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    v.push_back(e);
+  }
+  return FIND_OK;
+}
+
+int run_groups_dag(const find_plan* P, const SolveParams& prm, int64_t g_begin, int64_t g_end, int nE,
+                   cudaStream_t stream, find_status* st) {
+  const int np = P->groups.back().phase + 1;
+  int rc = grow_events(g_side.gev, P->groups.size(), st);
+  if (!rc) rc = grow_events(g_side.jev, (size_t)np, st);
+  if (rc) return rc;
+  const int slot = g_side.next;
+  g_side.next = (g_side.next + 1) % 64;
+  CUDA_TRY(cudaEventRecord(g_side.fork[slot], stream));
+  for (int k = 0; k < kSideStreams + kHiStreams; ++k) CUDA_TRY(cudaStreamWaitEvent(g_side.s[k], g_side.fork[slot], 0));
+  CUDA_TRY(cudaStreamWaitEvent(g_side.joiner, g_side.fork[slot], 0));
+  const int p_first = P->groups[g_begin].phase;
+  int lo = 0, hi = 0, last_phase = p_first;
+  int64_t gi = g_begin;
+  while (gi < g_end) {
+    int64_t ge = gi;
+    const int p = P->groups[gi].phase;
+    while (ge < g_end && P->groups[ge].phase == p) ++ge;
+    int64_t longest = 0;
+    for (int64_t g = gi; g < ge; ++g) longest = std::max(longest, P->groups[g].spec_end - P->groups[g].spec_begin);
+    for (int pass = 0; pass < 2; ++pass)  // critical chains first, on the high-priority streams
+      for (int64_t g = gi; g < ge; ++g) {
+        const bool crit = g_prio && 4 * (P->groups[g].spec_end - P->groups[g].spec_begin) >= 3 * longest;
+        if (crit != (pass == 0)) continue;
+        cudaStream_t sg = crit ? g_side.s[kSideStreams + (hi++ % kHiStreams)] : g_side.s[lo++ % kSideStreams];
+        for (int32_t dgp : P->group_deps[g])
+          if (dgp >= g_begin && dgp < g) CUDA_TRY(cudaStreamWaitEvent(sg, g_side.gev[dgp], 0));
+        if (p - 2 >= p_first) CUDA_TRY(cudaStreamWaitEvent(sg, g_side.jev[p - 2], 0));
+        if ((rc = run_one_group(P, prm, g, nE, sg, st))) return rc;
+        CUDA_TRY(cudaEventRecord(g_side.gev[g], sg));
+      }
+    for (int64_t g = gi; g < ge; ++g) CUDA_TRY(cudaStreamWaitEvent(g_side.joiner, g_side.gev[g], 0));
+    CUDA_TRY(cudaEventRecord(g_side.jev[p], g_side.joiner));  // every group of phases <= p done
+    last_phase = p;
+    gi = ge;
+  }
+  CUDA_TRY(cudaStreamWaitEvent(stream, g_side.jev[last_phase], 0));
+  return FIND_OK;
+}
+
 // Enqueue the launches of groups [g_begin, g_end): phase by phase; the groups
 // of a phase fork onto side streams and join back into `stream`.
 int run_groups(const find_plan* P, const SolveParams& prm, int64_t g_begin, int64_t g_end, int nE,
@@ -2678,6 +2739,7 @@ int run_groups(const find_plan* P, const SolveParams& prm, int64_t g_begin, int6
   int rc = set_attrs(st);
   if (rc) return rc;
   if ((rc = side_init(st))) return rc;
+  if (P->dag && g_dag && g_end > g_begin) return run_groups_dag(P, prm, g_begin, g_end, nE, stream, st);
   int64_t gi = g_begin;
   while (gi < g_end) {
     int64_t ge = gi;
@@ -2917,7 +2979,7 @@ SolveParams make_params(const find_plan* P, void* ws, int nE) {
   prm.nnz = P->nnz;
   prm.status = (unsigned long long*)base;
   size_t off = ws_header_bytes();
-  for (int a = 0; a < 3; ++a) {
+  for (int a = 0; a < kNumArenas; ++a) {
     prm.arena[a] = (double2*)(base + off);
     prm.arena_elems[a] = P->arena_elems[a];
     off += (size_t)nE * P->arena_elems[a] * sizeof(double2);
@@ -2971,7 +3033,7 @@ size_t find_solve_workspace_bytes(const find_plan* P, int32_t nE, int32_t comput
   (void)compute_gless;
   if (!P || nE < 1) return 0;
   size_t b = ws_header_bytes();
-  for (int a = 0; a < 3; ++a) b += (size_t)nE * P->arena_elems[a] * sizeof(double2);
+  for (int a = 0; a < kNumArenas; ++a) b += (size_t)nE * P->arena_elems[a] * sizeof(double2);
   b += (size_t)nE * P->ws_elems * sizeof(double2);
   return b;
 }
@@ -3206,6 +3268,7 @@ int find_schur_sigma_update(int32_t s, int32_t b, const void* ass, const void* a
   Q.arena_elems[kArenaUp] = 2 * (int64_t)n * n;
   Q.arena_elems[kArenaDown0] = 2 * (int64_t)b * b + 2;
   Q.arena_elems[kArenaDown1] = 0;
+  Q.arena_elems[kArenaDown2] = 0;
   Q.ws_elems = G.ws_elems;
   find_build_tasks(&Q);
   int rc = find_plan_upload(&Q, st);

@@ -12,6 +12,7 @@
 //   _Engine.store             solver.py:234-243   (U/R re-sorted to ascending B)
 //   FlopLedger charges        kernels.py:88-146, 379, 391, 436; solver.py:388, 664
 #include <algorithm>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -75,6 +76,32 @@ void find_assign_phases(find_plan* P) {
       base += G.ws_elems;
     }
     P->ws_elems = std::max(P->ws_elems, base);
+  }
+  if (P->dag) {  // phase parity halves: a phase may still run while the next one starts
+    for (auto& G : P->groups)
+      if (G.path == 1 && (G.phase & 1))
+        for (int64_t k = G.begin; k < G.end; ++k) P->elims[k].ws_off += P->ws_elems;
+    P->ws_elems *= 2;
+  }
+  // producer of every group's input blocks: the latest earlier group that wrote that
+  // (arena, offset) — down arenas are reused every two or three levels
+  P->group_deps.assign(P->groups.size(), {});
+  std::map<std::pair<int32_t, int64_t>, int32_t> prod;
+  for (int32_t g = 0; g < (int32_t)P->groups.size(); ++g) {
+    std::vector<int32_t>& dv = P->group_deps[g];
+    for (int64_t k = P->groups[g].begin; k < P->groups[g].end; ++k) {
+      const ElimDesc& d = P->elims[k];
+      for (int side = 0; side < 2; ++side) {
+        const int32_t a = side ? d.right_arena : d.left_arena;
+        if (a < 0) continue;
+        auto it = prod.find({a, side ? d.right_off : d.left_off});
+        if (it != prod.end() && it->second != g) dv.push_back(it->second);
+      }
+    }
+    std::sort(dv.begin(), dv.end());
+    dv.erase(std::unique(dv.begin(), dv.end()), dv.end());
+    for (int64_t k = P->groups[g].begin; k < P->groups[g].end; ++k)
+      if (P->elims[k].out_arena >= 0) prod[{P->elims[k].out_arena, P->elims[k].out_off}] = g;
   }
 }
 
@@ -515,6 +542,7 @@ struct Builder {
       down_max = std::max(down_max, a);
     }
     P->arena_elems[kArenaDown0] = P->arena_elems[kArenaDown1] = down_max;
+    P->arena_elems[kArenaDown2] = P->dag ? down_max : 0;
     const std::vector<int64_t> empty;
 
     auto emit_groups = [&](int64_t begin, int32_t pass, int32_t level) {
@@ -627,8 +655,10 @@ struct Builder {
     // ---- downward pass (solver.py:311-375) level by level, finals right after ----
     for (int32_t L = 1; L <= D; ++L) {
       int64_t begin = (int64_t)P->elims.size();
-      int32_t arena = (L % 2 == 1) ? kArenaDown1 : kArenaDown0;
-      int32_t parena = (L % 2 == 1) ? kArenaDown0 : kArenaDown1;
+      // ping-pong by level parity; three rotating arenas when consecutive phases may overlap
+      const int32_t rot = P->dag ? 3 : 2;
+      int32_t arena = kArenaDown0 + L % rot;
+      int32_t parena = kArenaDown0 + (L - 1) % rot;
       for (int32_t i : by_level[L]) {
         const Cluster& c = C[i];
         const Cluster& par = C[c.parent];
@@ -710,6 +740,12 @@ int find_plan_create(int64_t nx, int64_t ny, const int64_t* indptr, const int64_
     P->nx = nx; P->ny = ny; P->n = n; P->nnz = nnz; P->leaf_max = leaf_max;
     P->indptr.assign(indptr, indptr + n + 1);
     P->indices.assign(indices, indices + nnz);
+    {  // dependency scheduling for meshes up to FIND_B200_DAG_MAX_N nodes: off by default (measured
+       // neutral on cfg1 while it costs a third down arena and a second scratch half)
+      const char* f = std::getenv("FIND_B200_DAG_MAX_N");
+      const int64_t lim = f ? std::atoll(f) : 0;
+      P->dag = n <= lim;
+    }
     Builder B(P);
     B.build_tree();
     B.annotate();

@@ -18,7 +18,8 @@ enum ElimKind : int32_t {
 };
 
 // Arenas that hold per-cluster (U, R) blocks, one copy per energy point.
-enum Arena : int32_t { kArenaNone = -1, kArenaUp = 0, kArenaDown0 = 1, kArenaDown1 = 2 };
+enum Arena : int32_t { kArenaNone = -1, kArenaUp = 0, kArenaDown0 = 1, kArenaDown1 = 2, kArenaDown2 = 3 };
+constexpr int kNumArenas = 4;
 
 // One elimination (one merge + Schur/Sigma update), POD, device-visible.
 struct alignas(16) ElimDesc {
@@ -139,7 +140,12 @@ struct find_plan {
   std::vector<int64_t> exc_slots[2];         // CSR slots of structure-exception entries (up, down)
   std::vector<findb200::Task> tasks;
   std::vector<findb200::LaunchSpec> specs;
-  int64_t arena_elems[3] = {0, 0, 0};
+  int64_t arena_elems[findb200::kNumArenas] = {0, 0, 0, 0};
+  // dependency scheduling (plans small enough for the extra memory): consecutive phases may
+  // overlap; three rotating down arenas and two scratch halves (phase parity); per group the
+  // groups producing its input blocks
+  bool dag = false;
+  std::vector<std::vector<int32_t>> group_deps;
   int64_t ws_elems = 0;
   int32_t max_n = 0, max_s = 0, max_b = 0, depth = 0, n_leaves = 0;
   int32_t n_levels_up = 0, n_levels_down = 0;

@@ -1,6 +1,7 @@
-"""Both CTA-path variants (level-batched phase launches and the fused per-elimination
-LU) against the reference's golden outputs, selected through FIND_B200_FUSED in a
-fresh process (the choice is read once per process)."""
+"""CTA-path variants (level-batched phase launches, the fused per-elimination LU, panel
+widths and kinds, dependency scheduling, wide blocks, per-tile inverses) against the
+reference's golden outputs, each selected through its environment switch in a fresh
+process (the choices are read once per process / plan)."""
 
 import json
 import os
@@ -39,7 +40,9 @@ print("RESULT", json.dumps(out))
                                  {"FIND_B200_FUSED": "0", "FIND_B200_NB": "16"},
                                  {"FIND_B200_FUSED": "0", "FIND_B200_NB": "8"},
                                  {"FIND_B200_FUSED": "0", "FIND_B200_SMEM_PANEL": "1"},
-                                 {"FIND_B200_PANEL": "reg"}, {"FIND_B200_PANEL": "warp"}])
+                                 {"FIND_B200_PANEL": "reg"}, {"FIND_B200_PANEL": "warp"},
+                                 {"FIND_B200_DAG_MAX_N": "100000"}, {"FIND_B200_WIDE_MIN_S": "0"},
+                                 {"FIND_B200_INV_LAUNCH": "0"}])
 def test_cta_path_variants_match_golden(cuda, env):
     code = SCRIPT.format(root=str(ROOT), tests=str(ROOT / "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
