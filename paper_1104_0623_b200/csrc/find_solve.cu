@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) small_elim_kernel(SolveParam
       const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
       if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
     }
-    const int pr = vi;
+    const int pr = [&] { const int q = __shfl_sync(0xffffffffu, vi, 0); return q >= k && q < s ? q : k; }();
     if (lane == 0) piv[k] = pr;
     if (pr != k && lane < n) {  // lane = column for the interchange
       const double2 tmp = MA[k * ld + lane];
@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kMidThreads) mid_elim_kernel(SolveParams P, in
       if (a > v) { v = a; vi = r; }
     }
     block_argmax<NT>(v, vi, cv[k & 1], ci[k & 1]);
-    const int pr = vi;
+    const int pr = vi >= k && vi < s ? vi : k;  // NaN / Inf entries: no interchange
     if (tid == 0) {
       piv[k] = pr;
       const double2 u = MA[pr * ld + k];
@@ -981,7 +981,7 @@ __device__ void panel_body(const SolveParams& P, int64_t eidx, const ElimDesc& d
     double v = (has && pos >= jj) ? cabs1(row[0]) : -1.0;
     int vi = (has && pos >= jj) ? pos : INT32_MAX;
     block_argmax<T>(v, vi, cand_v[buf], cand_i[buf]);
-    const int pr = vi;
+    const int pr = vi >= jj && vi < R ? vi : jj;  // NaN / Inf entries: no interchange
     const bool winner = has && pos == pr;
     if (winner) {
 #pragma unroll
@@ -1152,7 +1152,8 @@ __global__ void __launch_bounds__(T, (T <= 96 ? 3 : (T <= 192 ? 2 : 1))) panel1_
     const int bhi = __reduce_max_sync(0xffffffffu, whi);
     const unsigned wlo = (unsigned)__double2loint(cvw);
     const unsigned blo = __reduce_max_sync(0xffffffffu, whi == bhi ? wlo : 0u);
-    const int pr = (int)__reduce_min_sync(0xffffffffu, (unsigned)((whi == bhi && wlo == blo) ? ciw : INT32_MAX));
+    const int pr0 = (int)__reduce_min_sync(0xffffffffu, (unsigned)((whi == bhi && wlo == blo) ? ciw : INT32_MAX));
+    const int pr = pr0 >= jj && pr0 < R ? pr0 : jj;  // NaN / Inf entries: no interchange
     // only the pivot row is published (live part + its inverse), then a second barrier
     if (has && pos == pr) {
       double2* slot = cand[buf][0];
@@ -1280,7 +1281,7 @@ __global__ void __launch_bounds__(256) warp_panel_kernel(SolveParams P, const Ta
       const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
       if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
     }
-    const int pr = vi;
+    const int pr = vi >= jj && vi < R ? vi : jj;  // NaN / Inf entries: no interchange
     if (pr != jj) {
       for (int c = lane; c < NB; c += 32) {
         const double2 x = A[jj * LD + c];
@@ -1393,7 +1394,7 @@ __global__ void __launch_bounds__(kThreads) panel_smem_kernel(SolveParams P, con
       if (a > v) { v = a; vi = r; }
     }
     block_argmax<kThreads>(v, vi, cand_v[jj & 1], cand_i[jj & 1]);
-    const int pr = vi;
+    const int pr = vi >= jj && vi < R ? vi : jj;  // NaN / Inf entries: no interchange
     if (tid == 0) {
       lpiv[jj] = pr;
       S.PIV[j0 + jj] = j0 + pr;
@@ -1540,6 +1541,7 @@ __global__ void __launch_bounds__(kThreads) panel_cluster_kernel(SolveParams P, 
       const int oi = cand_i[buf][k];
       if (ov > bv || (ov == bv && oi < pr)) { bv = ov; pr = oi; }
     }
+    if (pr < jj || pr >= R) pr = jj;  // NaN / Inf entries: no interchange
     const int own_pr = pr / chunk, own_jj = jj / chunk;
     if (rank == own_pr) {  // broadcast the pivot row and 1/u
       const double2* src = panel + (pr - r_lo) * PS;
