@@ -1857,13 +1857,12 @@ __global__ void __launch_bounds__(kThreads, 2) schur_kernel(SolveParams P, const
 // ---- X_j = (Y_j - X_{>j} L11[>j, j]) L_jj^-1 for 64 B rows: Z = Y_j - X_{>j} L11[>j, j]
 // (one DMMA tile, K = s - j1) is written to X_j, then X_j = Z L_jj^-1 (second DMMA
 // tile, K = jb) with the inverse published by the panel / TRSM launch of step j.
-template <int NB>
-__device__ void xsolve_tile(const Scr& S, int n, int s, int j, int r0, double2* smem) {
-  using TT = typename XTileSel<NB>::T;
+template <int NB, class TT = typename XTileSel<NB>::T>
+__device__ void xsolve_tile(const Scr& S, int n, int s, int j, int r0, double2* smem, int rows = kTile) {
   double2* M = S.M;
   const int b = n - s;
   const int j0 = j * NB, jb = min(NB, s - j0), j1 = j0 + jb;
-  const int nr = min(kTile, b - r0);
+  const int nr = min(rows, b - r0);
   {
     TT T;
     T.zero();
@@ -1891,6 +1890,11 @@ __global__ void __launch_bounds__(kThreads) xsolve_kernel(SolveParams P, const T
   const int e = blockIdx.y;
   const ElimDesc d = P.elims[t.e];
   const Scr S = scratch_of(P, d, e, NB);
+  if (NB == 32 && t.b == 16) {  // 16-row tiles: 4x the CTAs for groups with few row tiles
+    for (int j = (d.s + NB - 1) / NB - 1; j >= 0; --j)
+      xsolve_tile<NB, Tile<2, 4, 1, 1, false>>(S, d.n, d.s, j, t.a * 16, reinterpret_cast<double2*>(smem_raw), 16);
+    return;
+  }
   for (int j = (d.s + NB - 1) / NB - 1; j >= 0; --j)
     xsolve_tile<NB>(S, d.n, d.s, j, t.a * kTile, reinterpret_cast<double2*>(smem_raw));
 }

@@ -106,6 +106,12 @@ void find_assign_phases(find_plan* P) {
 }
 
 // Flattened task lists of every phase launch (see LaunchKind).
+// X solve with 16-row tiles for groups with fewer than 148 row tiles of 64 (FIND_B200_XS16=0 disables).
+bool xsolve16_enabled() {
+  const char* f = std::getenv("FIND_B200_XS16");
+  return !(f && f[0] == '0');
+}
+
 // Groups whose largest S exceeds this use wide (K = 64) trailing updates (FIND_B200_WIDE_MIN_S).
 int wide_min_s() {
   const char* f = std::getenv("FIND_B200_WIDE_MIN_S");
@@ -211,10 +217,16 @@ void find_build_tasks(find_plan* P) {
     // X = Y L11^-1: one task per 64-row tile of B, each walking the block columns right to
     // left (a row tile depends only on its own rows of X)
     off = (int64_t)P->tasks.size();
-    for (int64_t e = G.begin; e < G.end; ++e) {
-      const ElimDesc& d = P->elims[e];
-      if (d.s == 0 || d.b == 0) continue;
-      for (int tm = 0; tm < (d.b + kTile - 1) / kTile; ++tm) push((int32_t)e, tm, 0, 0);
+    {
+      int64_t tiles = 0;  // few 64-row tiles (large-S groups): 16-row tiles, 4x the parallelism
+      for (int64_t e = G.begin; e < G.end; ++e)
+        if (P->elims[e].s > 0) tiles += (P->elims[e].b + kTile - 1) / kTile;
+      const int rows = (nb == 32 && tiles < 148 && xsolve16_enabled()) ? 16 : kTile;
+      for (int64_t e = G.begin; e < G.end; ++e) {
+        const ElimDesc& d = P->elims[e];
+        if (d.s == 0 || d.b == 0) continue;
+        for (int tm = 0; tm < (d.b + rows - 1) / rows; ++tm) push((int32_t)e, tm, rows == 16 ? 16 : 0, 0);
+      }
     }
     spec(kLXSolve, -1, nb, gi, off);
     off = (int64_t)P->tasks.size();
