@@ -77,6 +77,12 @@ int64_t find_plan_cluster_set(const find_plan* plan, int64_t label, int32_t whic
  * n_elims entries (find_plan_info out[3]). */
 int find_plan_elims(const find_plan* plan, int32_t* kind, int32_t* s, int32_t* b, int64_t* label);
 
+/* Per elimination (find_plan_elims order): when the block A(B_r, S_l) of the merged
+ * matrix [S_l, S_r, B_l, B_r] is structurally zero (no exception entry; the paper's zero
+ * sub-blocks, kernels.py:400-463), s_left = |S_l| and b_left = |B_l| (the kernels then skip
+ * the products with Y(B_r, S_l) = 0); otherwise both 0.  Any pointer may be NULL. */
+int find_plan_elim_splits(const find_plan* plan, int32_t* s_left, int32_t* b_left);
+
 /* CSR slots of the merge-structure exception entries (kernels.py:192-202,
  * counted into SelectedInverse.stats at solver.py:217-219) for pass 0
  * (upward merges) or 1 (downward merges); an entry counts when its value is

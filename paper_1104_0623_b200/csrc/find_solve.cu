@@ -117,6 +117,7 @@ struct SolveParams {
   const int64_t* off_item_off;
   int64_t n_pairs;
   int32_t off_sym;  // +1 / -1: Sigma^< exactly Hermitian / skew-Hermitian (then G^< is too), 0 general
+  int32_t zskip;    // skip the products of structurally zero (B_r, S_l) blocks (ElimDesc::zsplit)
 };
 
 __device__ __forceinline__ void report_bad(const SolveParams& P, int64_t elim_global, int e, int pos) {
@@ -1693,6 +1694,8 @@ __device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, dou
     wide_trsm_tile<NB>(S, n, s, j, t.b, smem);
     return;
   }
+  if (t.a == 1 && inv_ready && P.zskip && d.zsplit && j0 + jb <= (d.zsplit & 0xffff) && t.b >= (d.zsplit >> 16))
+    return;  // L21 rows in B_r of a panel inside S_l: A(B_r, S_l) structurally zero, L21 stays zero
   if (t.a != 1) {
     // this panel's row interchanges on columns [c0, c0+64) (solver-side zgetrf laswp), or the
     // t.c-wide strip of the next panel of a wide block: all moved rows are read before any is written
@@ -1807,6 +1810,8 @@ __device__ void trail_body(const SolveParams& P, const Task& t, int e, int j, in
   double2* M = scratch_of(P, d, e).M;
   const int r0 = j1 + t.a * kTile, c0 = j1 + t.b * kTile;
   const int cw = t.c == 2 ? min(nb, s - j1) : kTile;
+  // all rows in B_r and the panel inside S_l with A(B_r, S_l) structurally zero: L21 = 0 there
+  if (P.zskip && d.zsplit && j1 <= (d.zsplit & 0xffff) && r0 >= s + (d.zsplit >> 16)) return;
   Tile64 T;
   T.zero();
   T.mma(M + (int64_t)r0 * n + j0, n, M + (int64_t)j0 * n + c0, n, min(kTile, n - r0), min(cw, n - c0), jb, smem);
@@ -1831,9 +1836,13 @@ __device__ void schur_body(const SolveParams& P, const Task& t, int e, double2* 
   const int n = d.n, s = d.s, b = d.b;
   double2* M = scratch_of(P, d, e).M;
   const int i0 = t.a * kTile, c0 = t.b * kTile;
+  // rows in B_r with A(B_r, S_l) structurally zero: Y is zero on the first s_l columns, so
+  // K starts at s_l (rounded down to the K chunk: the same products in the same order)
+  const int k0 = (P.zskip && d.zsplit && i0 >= (d.zsplit >> 16)) ? ((d.zsplit & 0xffff) / kKC) * kKC : 0;
   Tile64 T;
   T.zero();
-  T.mma(M + (int64_t)(s + i0) * n, n, M + s + c0, n, min(kTile, b - i0), min(kTile, b - c0), s, smem);
+  T.mma(M + (int64_t)(s + i0) * n + k0, n, M + (int64_t)k0 * n + s + c0, n, min(kTile, b - i0), min(kTile, b - c0),
+        s - k0, smem);
   const bool store = d.kind != kFinal && d.out_arena >= 0;
   double2* out = store ? P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off : nullptr;
   const int32_t* rank = P.i32 + d.rank_off;
@@ -2628,6 +2637,12 @@ const bool g_inv_launch = [] {
   return !(f && f[0] == '0');
 }();
 
+// Structural-zero skips (ElimDesc::zsplit), on unless FIND_B200_STRUCT=0.
+const bool g_zskip = [] {
+  const char* f = std::getenv("FIND_B200_STRUCT");
+  return !(f && f[0] == '0');
+}();
+
 // Fused-LU launches (one CTA per elimination and energy) instead of the
 // level-batched phase launches: opt-in (FIND_B200_FUSED=1, for groups that fill
 // the GPU); measured slower than the phase launches once the mid path takes the
@@ -3103,6 +3118,7 @@ int find_solve_offdiag_groups(find_plan* P, const void* a_vals, const void* s_va
   prm.rtol = rtol;
   prm.gr_out = (double2*)gr_out;
   prm.gl_out = (double2*)gl_out;
+  prm.zskip = g_zskip ? 1 : 0;
   if (off_gr) {
     prm.off_gr = (double2*)off_gr;
     prm.off_gl = (double2*)off_gl;

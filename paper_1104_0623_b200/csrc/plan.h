@@ -26,7 +26,7 @@ struct alignas(16) ElimDesc {
   int32_t s, b, n, p;        // |S|, |B|, s+b, |left|
   int32_t kind, nsparse;     // ElimKind, number of sparse (CSR-sourced) entries
   int32_t left_arena, right_arena;
-  int32_t out_arena, pad0;
+  int32_t out_arena, zsplit;  // zsplit: s_l | b_l << 16 when A(B_r, S_l) is structurally zero, else 0
   int64_t label;             // cluster label (negative = complement); final: leaf label
   int64_t left_off, right_off;  // complex-element offsets of child U blocks in their arena (R follows at +sz*sz)
   int64_t out_off;           // offset of the output U block (R at +b*b); final: unused

@@ -4,7 +4,9 @@ Counts the complex multiply-adds each kernel kind actually performs, from the
 plan's (s, b) per elimination and the group panel width; ``x 8`` gives real
 FP64 flops.  This is the kernels' own arithmetic (e.g. the Schur launch does
 s*b^2 = the sb^2 term of the reference's naive_dense count, kernels.py:90),
-distinct from the paper's ledger W that ``fp64_tflops`` is quoted on.
+distinct from the paper's ledger W that ``fp64_tflops`` is quoted on.  The structural-zero
+skips (ElimDesc::zsplit: Schur K from |S_l|, trailing / L21 tiles of B_r rows) are not
+subtracted: they remove about 4 % of the Schur MACs on cfg1 (find_plan_elim_splits).
 """
 
 from __future__ import annotations

@@ -42,7 +42,7 @@ print("RESULT", json.dumps(out))
                                  {"FIND_B200_FUSED": "0", "FIND_B200_SMEM_PANEL": "1"},
                                  {"FIND_B200_PANEL": "reg"}, {"FIND_B200_PANEL": "warp"},
                                  {"FIND_B200_DAG_MAX_N": "100000"}, {"FIND_B200_WIDE_MIN_S": "0"},
-                                 {"FIND_B200_INV_LAUNCH": "0"}])
+                                 {"FIND_B200_INV_LAUNCH": "0"}, {"FIND_B200_STRUCT": "0"}])
 def test_cta_path_variants_match_golden(cuda, env):
     code = SCRIPT.format(root=str(ROOT), tests=str(ROOT / "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
@@ -53,3 +53,28 @@ def test_cta_path_variants_match_golden(cuda, env):
     for name, (egr, egl) in res.items():
         assert egr < 1e-10 and egl < 1e-10, (name, egr, egl, env)
 
+
+
+HASH_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, {root!r})
+from paper_1104_0623_b200.configs import build_problem
+from paper_1104_0623_b200.plan import plan_for
+from paper_1104_0623_b200.solver import sigma_symmetry, solve_values
+p = build_problem(96, 40, [0.9, 2.7], seed=17, stencil=5)
+plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
+gr, gl, _, _ = solve_values(plan, p.a_vals_all(), p.s_vals, sigma_sym=sigma_symmetry(p.sigma_csr()))
+print("HASH", hashlib.sha1(gr.tobytes() + gl.tobytes()).hexdigest())
+"""
+
+
+def test_structural_zero_skips_are_bit_identical(cuda):
+    """The skipped (B_r, S_l) products are exact zeros: results bit-identical with and without."""
+    code = HASH_SCRIPT.format(root=str(ROOT))
+    out = []
+    for v in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "FIND_B200_STRUCT": v},
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out.append([l for l in r.stdout.splitlines() if l.startswith("HASH")][-1])
+    assert out[0] == out[1]
