@@ -1626,6 +1626,26 @@ struct TrsmTiles<8> { using U = Tile<1, 8, 1, 1, false>; using L = Tile<8, 1, 1,
 template <>
 struct TrsmTiles<4> { using U = Tile<1, 8, 1, 1, false>; using L = Tile<8, 1, 1, 1, false>; };
 
+// ---- pivot permutation sigma (pivoted position -> merged position) and its inverse from
+// the row interchanges PIV (LAPACK order); sig: shared scratch of s ints
+__device__ void finish_sigma(const Scr& S, int s, int* sig) {
+  const int tid = threadIdx.x;
+  for (int k = tid; k < s; k += blockDim.x) sig[k] = k;
+  __syncthreads();
+  if (tid == 0)
+    for (int k = 0; k < s; ++k) {
+      const int pk = S.PIV[k];
+      const int tmp = sig[k];
+      sig[k] = sig[pk];
+      sig[pk] = tmp;
+    }
+  __syncthreads();
+  for (int k = tid; k < s; k += blockDim.x) {
+    S.SIG[k] = sig[k];
+    S.ISG[sig[k]] = k;
+  }
+}
+
 // ---- wide (two-panel) block TRSM for columns [c0, c0+64) right of the block [J0, J0+2NB):
 // both panels' row interchanges in order (PERM2 of panel j-1 at J0, PERM of panel j at
 // J0+NB), then U12 = L_JJ^-1 A12 as top = L1^-1 A_top, A_bot -= L21 top, bot = L2^-1 A_bot.
@@ -1797,6 +1817,11 @@ __global__ void __launch_bounds__(kThreads) panel_inv_kernel(SolveParams P, cons
   for (int q = ht; q < NB * NB; q += H) {
     const int r = q / NB, c = q % NB;
     out[q] = (r < jb && c < jb) ? Xh[r][c] : cz();
+  }
+  if (j0 + jb == s) {  // last panel: every pivot is known -> sigma and its inverse (the finish step)
+    int* sig = reinterpret_cast<int*>(Wm + 3 * NB);
+    __syncthreads();
+    finish_sigma(S, s, sig);
   }
 }
 
@@ -2551,8 +2576,10 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<4>()));
-  CUDA_TRY(cudaFuncSetAttribute(panel_inv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(5 * 32 * 33 * sizeof(double2))));
+  CUDA_TRY(cudaFuncSetAttribute(panel_inv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(panel_inv_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(panel_inv_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(panel_inv_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<4>()));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<32>()));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem<16>()));
@@ -2837,6 +2864,9 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
       const LaunchSpec& L = P->specs[si];
       if (!prm.compute_gless && (L.kind == kLGatherS || L.kind == kLTGemm)) continue;
       if (L.kind == kLPanelInv && !g_inv_launch) continue;
+      // sigma comes from the last panel's inverse launch; the finish launch remains for the
+      // unit-test shim's L output (and when the inverse launches are off)
+      if (L.kind == kLFinish && g_inv_launch && !prm.dbg_l && !fused) continue;
       const Task* tk = dtasks + L.task_off;
       const unsigned cnt = (unsigned)L.task_count;
       const dim3 grid(cnt, (unsigned)nE);
@@ -2908,10 +2938,13 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           break;
         }
         case kLPanelInv:
-          if (L.nb == 32) launch_k(panel_inv_kernel<32>, grid, kThreads, 5 * 32 * 33 * sizeof(double2), stream, prm, tk);
-          else if (L.nb == 16) launch_k(panel_inv_kernel<16>, grid, kThreads, 5 * 16 * 17 * sizeof(double2), stream, prm, tk);
-          else if (L.nb == 8) launch_k(panel_inv_kernel<8>, grid, kThreads, 5 * 8 * 9 * sizeof(double2), stream, prm, tk);
-          else launch_k(panel_inv_kernel<4>, grid, kThreads, 5 * 4 * 5 * sizeof(double2), stream, prm, tk);
+        {
+          const size_t si = (size_t)G.max_s * sizeof(int);  // + sigma scratch (last panel)
+          if (L.nb == 32) launch_k(panel_inv_kernel<32>, grid, kThreads, 5 * 32 * 33 * sizeof(double2) + si, stream, prm, tk);
+          else if (L.nb == 16) launch_k(panel_inv_kernel<16>, grid, kThreads, 5 * 16 * 17 * sizeof(double2) + si, stream, prm, tk);
+          else if (L.nb == 8) launch_k(panel_inv_kernel<8>, grid, kThreads, 5 * 8 * 9 * sizeof(double2) + si, stream, prm, tk);
+          else launch_k(panel_inv_kernel<4>, grid, kThreads, 5 * 4 * 5 * sizeof(double2) + si, stream, prm, tk);
+        }
           break;
         case kLTrsm: {
           const int ir = g_inv_launch ? 1 : 0;  // inverses published by the kLPanelInv launch
@@ -2985,6 +3018,7 @@ void for_each_launch(const find_plan* P, int nE, F f) {
     const bool fu = use_fused(G, nE);
     for (int64_t si = fu ? G.fspec_begin : G.spec_begin; si < (fu ? G.fspec_end : G.spec_end); ++si) {
       if (P->specs[si].kind == kLPanelInv && !g_inv_launch) continue;
+      if (P->specs[si].kind == kLFinish && g_inv_launch && !fu) continue;  // folded into the last inverse launch
       f(P->specs[si].kind, P->specs[si].step, P->specs[si].group, P->specs[si].task_count);
     }
   }
