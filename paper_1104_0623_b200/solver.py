@@ -375,13 +375,16 @@ def _prepare(mesh, a_list, sigma, config):
     am0 = _csr_sorted(a_list[0].matrix)
     plan, _ = plan_for(mesh.nx, mesh.ny, am0.indptr, am0.indices, config.leaf_max)
     _validate(mesh, a_list[0], sigma, config, plan.cache)
+    import torch
+
     vals = plan.host_values(len(a_list))
+    vt = plan.pinned_tensor(vals)  # the same pinned buffer as a tensor: multi-threaded copies
     for k, a in enumerate(a_list):
         am = am0 if k == 0 else _csr_sorted(a.matrix)
         if am.nnz != am0.nnz or not (am.indptr is am0.indptr or np.array_equal(am.indptr, am0.indptr)) or not (
                 am.indices is am0.indices or np.array_equal(am.indices, am0.indices)):
             raise ValueError("all operators of a batch must share one sparsity pattern")
-        vals[k] = am.data
+        vt[k].copy_(torch.from_numpy(np.ascontiguousarray(am.data)))
     s_vals, ssym, sherm = (None, 0, False)
     if config.compute_gless:
         s_vals, ssym, sherm = _sigma_prepare(plan, am0, sigma)
