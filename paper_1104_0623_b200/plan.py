@@ -73,6 +73,9 @@ class Plan:
         self.cache: dict = {}  # per-pattern host-side caches (validation, maps, ledgers)
         self._pin_in = None
         self._pin_out = None
+        self._dev_bufs: dict = {}  # persistent device buffers of solve_values (graph-stable pointers)
+        self._graphs: dict = {}    # captured CUDA graphs of the level schedule, per (groups, shapes, pointers)
+        self._graph_seen: dict = {}
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -200,12 +203,60 @@ class Plan:
         with self._lock:
             if self._ws is None or self._ws.numel() < need or self._ws.device != device:
                 self._ws = None
+                self._graphs.clear()  # captured graphs point into the old workspace
+                self._graph_seen.clear()
                 try:
                     self._ws = torch.empty(need, dtype=torch.uint8, device=device)
                 except torch.OutOfMemoryError:
                     release_workspaces(keep=self)  # workspaces cached by other plans
                     self._ws = torch.empty(need, dtype=torch.uint8, device=device)
             return self._ws
+
+    def solve_stream(self, device):
+        """A non-default CUDA stream owned by the plan (graph capture needs one)."""
+        import torch
+
+        st = self.cache.get(("stream", str(device)))
+        if st is None:
+            st = torch.cuda.Stream(device)
+            self.cache[("stream", str(device))] = st
+        return st
+
+    def device_buffer(self, name: str, shape: tuple, device):
+        """A persistent complex128 device tensor owned by the plan (stable address for graph replay)."""
+        import torch
+
+        key = (name, tuple(shape), str(device))
+        t = self._dev_bufs.get(key)
+        if t is None:
+            t = torch.empty(shape, dtype=torch.complex128, device=device)
+            self._dev_bufs[key] = t
+        return t
+
+    def replay_or_run(self, key, stream, fn):
+        """Run fn() (stream-ordered work on `stream` into fixed buffers) eagerly the first time a
+        key is seen; the second time capture it into a CUDA graph; afterwards replay the graph:
+        one launch instead of ~2000 host-side kernel launches per solve.  FIND_B200_GRAPH=0 off."""
+        import os
+
+        import torch
+
+        if os.environ.get("FIND_B200_GRAPH", "1") == "0":
+            return fn()
+        g = self._graphs.get(key)
+        if g is not None:
+            g.replay()
+            return None
+        n = self._graph_seen.get(key, 0) + 1
+        self._graph_seen[key] = n
+        if n < 2:
+            return fn()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        self._graphs[key] = g
+        g.replay()
+        return None
 
     def run(self, a_dev, s_dev, gr_dev, gl_dev, compute_gless=True, pivot_rtol=1e-12, s_broadcast=True, ws=None,
             stream=None, groups=(0, -1), check=True, sigma_sym=0, off_gr=None, off_gl=None):
@@ -271,6 +322,9 @@ def release_workspaces(keep: "Plan | None" = None) -> None:
     for p in plans:
         if p is not keep:
             p._ws = None
+            p._graphs.clear()
+            p._graph_seen.clear()
+            p._dev_bufs.clear()
     if torch.cuda.is_available():
         torch.cuda.empty_cache()
 

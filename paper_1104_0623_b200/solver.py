@@ -228,53 +228,68 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
     chunk = max(1, min(n_e, int((0.85 * (free + held) - plan.workspace_bytes(1, compute_gless) + per_energy) // per_energy)))
     if max_chunk:
         chunk = min(chunk, max_chunk)
-    stream = torch.cuda.current_stream(dev)
+    # the plan's own (non-default) stream, ordered after the caller's current stream; every chunk
+    # ends with a host synchronisation, so the caller's stream needs no wait afterwards
+    stream = plan.solve_stream(dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))
     gr = np.empty((n_e, plan.n), np.complex128)
     gl = np.empty((n_e, plan.n), np.complex128) if compute_gless else None
-    s_all = torch.from_numpy(s_vals).to(dev, non_blocking=True) if (compute_gless and s_b) else None
+    s_all = torch.from_numpy(s_vals) if (compute_gless and s_b) else None
     a_host = plan.pinned_tensor(a_vals) if plan.is_pinned_view(a_vals) else torch.from_numpy(a_vals)
     if compute_offdiag:
         offdiag_out["gr"] = np.empty((n_e, n_pairs), np.complex128)
         offdiag_out["gl"] = np.empty((n_e, n_pairs), np.complex128) if compute_gless else None
     t_up = t_down = 0.0
-    for k0 in range(0, n_e, chunk):
-        k1 = min(n_e, k0 + chunk)
-        a_d = a_host[k0:k1].to(dev, non_blocking=True)
-        s_d = s_all if s_b else (torch.from_numpy(s_vals[k0:k1]).to(dev) if compute_gless else None)
-        gr_d = torch.empty((k1 - k0, plan.n), dtype=torch.complex128, device=dev)
-        gl_d = torch.empty((k1 - k0, plan.n), dtype=torch.complex128, device=dev) if compute_gless else None
-        og_d = ol_d = None
-        if compute_offdiag:
-            og_d = torch.empty((k1 - k0, max(n_pairs, 1)), dtype=torch.complex128, device=dev)
-            ol_d = torch.empty_like(og_d) if compute_gless else None
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        ev[0].record(stream)
-        ws = plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, stream=stream,
-                      groups=(0, plan.first_down_group), sigma_sym=sigma_sym)
-        ev[1].record(stream)
-        plan.run(a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, ws=ws, stream=stream,
-                 groups=(plan.first_down_group, -1), sigma_sym=sigma_sym, off_gr=og_d, off_gl=ol_d)
-        ev[2].record(stream)
-        out_h = plan.host_outputs(k1 - k0, compute_gless)
-        out_h[0].copy_(gr_d, non_blocking=True)
-        if compute_gless:
-            out_h[1].copy_(gl_d, non_blocking=True)
-        try:
-            plan.check_status(ws, k1 - k0, stream)
-        except Exception as exc:
-            if hasattr(exc, "energy") and exc.energy is not None:
-                exc.energy += k0
-            raise
-        gr[k0:k1] = out_h[0].numpy()
-        if compute_gless:
-            gl[k0:k1] = out_h[1].numpy()
-        if compute_offdiag:
-            offdiag_out["gr"][k0:k1] = og_d[:, :n_pairs].cpu().numpy()
+    with torch.cuda.stream(stream):  # copies, events and kernels all on the plan's stream
+        for k0 in range(0, n_e, chunk):
+            k1 = min(n_e, k0 + chunk)
+            c = k1 - k0
+            # inputs / outputs in plan-owned device buffers: fixed addresses, so the level schedule
+            # is captured once as a CUDA graph and replayed (Plan.replay_or_run)
+            a_d = plan.device_buffer("a", (c, plan.nnz), dev)
+            a_d.copy_(a_host[k0:k1], non_blocking=True)
+            s_d = None
             if compute_gless:
-                offdiag_out["gl"][k0:k1] = ol_d[:, :n_pairs].cpu().numpy()
-        t_up += ev[0].elapsed_time(ev[1]) * 1e-3
-        t_down += ev[1].elapsed_time(ev[2]) * 1e-3
-        del a_d, gr_d, gl_d
+                s_d = plan.device_buffer("s", (plan.nnz,) if s_b else (c, plan.nnz), dev)
+                s_d.copy_(s_all if s_b else torch.from_numpy(s_vals[k0:k1]), non_blocking=True)
+            gr_d = plan.device_buffer("gr", (c, plan.n), dev)
+            gl_d = plan.device_buffer("gl", (c, plan.n), dev) if compute_gless else None
+            og_d = ol_d = None
+            if compute_offdiag:
+                og_d = plan.device_buffer("og", (c, max(n_pairs, 1)), dev)
+                ol_d = plan.device_buffer("ol", (c, max(n_pairs, 1)), dev) if compute_gless else None
+            ws = plan.workspace(c, compute_gless, dev)
+            key = (c, int(compute_gless), int(s_b), int(sigma_sym), float(pivot_rtol), bool(compute_offdiag),
+                   ws.data_ptr(), stream.cuda_stream)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record(stream)
+            plan.replay_or_run(("up",) + key, stream, lambda: plan.run(
+                a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, ws=ws, stream=stream,
+                groups=(0, plan.first_down_group), sigma_sym=sigma_sym))
+            ev[1].record(stream)
+            plan.replay_or_run(("down",) + key, stream, lambda: plan.run(
+                a_d, s_d, gr_d, gl_d, compute_gless, pivot_rtol, s_b, ws=ws, stream=stream,
+                groups=(plan.first_down_group, -1), sigma_sym=sigma_sym, off_gr=og_d, off_gl=ol_d))
+            ev[2].record(stream)
+            out_h = plan.host_outputs(k1 - k0, compute_gless)
+            out_h[0].copy_(gr_d, non_blocking=True)
+            if compute_gless:
+                out_h[1].copy_(gl_d, non_blocking=True)
+            try:
+                plan.check_status(ws, k1 - k0, stream)
+            except Exception as exc:
+                if hasattr(exc, "energy") and exc.energy is not None:
+                    exc.energy += k0
+                raise
+            gr[k0:k1] = out_h[0].numpy()
+            if compute_gless:
+                gl[k0:k1] = out_h[1].numpy()
+            if compute_offdiag:
+                offdiag_out["gr"][k0:k1] = og_d[:, :n_pairs].cpu().numpy()
+                if compute_gless:
+                    offdiag_out["gl"][k0:k1] = ol_d[:, :n_pairs].cpu().numpy()
+            t_up += ev[0].elapsed_time(ev[1]) * 1e-3
+            t_down += ev[1].elapsed_time(ev[2]) * 1e-3
     return gr, gl, t_up, t_down
 
 

@@ -352,3 +352,32 @@ def test_non_finite_values_do_not_fault(cuda):
             pass
         ok = solve(Mesh(p.nx, p.ny), SparseOperator(p.a_csr(0)), SparseOperator(p.sigma_csr()), SolverConfig())
         assert np.all(np.isfinite(ok.gr_diag))
+
+
+def test_graph_replay_matches_eager(cuda):
+    """solve_values captures the level schedule as a CUDA graph on the second call with the same
+    shapes and replays it afterwards: identical results to the eager run, new values honoured."""
+    from paper_1104_0623_b200.configs import build_problem
+    from paper_1104_0623_b200.plan import plan_for
+    from paper_1104_0623_b200.solver import sigma_symmetry, solve_values
+
+    p = build_problem(70, 30, [0.8, 1.9, 3.1], seed=21, stencil=5)
+    q = build_problem(70, 30, [1.2, 2.2, 2.9], seed=21, stencil=5)
+    plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
+    sym = sigma_symmetry(p.sigma_csr())
+    plan._graphs.clear()
+    plan._graph_seen.clear()
+    r1 = solve_values(plan, p.a_vals_all(), p.s_vals, sigma_sym=sym)  # eager
+    r2 = solve_values(plan, p.a_vals_all(), p.s_vals, sigma_sym=sym)  # captured + replayed
+    r3 = solve_values(plan, q.a_vals_all(), q.s_vals, sigma_sym=sym)  # replayed, other energies
+    assert len(plan._graphs) == 2
+    assert np.array_equal(r1[0], r2[0]) and np.array_equal(r1[1], r2[1])
+    import os
+
+    os.environ["FIND_B200_GRAPH"] = "0"
+    try:
+        r4 = solve_values(plan, q.a_vals_all(), q.s_vals, sigma_sym=sym)  # eager again
+    finally:
+        os.environ.pop("FIND_B200_GRAPH")
+    assert np.array_equal(r3[0], r4[0]) and np.array_equal(r3[1], r4[1])
+    assert not np.array_equal(r3[0], r1[0])

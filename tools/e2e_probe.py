@@ -1,0 +1,29 @@
+import sys, time
+sys.path.insert(0, '/root/repo')
+import numpy as np, torch
+from paper_1104_0623_b200 import Mesh, SolverConfig, SparseOperator, solve_batch
+from paper_1104_0623_b200 import solver as S
+from paper_1104_0623_b200.configs import config_problem
+p = config_problem(1)
+mesh = Mesh(p.nx, p.ny)
+ops = [SparseOperator(p.a_csr(k)) for k in range(16)]
+sig = SparseOperator(p.sigma_csr())
+conf = SolverConfig()
+orig = S.solve_values
+tm = {}
+def timed(name, f):
+    def g(*a, **k):
+        t = time.perf_counter(); r = f(*a, **k); tm.setdefault(name, []).append(time.perf_counter() - t); return r
+    return g
+S.solve_values = timed("solve_values", S.solve_values)
+S._prepare = timed("prepare", S._prepare)
+S._stats = timed("stats", S._stats)
+pl = None
+for i in range(12):
+    t = time.perf_counter()
+    r = solve_batch(mesh, ops, sig, conf)
+    tm.setdefault("call", []).append(time.perf_counter() - t)
+    tm.setdefault("device", []).append(r.timings["upward"] + r.timings["downward_extract"])
+for k, v in tm.items():
+    v = np.array(v[2:]) * 1e3
+    print(f"{k:14s} median {np.median(v):7.2f} ms  min {v.min():7.2f}  max {v.max():7.2f}")
