@@ -106,7 +106,8 @@ void find_assign_phases(find_plan* P) {
 }
 
 // Flattened task lists of every phase launch (see LaunchKind).
-// X solve with 16-row tiles for groups with fewer than 148 row tiles of 64 (FIND_B200_XS16=0 disables).
+// X solve with 16-row tiles for large-S groups with fewer than 148 row tiles of 64 (long, narrow
+// chains: cfg2-4 near the root); FIND_B200_XS16=0 disables.
 bool xsolve16_enabled() {
   const char* f = std::getenv("FIND_B200_XS16");
   return !(f && f[0] == '0');
@@ -221,7 +222,7 @@ void find_build_tasks(find_plan* P) {
       int64_t tiles = 0;  // few 64-row tiles (large-S groups): 16-row tiles, 4x the parallelism
       for (int64_t e = G.begin; e < G.end; ++e)
         if (P->elims[e].s > 0) tiles += (P->elims[e].b + kTile - 1) / kTile;
-      const int rows = (nb == 32 && tiles < 148 && xsolve16_enabled()) ? 16 : kTile;
+      const int rows = (nb == 32 && tiles < 148 && G.max_s > 288 && xsolve16_enabled()) ? 16 : kTile;
       for (int64_t e = G.begin; e < G.end; ++e) {
         const ElimDesc& d = P->elims[e];
         if (d.s == 0 || d.b == 0) continue;
