@@ -88,6 +88,13 @@ __device__ __forceinline__ double2 cinv(double2 a) {  // Smith's algorithm
   return make_double2(r / d, -1.0 / d);
 }
 
+// epilogue operand prefetch in the DMMA tiles (compile with -DFIND_NO_PREFETCH_C to drop)
+#ifdef FIND_NO_PREFETCH_C
+constexpr bool g_prefetch_c = false;
+#else
+constexpr bool g_prefetch_c = true;
+#endif
+
 // ------------------------------------------------------------------ params
 struct SolveParams {
   const ElimDesc* elims;
@@ -758,6 +765,22 @@ struct Tile {
       }
       __syncthreads();
     }
+  }
+
+  // L2 -> L1 prefetch of this thread's epilogue elements of C[Mv x Nv] (row stride ld), issued
+  // before the K loop so the read-modify-write epilogue does not wait on them
+  __device__ __forceinline__ void prefetch_c(const double2* C, int64_t ld, int Mv, int Nv) const {
+    if (!g_prefetch_c) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp % WM, wn = warp / WM;
+    const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int r = wm * MT * 8 + mt * 8 + fr, c = wn * NT * 8 + nt * 8 + 2 * fc;
+        if (r < Mv && c < Nv) asm volatile("prefetch.global.L1 [%0];" ::"l"(C + (int64_t)r * ld + c));
+      }
   }
 
   template <class F>
@@ -1839,6 +1862,7 @@ __device__ void trail_body(const SolveParams& P, const Task& t, int e, int j, in
   if (P.zskip && d.zsplit && j1 <= (d.zsplit & 0xffff) && r0 >= s + (d.zsplit >> 16)) return;
   Tile64 T;
   T.zero();
+  T.prefetch_c(M + (int64_t)r0 * n + c0, n, min(kTile, n - r0), min(cw, n - c0));
   T.mma(M + (int64_t)r0 * n + j0, n, M + (int64_t)j0 * n + c0, n, min(kTile, n - r0), min(cw, n - c0), jb, smem);
   T.for_each([&](int r, int c, double2 v) {
     if (r0 + r < n && c < cw && c0 + c < n && (r0 + r < s || c0 + c < s)) {
@@ -1866,6 +1890,7 @@ __device__ void schur_body(const SolveParams& P, const Task& t, int e, double2* 
   const int k0 = (P.zskip && d.zsplit && i0 >= (d.zsplit >> 16)) ? ((d.zsplit & 0xffff) / kKC) * kKC : 0;
   Tile64 T;
   T.zero();
+  T.prefetch_c(M + (int64_t)(s + i0) * n + s + c0, n, min(kTile, b - i0), min(kTile, b - c0));
   T.mma(M + (int64_t)(s + i0) * n + k0, n, M + (int64_t)k0 * n + s + c0, n, min(kTile, b - i0), min(kTile, b - c0),
         s - k0, smem);
   const bool store = d.kind != kFinal && d.out_arena >= 0;
@@ -1900,6 +1925,7 @@ __device__ void xsolve_tile(const Scr& S, int n, int s, int j, int r0, double2* 
   {
     TT T;
     T.zero();
+    T.prefetch_c(M + (int64_t)(s + r0) * n + j0, n, nr, jb);
     if (s > j1) T.mma(S.X + (int64_t)r0 * s + j1, s, M + (int64_t)j1 * n + j0, n, nr, jb, s - j1, smem);
     T.for_each([&](int r, int c, double2 v) {
       if (r < nr && c < jb) S.X[(int64_t)(r0 + r) * s + j0 + c] = csub(M[(int64_t)(s + r0 + r) * n + j0 + c], v);
@@ -2085,6 +2111,7 @@ __device__ void tgemm_body(const SolveParams& P, const Task& t, int e, int nb, d
   const int i0 = t.a * kTile, c0 = t.b * kTile;
   Tile64 T;
   T.zero();
+  T.prefetch_c(S.MS + (int64_t)(s + i0) * n + c0, n, min(kTile, b - i0), min(kTile, s - c0));
   const Scr SX = scratch_of(P, d, e, nb);
   T.mma(SX.X + (int64_t)i0 * s, s, S.MS + c0, n, min(kTile, b - i0), min(kTile, s - c0), s, smem);
   T.for_each([&](int r, int c, double2 v) {
@@ -2114,6 +2141,7 @@ __device__ void rgemm_body(const SolveParams& P, const Task& t, int e, int nb, d
   const int mv = min(kTile, b - i0), nv = min(kTile, b - c0);
   Tile64 T;
   T.zero();
+  T.prefetch_c(S.MS + (int64_t)(s + i0) * n + s + c0, n, mv, nv);
   const Scr SX = scratch_of(P, d, e, nb);
   T.mma<false>(SX.X + (int64_t)i0 * s, s, S.MS + s + c0, n, mv, nv, s, smem);          // X Sigma'_SB
   T.mma<true>(S.MS + (int64_t)(s + i0) * n, n, SX.X + (int64_t)c0 * s, s, mv, nv, s, smem);  // T_S X^H
