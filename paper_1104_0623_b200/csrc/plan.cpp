@@ -566,8 +566,73 @@ struct Builder {
       for (int32_t i : by_level[L]) { down_off[i] = a; a += 2 * (int64_t)C[i].CB.size() * C[i].CB.size(); }
       down_max = std::max(down_max, a);
     }
+    // Memory-bounded downward pass: when one level's complement blocks
+    // exceed kSplitDownElems per energy, levels >= K run subtree by subtree (one level-K cluster
+    // and its descendants at a time, the down arenas reused per subtree); the complements of
+    // level K-1 stay in the third arena for all subtrees.  More energy points then fit at once.
+    int32_t split = 0;
+    if (!P->dag) {
+      const char* f = std::getenv("FIND_B200_SPLIT_K");
+      if (f) split = std::max(0, std::min(std::atoi(f), D));
+      else if (down_max > kSplitDownElems)
+        for (split = 1; split < std::min<int32_t>(D, 6); ++split) {
+          int64_t mx = 0;  // largest (subtree, level) block set with this split
+          for (int32_t r : by_level[split]) {
+            std::vector<int32_t> cur{r};
+            while (!cur.empty()) {
+              int64_t a = 0;
+              std::vector<int32_t> nxt;
+              for (int32_t i : cur) {
+                a += 2 * (int64_t)C[i].CB.size() * C[i].CB.size();
+                if (!C[i].leaf()) { nxt.push_back(C[i].child0); nxt.push_back(C[i].child1); }
+              }
+              mx = std::max(mx, a);
+              cur.swap(nxt);
+            }
+          }
+          if (mx <= kSplitDownElems) break;
+        }
+    }
+    P->split_level = split;
+    std::vector<int32_t> sub_of(C.size(), -1);  // subtree (level-K ancestor index) of clusters at level >= K
+    if (split > 0) {
+      for (int32_t r : by_level[split]) {
+        std::vector<int32_t> st{r};
+        while (!st.empty()) {
+          const int32_t i = st.back();
+          st.pop_back();
+          sub_of[i] = r;
+          if (!C[i].leaf()) { st.push_back(C[i].child0); st.push_back(C[i].child1); }
+        }
+      }
+      down_max = 0;
+      for (int32_t L = split; L <= D; ++L) {
+        std::map<int32_t, int64_t> a;  // per subtree
+        for (int32_t i : by_level[L]) {
+          int64_t& x = a[sub_of[i]];
+          down_off[i] = x;
+          x += 2 * (int64_t)C[i].CB.size() * C[i].CB.size();
+          down_max = std::max(down_max, x);
+        }
+      }
+      int64_t top = 0;
+      for (int32_t L = 1; L < split; ++L) {
+        int64_t a = 0;
+        for (int32_t i : by_level[L]) {
+          if (L == split - 1) down_off[i] = a;
+          a += 2 * (int64_t)C[i].CB.size() * C[i].CB.size();
+        }
+        if (L == split - 1) top = a;
+        else down_max = std::max(down_max, a);
+      }
+      for (int32_t L = 1; L < split - 1; ++L) {  // levels above K-1: ping-pong as usual
+        int64_t a = 0;
+        for (int32_t i : by_level[L]) { down_off[i] = a; a += 2 * (int64_t)C[i].CB.size() * C[i].CB.size(); }
+      }
+      P->arena_elems[kArenaDown2] = top;
+    }
     P->arena_elems[kArenaDown0] = P->arena_elems[kArenaDown1] = down_max;
-    P->arena_elems[kArenaDown2] = P->dag ? down_max : 0;
+    if (split == 0) P->arena_elems[kArenaDown2] = P->dag ? down_max : 0;
     const std::vector<int64_t> empty;
 
     auto emit_groups = [&](int64_t begin, int32_t pass, int32_t level) {
@@ -677,14 +742,18 @@ struct Builder {
       if ((int64_t)P->elims.size() > begin) P->n_levels_up++;
       emit_groups(begin, 0, L);
     }
-    // ---- downward pass (solver.py:311-375) level by level, finals right after ----
-    for (int32_t L = 1; L <= D; ++L) {
+    // ---- downward pass (solver.py:311-375) level by level, finals right after; with a split,
+    // levels >= K subtree by subtree ----
+    auto arena_of = [&](int32_t L) -> int32_t {
+      if (split > 0 && L == split - 1) return kArenaDown2;  // kept for every subtree
+      const int32_t rot = P->dag ? 3 : 2;  // ping-pong by level parity; three when phases may overlap
+      return kArenaDown0 + L % rot;
+    };
+    auto down_level = [&](int32_t L, const std::vector<int32_t>& clusters) {
       int64_t begin = (int64_t)P->elims.size();
-      // ping-pong by level parity; three rotating arenas when consecutive phases may overlap
-      const int32_t rot = P->dag ? 3 : 2;
-      int32_t arena = kArenaDown0 + L % rot;
-      int32_t parena = kArenaDown0 + (L - 1) % rot;
-      for (int32_t i : by_level[L]) {
+      int32_t arena = arena_of(L);
+      int32_t parena = arena_of(L - 1);
+      for (int32_t i : clusters) {
         const Cluster& c = C[i];
         const Cluster& par = C[c.parent];
         int32_t sib = par.child0 == i ? par.child1 : par.child0;
@@ -695,7 +764,7 @@ struct Builder {
       if ((int64_t)P->elims.size() > begin) P->n_levels_down++;
       emit_groups(begin, 1, L);
       begin = (int64_t)P->elims.size();
-      for (int32_t i : by_level[L]) {
+      for (int32_t i : clusters) {
         const Cluster& c = C[i];
         if (!c.leaf()) continue;
         std::vector<int64_t> nodes;
@@ -705,7 +774,16 @@ struct Builder {
                  &nodes, false);
       }
       emit_groups(begin, 2, L);
-    }
+    };
+    for (int32_t L = 1; L <= D && (split == 0 || L < split); ++L) down_level(L, by_level[L]);
+    if (split > 0)
+      for (int32_t r : by_level[split])
+        for (int32_t L = split; L <= D; ++L) {
+          std::vector<int32_t> cl;
+          for (int32_t i : by_level[L])
+            if (sub_of[i] == r) cl.push_back(i);
+          if (!cl.empty()) down_level(L, cl);
+        }
     if (C[0].leaf()) {  // single-cluster mesh: only the final step of the root
       int64_t begin = (int64_t)P->elims.size();
       const Cluster& c = C[0];

@@ -84,6 +84,7 @@ inline int pick_nb_host(int64_t max_s) {
   return 0;
 }
 constexpr int kTile = 64;       // DMMA output tile edge
+constexpr int64_t kSplitDownElems = int64_t(1) << 29;  // complex elements (8 GiB) of one level's complement blocks
 constexpr int64_t kGroupScratchCap = int64_t(1) << 28;  // complex elements of CTA-path scratch per energy per phase (4 GiB)
 constexpr int kRowChunk = 16;   // gather rows per CTA
 
@@ -145,6 +146,7 @@ struct find_plan {
   // overlap; three rotating down arenas and two scratch halves (phase parity); per group the
   // groups producing its input blocks
   bool dag = false;
+  int32_t split_level = 0;  // > 0: downward levels >= split_level run subtree by subtree
   std::vector<std::vector<int32_t>> group_deps;
   int64_t ws_elems = 0;
   int32_t max_n = 0, max_s = 0, max_b = 0, depth = 0, n_leaves = 0;

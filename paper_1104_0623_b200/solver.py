@@ -228,6 +228,7 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
     chunk = max(1, min(n_e, int((0.85 * (free + held) - plan.workspace_bytes(1, compute_gless) + per_energy) // per_energy)))
     if max_chunk:
         chunk = min(chunk, max_chunk)
+    chunk = -(-n_e // -(-n_e // chunk))  # balanced chunks (8 points at <= 7 per chunk -> 4 + 4)
     # the plan's own (non-default) stream, ordered after the caller's current stream; every chunk
     # ends with a host synchronisation, so the caller's stream needs no wait afterwards
     stream = plan.solve_stream(dev)

@@ -42,7 +42,8 @@ print("RESULT", json.dumps(out))
                                  {"FIND_B200_FUSED": "0", "FIND_B200_SMEM_PANEL": "1"},
                                  {"FIND_B200_PANEL": "reg"}, {"FIND_B200_PANEL": "warp"},
                                  {"FIND_B200_DAG_MAX_N": "100000"}, {"FIND_B200_WIDE_MIN_S": "0"},
-                                 {"FIND_B200_INV_LAUNCH": "0"}, {"FIND_B200_STRUCT": "0"}])
+                                 {"FIND_B200_INV_LAUNCH": "0"}, {"FIND_B200_STRUCT": "0"},
+                                 {"FIND_B200_SPLIT_K": "1"}, {"FIND_B200_SPLIT_K": "3"}])
 def test_cta_path_variants_match_golden(cuda, env):
     code = SCRIPT.format(root=str(ROOT), tests=str(ROOT / "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
