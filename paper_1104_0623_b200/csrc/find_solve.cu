@@ -1492,7 +1492,7 @@ __global__ void __launch_bounds__(kThreads) panel_smem_kernel(SolveParams P, con
 constexpr int kClusterMax = 8;
 constexpr int kClusterRows = 384;  // rows per CTA: 384 * 33 * 16 B = 198 KB
 __host__ __device__ constexpr size_t cluster_panel_smem() {
-  return ((size_t)kClusterRows * 33 + 2 * 33) * sizeof(double2);
+  return ((size_t)kClusterRows * 33 + 2 * kClusterMax * 33 + 2 * 33) * sizeof(double2);
 }
 
 __global__ void __launch_bounds__(kThreads) panel_cluster_kernel(SolveParams P, const Task* tasks) {
@@ -1503,15 +1503,17 @@ __global__ void __launch_bounds__(kThreads) panel_cluster_kernel(SolveParams P, 
   const int rank = (int)cluster.block_rank();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* panel = reinterpret_cast<double2*>(smem_raw);  // [chunk][PS]
-  double2* prow = panel + (size_t)kClusterRows * PS;       // pivot row (+ 1/u in [NB])
-  double2* srow = prow + PS;                               // row jj, sent to the pivot row's owner
+  // per column parity: every CTA's candidate row [kClusterMax][PS] (+ its |.| and row index) and
+  // the current row jj, posted by their owners to every CTA of the cluster
+  double2* crow = panel + (size_t)kClusterRows * PS;       // [2][kClusterMax][PS]
+  double2* jrow = crow + 2 * kClusterMax * PS;             // [2][PS]
   __shared__ double cand_v[2][kClusterMax];
   __shared__ int cand_i[2][kClusterMax];
   __shared__ double wv[kThreads / 32];
   __shared__ int wi[kThreads / 32];
   __shared__ int lpiv[NB], dsrc[2 * NB], ddst[2 * NB];
   __shared__ int s_bad, s_nd;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const Task t = tasks[blockIdx.x / CS];
   const int e = blockIdx.y;
   const ElimDesc d = P.elims[t.e];
@@ -1536,14 +1538,14 @@ __global__ void __launch_bounds__(kThreads) panel_cluster_kernel(SolveParams P, 
         *S.scale = scale;
         if (scale == 0.0) s_bad = 0;
       }
-    } else {
-      scale = *reinterpret_cast<volatile double*>(S.scale);
     }
   }
   cluster.sync();
+  scale = *reinterpret_cast<volatile double*>(S.scale);
+  // One cluster barrier per column: before it every CTA posts its best candidate's whole row and
+  // the owner of row jj posts row jj; after it all pick the same winner from their own copies.
   for (int jj = 0; jj < jb; ++jj) {
     const int buf = jj & 1;
-    // local candidate
     double v = -1.0;
     int vi = INT32_MAX;
     for (int r = max(jj - r_lo, 0) + tid; r < nloc; r += kThreads) {
@@ -1551,47 +1553,43 @@ __global__ void __launch_bounds__(kThreads) panel_cluster_kernel(SolveParams P, 
       if (a > v) { v = a; vi = r_lo + r; }
     }
     block_argmax<kThreads>(v, vi, wv, wi);
-    if (tid < CS) {  // post to every CTA of the cluster
-      double* rv = cluster.map_shared_rank(&cand_v[buf][rank], tid);
-      int* ri = cluster.map_shared_rank(&cand_i[buf][rank], tid);
-      *rv = v;
-      *ri = vi;
+    const bool have = vi >= r_lo && vi < r_hi;
+    for (int q = tid; q < CS * (NB + 2); q += kThreads) {  // candidate (value, index, row) to every CTA
+      const int dst = q / (NB + 2), c = q % (NB + 2);
+      if (c == NB) {
+        *cluster.map_shared_rank(&cand_v[buf][rank], dst) = have ? v : -1.0;
+        *cluster.map_shared_rank(&cand_i[buf][rank], dst) = have ? vi : INT32_MAX;
+      } else if (c < NB && have) {
+        cluster.map_shared_rank(crow, dst)[(buf * kClusterMax + rank) * PS + c] = panel[(vi - r_lo) * PS + c];
+      }
     }
+    if (jj >= r_lo && jj < r_hi)  // row jj (current diagonal position) to every CTA
+      for (int q = tid; q < CS * NB; q += kThreads) {
+        const int dst = q / NB, c = q % NB;
+        cluster.map_shared_rank(jrow, dst)[buf * PS + c] = panel[(jj - r_lo) * PS + c];
+      }
     cluster.sync();
     double bv = -1.0;
-    int pr = INT32_MAX;
+    int pr = INT32_MAX, pk = 0;
     for (int k = 0; k < CS; ++k) {
       const double ov = cand_v[buf][k];
       const int oi = cand_i[buf][k];
-      if (ov > bv || (ov == bv && oi < pr)) { bv = ov; pr = oi; }
+      if (ov > bv || (ov == bv && oi < pr)) { bv = ov; pr = oi; pk = k; }
     }
-    if (pr < jj || pr >= R) pr = jj;  // NaN / Inf entries: no interchange
-    const int own_pr = pr / chunk, own_jj = jj / chunk;
-    if (rank == own_pr) {  // broadcast the pivot row and 1/u
-      const double2* src = panel + (pr - r_lo) * PS;
-      for (int q = tid; q < CS * (NB + 1); q += kThreads) {
-        const int dst = q / (NB + 1), c = q % (NB + 1);
-        double2* pd = cluster.map_shared_rank(prow, dst);
-        pd[c] = c < NB ? src[c] : cinv(src[jj]);
-      }
-      if (tid == 0 && cabs(src[jj]) < P.rtol * *reinterpret_cast<volatile double*>(S.scale))
-        atomicMin(&s_bad, j0 + jj);
+    const double2* prow = crow + (size_t)(buf * kClusterMax + pk) * PS;
+    if (pr < jj || pr >= R) { pr = jj; prow = jrow + buf * PS; }  // NaN / Inf entries: no interchange
+    if (tid == 0) {
+      lpiv[jj] = pr;
+      if (rank == 0 && cabs(prow[jj]) < P.rtol * scale) atomicMin(&s_bad, j0 + jj);
     }
-    if (rank == own_jj && pr != jj) {  // row jj goes to the pivot row's owner
-      const double2* src = panel + (jj - r_lo) * PS;
-      double2* sd = cluster.map_shared_rank(srow, own_pr);
-      for (int c = tid; c < NB; c += kThreads) sd[c] = src[c];
-    }
-    if (tid == 0) lpiv[jj] = pr;
-    cluster.sync();
-    if (pr != jj) {
-      if (rank == own_jj)
+    if (pr != jj) {  // exchange rows jj and pr (each owner rewrites its own copy)
+      if (jj >= r_lo && jj < r_hi)
         for (int c = tid; c < NB; c += kThreads) panel[(jj - r_lo) * PS + c] = prow[c];
-      if (rank == own_pr)
-        for (int c = tid; c < NB; c += kThreads) panel[(pr - r_lo) * PS + c] = srow[c];
+      if (pr >= r_lo && pr < r_hi)
+        for (int c = tid; c < NB; c += kThreads) panel[(pr - r_lo) * PS + c] = jrow[buf * PS + c];
     }
     __syncthreads();
-    const double2 uinv = prow[NB];
+    const double2 uinv = cinv(prow[jj]);
     for (int r = max(jj + 1 - r_lo, 0) + tid; r < nloc; r += kThreads) {
       double2* rw = panel + r * PS;
       const double2 l = cmul(rw[jj], uinv);
