@@ -178,20 +178,6 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def _unused_group_work(plan):
-    """Algorithmic work (paper ledger, complex mults) per launch group, one energy point."""
-    from paper_1104_0623_b200.ledger import plan_ledger
-
-    out = []
-    start = 0
-    for cnt in plan.groups["count"]:
-        sl = slice(start, start + int(cnt))
-        led = plan_ledger(plan.kind[sl], plan.s[sl], plan.b[sl], "naive", True)
-        out.append(float(led.multiplications))
-        start += int(cnt)
-    return np.array(out)
-
-
 def run_b200(args):
     import torch
     import torch.distributed as dist
