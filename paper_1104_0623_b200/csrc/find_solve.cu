@@ -1647,26 +1647,6 @@ struct TrsmTiles<8> { using U = Tile<1, 8, 1, 1, false>; using L = Tile<8, 1, 1,
 template <>
 struct TrsmTiles<4> { using U = Tile<1, 8, 1, 1, false>; using L = Tile<8, 1, 1, 1, false>; };
 
-// ---- pivot permutation sigma (pivoted position -> merged position) and its inverse from
-// the row interchanges PIV (LAPACK order); sig: shared scratch of s ints
-__device__ void finish_sigma(const Scr& S, int s, int* sig) {
-  const int tid = threadIdx.x;
-  for (int k = tid; k < s; k += blockDim.x) sig[k] = k;
-  __syncthreads();
-  if (tid == 0)
-    for (int k = 0; k < s; ++k) {
-      const int pk = S.PIV[k];
-      const int tmp = sig[k];
-      sig[k] = sig[pk];
-      sig[pk] = tmp;
-    }
-  __syncthreads();
-  for (int k = tid; k < s; k += blockDim.x) {
-    S.SIG[k] = sig[k];
-    S.ISG[sig[k]] = k;
-  }
-}
-
 // ---- wide (two-panel) block TRSM for columns [c0, c0+64) right of the block [J0, J0+2NB):
 // both panels' row interchanges in order (PERM2 of panel j-1 at J0, PERM of panel j at
 // J0+NB), then U12 = L_JJ^-1 A12 as top = L1^-1 A_top, A_bot -= L21 top, bot = L2^-1 A_bot.
@@ -1821,11 +1801,20 @@ __global__ void __launch_bounds__(kThreads) panel_inv_kernel(SolveParams P, cons
   Row* Dm = reinterpret_cast<Row*>(smem_raw);
   Row* Xm = Dm + NB;
   Row* Wm = Xm + NB;
+  // sigma (pivoted position -> merged position) kept up to date panel by panel: this panel's
+  // net row interchange PERM applied to SIG[j0:s) exactly as to the rows of M (identity
+  // before panel 0), so the last panel only inverts it -- no serial pass over PIV
+  int* stg = reinterpret_cast<int*>(Wm + 3 * NB);
+  const int nd = S.PERM[0];
+  if (j == 0)
+    for (int k = threadIdx.x; k < s; k += kThreads) S.SIG[k] = k;
+  for (int k = threadIdx.x; k < nd; k += kThreads) stg[k] = j == 0 ? S.PERM[1 + k] : S.SIG[j0 + S.PERM[1 + k]];
   for (int q = threadIdx.x; q < NB * NB; q += kThreads) {
     const int r = q / NB, c = q % NB;
     Dm[r][c] = (r < jb && c < jb) ? S.M[(int64_t)(j0 + r) * n + j0 + c] : cz();
   }
   __syncthreads();
+  for (int k = threadIdx.x; k < nd; k += kThreads) S.SIG[j0 + S.PERM[1 + 2 * NB + k]] = stg[k];
   // L_jj^-1 on threads [0, 128), U_jj^-1 on [128, 256), concurrently (named barriers 1 and 2)
   constexpr int H = kThreads / 2;
   const bool lower = threadIdx.x < H;
@@ -1839,10 +1828,9 @@ __global__ void __launch_bounds__(kThreads) panel_inv_kernel(SolveParams P, cons
     const int r = q / NB, c = q % NB;
     out[q] = (r < jb && c < jb) ? Xh[r][c] : cz();
   }
-  if (j0 + jb == s) {  // last panel: every pivot is known -> sigma and its inverse (the finish step)
-    int* sig = reinterpret_cast<int*>(Wm + 3 * NB);
+  if (j0 + jb == s) {  // last panel: sigma is final -> its inverse (the finish step)
     __syncthreads();
-    finish_sigma(S, s, sig);
+    for (int k = threadIdx.x; k < s; k += kThreads) S.ISG[S.SIG[k]] = k;
   }
 }
 
