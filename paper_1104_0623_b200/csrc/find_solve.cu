@@ -899,40 +899,43 @@ __device__ void block_tri_inverse_t(const double2 (*D)[NB + 1], int jb, double2 
     X[r][c] = r != c ? cz() : ((LOWER || r >= jb) ? make_double2(1.0, 0.0) : cinv(D[r][r]));
   }
   part_sync<NT>(bar_id);
-#pragma unroll 1
+  // Fixed-length inner products: the triangle's structural zeros (X triangular, D zero
+  // outside jb) add exact zeros, so the sums equal the triangular ranges term for term and
+  // every loop has a compile-time trip count (operand loads hoisted out of the FMA chain).
+#pragma unroll
   for (int bs = 1; bs < NB; bs *= 2) {
+#pragma unroll
     for (int q = tid; q < (NB / 2) * bs; q += NT) {
       const int pair = q / (bs * bs), loc = q % (bs * bs);
       const int k = pair * 2 * bs, a = loc / bs, b = loc % bs;
       double2 acc = cz();
       if (LOWER) {  // W[i][j] = sum_q L[i][q] X[q][j], i in B, q and j in A
         const int i = k + bs + a, jc = k + b;
-#pragma unroll 1
-        for (int qq = jc; qq < k + bs; ++qq)
-          if (i < jb && qq < jb) acc = cfma(acc, D[i][qq], X[qq][jc]);
+#pragma unroll
+        for (int qq = k; qq < k + bs; ++qq) acc = cfma(acc, D[i][qq], X[qq][jc]);
         W[i][jc] = acc;
       } else {  // W[i][j] = sum_q X[i][q] U[q][j], i and q in A, j in B
         const int i = k + a, jc = k + bs + b;
-#pragma unroll 1
-        for (int qq = i; qq < k + bs; ++qq)
-          if (qq < jb && jc < jb) acc = cfma(acc, X[i][qq], D[qq][jc]);
+#pragma unroll
+        for (int qq = k; qq < k + bs; ++qq) acc = cfma(acc, X[i][qq], D[qq][jc]);
         W[i][jc] = acc;
       }
     }
     part_sync<NT>(bar_id);
+#pragma unroll
     for (int q = tid; q < (NB / 2) * bs; q += NT) {
       const int pair = q / (bs * bs), loc = q % (bs * bs);
       const int k = pair * 2 * bs, a = loc / bs, b = loc % bs;
       double2 acc = cz();
       if (LOWER) {  // X[i][j] = -sum_p X[i][p] W[p][j], p in B
         const int i = k + bs + a, jc = k + b;
-#pragma unroll 1
-        for (int p = k + bs; p <= i; ++p) acc = cfma(acc, X[i][p], W[p][jc]);
+#pragma unroll
+        for (int p = k + bs; p < k + 2 * bs; ++p) acc = cfma(acc, X[i][p], W[p][jc]);
         X[i][jc] = make_double2(-acc.x, -acc.y);
       } else {  // X[i][j] = -sum_p W[i][p] X[p][j], p in B
         const int i = k + a, jc = k + bs + b;
-#pragma unroll 1
-        for (int p = k + bs; p <= jc; ++p) acc = cfma(acc, W[i][p], X[p][jc]);
+#pragma unroll
+        for (int p = k + bs; p < k + 2 * bs; ++p) acc = cfma(acc, W[i][p], X[p][jc]);
         X[i][jc] = make_double2(-acc.x, -acc.y);
       }
     }

@@ -332,12 +332,29 @@ def release_workspaces(keep: "Plan | None" = None) -> None:
 _LAST: list = []  # (nx, ny, leaf_max, indptr, indices, plan) of the last lookup: memcmp fast path
 
 
+_libc = C.CDLL(None)
+_libc.memcmp.restype = C.c_int
+_libc.memcmp.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+
+
+def same_array(a: np.ndarray, b: np.ndarray) -> bool:
+    """a == b element for element; one memcmp (GIL released) when dtype and layout match."""
+    if a is b:
+        return True
+    a, b = np.asarray(a), np.asarray(b)
+    if a.shape != b.shape:
+        return False
+    if a.dtype == b.dtype and a.flags.c_contiguous and b.flags.c_contiguous and a.dtype.kind in "iub":
+        return a.nbytes == 0 or _libc.memcmp(a.ctypes.data, b.ctypes.data, a.nbytes) == 0
+    return bool(np.array_equal(a, b))
+
+
 def plan_for(nx: int, ny: int, indptr: np.ndarray, indices: np.ndarray, leaf_max: int = 2) -> tuple[Plan, float]:
     """Cached plan for a pattern; returns (plan, seconds spent building it now)."""
     if _LAST:
         lx, ly, ll, lp, li, lplan = _LAST[0]
         if (lx, ly, ll) == (int(nx), int(ny), int(leaf_max)) and lp.size == np.size(indptr) and li.size == np.size(
-                indices) and np.array_equal(lp, indptr) and np.array_equal(li, indices):
+                indices) and same_array(lp, indptr) and same_array(li, indices):
             return lplan, 0.0
     p, t = _plan_for_hashed(nx, ny, indptr, indices, leaf_max)
     _LAST[:] = [(int(nx), int(ny), int(leaf_max), p.indptr, p.indices, p)]

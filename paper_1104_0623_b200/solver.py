@@ -16,7 +16,7 @@ import scipy.sparse as sp
 from .errors import NativeLibraryError
 from .ledger import BLOCK_KERNELS, HERMITIAN_KERNELS, KERNEL_NAMES, FlopLedger
 from .operators import check_pattern_subset, check_structural_symmetry, is_hermitian
-from .plan import Plan, plan_for
+from .plan import Plan, plan_for, same_array
 
 
 @dataclass
@@ -126,7 +126,7 @@ def _sigma_prepare(plan: Plan, am: sp.csr_matrix, sigma) -> tuple[np.ndarray, in
     sm = _csr_sorted(sigma.matrix)
     last = plan.cache.get("sigma_last")
     if (last is not None and last[0].size == sm.indptr.size and last[1].size == sm.indices.size
-            and np.array_equal(last[0], sm.indptr) and np.array_equal(last[1], sm.indices)
+            and same_array(last[0], sm.indptr) and same_array(last[1], sm.indices)
             and np.array_equal(last[2], sm.data)):
         return last[3]
     out = _sigma_prepare_full(plan, sm)
@@ -196,7 +196,8 @@ def _device():
 
 
 def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, compute_gless=True, pivot_rtol=1e-12,
-                 sigma_sym=0, max_chunk: int | None = None, compute_offdiag=False, offdiag_out: dict | None = None):
+                 sigma_sym=0, max_chunk: int | None = None, compute_offdiag=False, offdiag_out: dict | None = None,
+                 host_work=None):
     """Run the plan on host value arrays a_vals [nE, nnz], s_vals [nnz] or [nE, nnz].
 
     Energy points are processed in chunks sized to the free device memory (one
@@ -204,6 +205,7 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
     kernels, status check, device -> host copy of the diagonals.
     With compute_offdiag, G^r (and G^< when compute_gless) on plan.offdiag_pairs() are
     stored into offdiag_out["gr"] / ["gl"] ([nE, n_pairs]).
+    host_work: optional callable run once while the first chunk executes on the device.
     Returns (gr, gl, device_seconds_up, device_seconds_down)."""
     import torch
 
@@ -276,6 +278,8 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
             out_h[0].copy_(gr_d, non_blocking=True)
             if compute_gless:
                 out_h[1].copy_(gl_d, non_blocking=True)
+            if host_work is not None and k0 == 0:
+                host_work()
             try:
                 plan.check_status(ws, k1 - k0, stream)
             except Exception as exc:
@@ -382,6 +386,18 @@ def _offdiag_dict(pairs: np.ndarray, vals: np.ndarray) -> dict:
     return dict(zip(map(tuple, pairs.tolist()), vals.tolist()))
 
 
+_PACK_THREADS = 4
+_POOL = []
+
+
+def _pack_pool():
+    if not _POOL:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _POOL.append(ThreadPoolExecutor(_PACK_THREADS, thread_name_prefix="find-pack"))
+    return _POOL[0]
+
+
 def _prepare(mesh, a_list, sigma, config):
     """Validation (solver.py:591-608), cached plan, values packed into a reused pinned buffer."""
     if not a_list:
@@ -391,16 +407,21 @@ def _prepare(mesh, a_list, sigma, config):
     am0 = _csr_sorted(a_list[0].matrix)
     plan, _ = plan_for(mesh.nx, mesh.ny, am0.indptr, am0.indices, config.leaf_max)
     _validate(mesh, a_list[0], sigma, config, plan.cache)
-    import torch
-
     vals = plan.host_values(len(a_list))
-    vt = plan.pinned_tensor(vals)  # the same pinned buffer as a tensor: multi-threaded copies
-    for k, a in enumerate(a_list):
-        am = am0 if k == 0 else _csr_sorted(a.matrix)
-        if am.nnz != am0.nnz or not (am.indptr is am0.indptr or np.array_equal(am.indptr, am0.indptr)) or not (
-                am.indices is am0.indices or np.array_equal(am.indices, am0.indices)):
-            raise ValueError("all operators of a batch must share one sparsity pattern")
-        vt[k].copy_(torch.from_numpy(np.ascontiguousarray(am.data)))
+    mats = [am0] + [_csr_sorted(a.matrix) for a in a_list[1:]]
+
+    def pack(ks):  # pattern check and value copy of operators ks (memcmp / copyto run without the GIL)
+        for k in ks:
+            am = mats[k]
+            if am.nnz != am0.nnz or not same_array(am.indptr, am0.indptr) or not same_array(am.indices, am0.indices):
+                return False
+            np.copyto(vals[k], am.data, casting="same_kind")
+        return True
+
+    parts = [range(k, len(mats), _PACK_THREADS) for k in range(min(_PACK_THREADS, len(mats)))]
+    ok = all(_pack_pool().map(pack, parts)) if len(parts) > 1 else pack(parts[0])
+    if not ok:
+        raise ValueError("all operators of a batch must share one sparsity pattern")
     s_vals, ssym, sherm = (None, 0, False)
     if config.compute_gless:
         s_vals, ssym, sherm = _sigma_prepare(plan, am0, sigma)
@@ -415,8 +436,10 @@ def solve(mesh, a, sigma, config: SolverConfig) -> SelectedInverse:
     plan, am, vals, s_vals, ssym, sherm = _prepare(mesh, [a], sigma, config)
     t1 = time.perf_counter()
     off = {}
+    side = {}
     gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol, ssym,
-                                        compute_offdiag=config.compute_offdiag, offdiag_out=off)
+                                        compute_offdiag=config.compute_offdiag, offdiag_out=off,
+                                        host_work=lambda: side.update(stats=_stats(plan, am.data)))
     led = _ledger_cached(plan, config, sherm)
     offd = offl = None
     if config.compute_offdiag:
@@ -431,7 +454,7 @@ def solve(mesh, a, sigma, config: SolverConfig) -> SelectedInverse:
         offdiag=offd,
         ledger=led,
         timings={"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},
-        stats=_stats(plan, am.data),
+        stats=side["stats"],
         offdiag_gless=offl,
     )
 
@@ -443,12 +466,15 @@ def solve_batch(mesh, a_list, sigma, config: SolverConfig) -> SelectedInverseBat
     plan, am0, vals, s_vals, ssym, sherm = _prepare(mesh, list(a_list), sigma, config)
     t1 = time.perf_counter()
     off = {}
+    side = {}
     gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol, ssym,
-                                        compute_offdiag=config.compute_offdiag, offdiag_out=off)
+                                        compute_offdiag=config.compute_offdiag, offdiag_out=off,
+                                        host_work=lambda: side.update(stats=_stats(plan, am0.data),
+                                                                      ledger=_ledger_cached(plan, config, sherm)))
     t3 = time.perf_counter()
-    res = SelectedInverseBatch(gr, gl, _ledger_cached(plan, config, sherm),
+    res = SelectedInverseBatch(gr, gl, side["ledger"],
                                {"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},
-                               _stats(plan, am0.data))
+                               side["stats"])
     if config.compute_offdiag:
         res.offdiag_pairs = plan.offdiag_pairs()
         res.offdiag_gr = off["gr"]

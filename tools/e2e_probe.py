@@ -27,3 +27,11 @@ for i in range(12):
 for k, v in tm.items():
     v = np.array(v[2:]) * 1e3
     print(f"{k:14s} median {np.median(v):7.2f} ms  min {v.min():7.2f}  max {v.max():7.2f}")
+if "--profile" in sys.argv:
+    import cProfile, pstats
+    pr = cProfile.Profile()
+    pr.enable()
+    for i in range(10):
+        solve_batch(mesh, ops, sig, conf)
+    pr.disable()
+    pstats.Stats(pr).sort_stats(sys.argv[-1] if sys.argv[-1] in ("cumulative", "tottime") else "tottime").print_stats(30)
