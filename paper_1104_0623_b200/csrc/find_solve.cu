@@ -88,12 +88,6 @@ __device__ __forceinline__ double2 cinv(double2 a) {  // Smith's algorithm
   return make_double2(r / d, -1.0 / d);
 }
 
-// epilogue operand prefetch in the DMMA tiles (compile with -DFIND_NO_PREFETCH_C to drop)
-#ifdef FIND_NO_PREFETCH_C
-constexpr bool g_prefetch_c = false;
-#else
-constexpr bool g_prefetch_c = true;
-#endif
 
 // ------------------------------------------------------------------ params
 struct SolveParams {
@@ -714,7 +708,8 @@ struct Tile {
     cp_async_commit();
   }
 
-  template <bool BT2 = BT>
+  // acc += A op(B), or acc -= A op(B) with NEG (acc seeded by load_c: C - A op(B) tiles)
+  template <bool BT2 = BT, bool NEG = false>
   __device__ __forceinline__ void mma(const double2* A, int64_t lda, const double2* B, int64_t ldb, int Mv, int Nv,
                                       int K, double2* smem) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -752,14 +747,14 @@ struct Tile {
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           if (mt >= mtv) break;
-          const double nai = -a[mt].y;
+          const double ax = NEG ? -a[mt].x : a[mt].x, ay = NEG ? -a[mt].y : a[mt].y, nai = -ay;
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             if (nt >= ntv) break;
-            dmma(acc[mt][nt][0][0], acc[mt][nt][0][1], a[mt].x, b[nt].x);
+            dmma(acc[mt][nt][0][0], acc[mt][nt][0][1], ax, b[nt].x);
             dmma(acc[mt][nt][0][0], acc[mt][nt][0][1], nai, b[nt].y);
-            dmma(acc[mt][nt][1][0], acc[mt][nt][1][1], a[mt].x, b[nt].y);
-            dmma(acc[mt][nt][1][0], acc[mt][nt][1][1], a[mt].y, b[nt].x);
+            dmma(acc[mt][nt][1][0], acc[mt][nt][1][1], ax, b[nt].y);
+            dmma(acc[mt][nt][1][0], acc[mt][nt][1][1], ay, b[nt].x);
           }
         }
       }
@@ -767,20 +762,23 @@ struct Tile {
     }
   }
 
-  // L2 -> L1 prefetch of this thread's epilogue elements of C[Mv x Nv] (row stride ld), issued
-  // before the K loop so the read-modify-write epilogue does not wait on them
-  __device__ __forceinline__ void prefetch_c(const double2* C, int64_t ld, int Mv, int Nv) const {
-    if (!g_prefetch_c) return;
+  // acc = this thread's elements of C[Mv x Nv] (row stride ld; zero outside), loaded before the
+  // K loop so the C - A op(B) epilogue only stores (the loads overlap the operand staging)
+  __device__ __forceinline__ void load_c(const double2* C, int64_t ld, int Mv, int Nv) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = warp % WM, wn = warp / WM;
     const int fr = lane >> 2, fc = lane & 3;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int r = wm * MT * 8 + mt * 8 + fr, c = wn * NT * 8 + nt * 8 + 2 * fc;
-        if (r < Mv && c < Nv) asm volatile("prefetch.global.L1 [%0];" ::"l"(C + (int64_t)r * ld + c));
-      }
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r = wm * MT * 8 + mt * 8 + fr, c = wn * NT * 8 + nt * 8 + 2 * fc + i;
+          const double2 v = (r < Mv && c < Nv) ? C[(int64_t)r * ld + c] : cz();
+          acc[mt][nt][0][i] = v.x;
+          acc[mt][nt][1][i] = v.y;
+        }
   }
 
   template <class F>
@@ -1850,14 +1848,11 @@ __device__ void trail_body(const SolveParams& P, const Task& t, int e, int j, in
   // all rows in B_r and the panel inside S_l with A(B_r, S_l) structurally zero: L21 = 0 there
   if (P.zskip && d.zsplit && j1 <= (d.zsplit & 0xffff) && r0 >= s + (d.zsplit >> 16)) return;
   Tile64 T;
-  T.zero();
-  T.prefetch_c(M + (int64_t)r0 * n + c0, n, min(kTile, n - r0), min(cw, n - c0));
-  T.mma(M + (int64_t)r0 * n + j0, n, M + (int64_t)j0 * n + c0, n, min(kTile, n - r0), min(cw, n - c0), jb, smem);
+  T.load_c(M + (int64_t)r0 * n + c0, n, min(kTile, n - r0), min(cw, n - c0));
+  T.mma<false, true>(M + (int64_t)r0 * n + j0, n, M + (int64_t)j0 * n + c0, n, min(kTile, n - r0), min(cw, n - c0), jb,
+                     smem);
   T.for_each([&](int r, int c, double2 v) {
-    if (r0 + r < n && c < cw && c0 + c < n && (r0 + r < s || c0 + c < s)) {
-      double2* p = M + (int64_t)(r0 + r) * n + c0 + c;
-      *p = csub(*p, v);
-    }
+    if (r0 + r < n && c < cw && c0 + c < n && (r0 + r < s || c0 + c < s)) M[(int64_t)(r0 + r) * n + c0 + c] = v;
   });
 }
 
@@ -1878,20 +1873,17 @@ __device__ void schur_body(const SolveParams& P, const Task& t, int e, double2* 
   // K starts at s_l (rounded down to the K chunk: the same products in the same order)
   const int k0 = (P.zskip && d.zsplit && i0 >= (d.zsplit >> 16)) ? ((d.zsplit & 0xffff) / kKC) * kKC : 0;
   Tile64 T;
-  T.zero();
-  T.prefetch_c(M + (int64_t)(s + i0) * n + s + c0, n, min(kTile, b - i0), min(kTile, b - c0));
-  T.mma(M + (int64_t)(s + i0) * n + k0, n, M + (int64_t)k0 * n + s + c0, n, min(kTile, b - i0), min(kTile, b - c0),
-        s - k0, smem);
+  T.load_c(M + (int64_t)(s + i0) * n + s + c0, n, min(kTile, b - i0), min(kTile, b - c0));
+  T.mma<false, true>(M + (int64_t)(s + i0) * n + k0, n, M + (int64_t)k0 * n + s + c0, n, min(kTile, b - i0),
+                     min(kTile, b - c0), s - k0, smem);
   const bool store = d.kind != kFinal && d.out_arena >= 0;
   double2* out = store ? P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off : nullptr;
   const int32_t* rank = P.i32 + d.rank_off;
   T.for_each([&](int r, int c, double2 v) {
     const int i = i0 + r, jj = c0 + c;
     if (i < b && jj < b) {
-      double2* p = M + (int64_t)(s + i) * n + s + jj;
-      const double2 val = csub(*p, v);
-      if (store) out[(int64_t)rank[i] * b + rank[jj]] = val;
-      else *p = val;
+      if (store) out[(int64_t)rank[i] * b + rank[jj]] = v;
+      else M[(int64_t)(s + i) * n + s + jj] = v;
     }
   });
 }
@@ -1913,11 +1905,11 @@ __device__ void xsolve_tile(const Scr& S, int n, int s, int j, int r0, double2* 
   const int nr = min(rows, b - r0);
   {
     TT T;
-    T.zero();
-    T.prefetch_c(M + (int64_t)(s + r0) * n + j0, n, nr, jb);
-    if (s > j1) T.mma(S.X + (int64_t)r0 * s + j1, s, M + (int64_t)j1 * n + j0, n, nr, jb, s - j1, smem);
+    T.load_c(M + (int64_t)(s + r0) * n + j0, n, nr, jb);
+    if (s > j1)
+      T.template mma<false, true>(S.X + (int64_t)r0 * s + j1, s, M + (int64_t)j1 * n + j0, n, nr, jb, s - j1, smem);
     T.for_each([&](int r, int c, double2 v) {
-      if (r < nr && c < jb) S.X[(int64_t)(r0 + r) * s + j0 + c] = csub(M[(int64_t)(s + r0 + r) * n + j0 + c], v);
+      if (r < nr && c < jb) S.X[(int64_t)(r0 + r) * s + j0 + c] = v;
     });
   }
   __syncthreads();
@@ -2099,15 +2091,11 @@ __device__ void tgemm_body(const SolveParams& P, const Task& t, int e, int nb, d
   const Scr S = scratch_of(P, d, e);
   const int i0 = t.a * kTile, c0 = t.b * kTile;
   Tile64 T;
-  T.zero();
-  T.prefetch_c(S.MS + (int64_t)(s + i0) * n + c0, n, min(kTile, b - i0), min(kTile, s - c0));
+  T.load_c(S.MS + (int64_t)(s + i0) * n + c0, n, min(kTile, b - i0), min(kTile, s - c0));
   const Scr SX = scratch_of(P, d, e, nb);
-  T.mma(SX.X + (int64_t)i0 * s, s, S.MS + c0, n, min(kTile, b - i0), min(kTile, s - c0), s, smem);
+  T.mma<false, true>(SX.X + (int64_t)i0 * s, s, S.MS + c0, n, min(kTile, b - i0), min(kTile, s - c0), s, smem);
   T.for_each([&](int r, int c, double2 v) {
-    if (i0 + r < b && c0 + c < s) {
-      double2* p = S.MS + (int64_t)(s + i0 + r) * n + c0 + c;
-      *p = csub(*p, v);
-    }
+    if (i0 + r < b && c0 + c < s) S.MS[(int64_t)(s + i0 + r) * n + c0 + c] = v;
   });
 }
 
@@ -2129,11 +2117,10 @@ __device__ void rgemm_body(const SolveParams& P, const Task& t, int e, int nb, d
   const int i0 = t.a * kTile, c0 = t.b * kTile;
   const int mv = min(kTile, b - i0), nv = min(kTile, b - c0);
   Tile64 T;
-  T.zero();
-  T.prefetch_c(S.MS + (int64_t)(s + i0) * n + s + c0, n, mv, nv);
+  T.load_c(S.MS + (int64_t)(s + i0) * n + s + c0, n, mv, nv);
   const Scr SX = scratch_of(P, d, e, nb);
-  T.mma<false>(SX.X + (int64_t)i0 * s, s, S.MS + s + c0, n, mv, nv, s, smem);          // X Sigma'_SB
-  T.mma<true>(S.MS + (int64_t)(s + i0) * n, n, SX.X + (int64_t)c0 * s, s, mv, nv, s, smem);  // T_S X^H
+  T.mma<false, true>(SX.X + (int64_t)i0 * s, s, S.MS + s + c0, n, mv, nv, s, smem);          // - X Sigma'_SB
+  T.mma<true, true>(S.MS + (int64_t)(s + i0) * n, n, SX.X + (int64_t)c0 * s, s, mv, nv, s, smem);  // - T_S X^H
   const bool store = d.kind != kFinal && d.out_arena >= 0;
   const bool mirror = store && P.rsym != 0;
   const double sg = P.rsym < 0 ? -1.0 : 1.0;
@@ -2143,10 +2130,9 @@ __device__ void rgemm_body(const SolveParams& P, const Task& t, int e, int nb, d
   T.for_each([&](int r, int c, double2 v) {
     const int i = i0 + r, jj = c0 + c;
     if (i < b && jj < b) {
-      double2* p = S.MS + (int64_t)(s + i) * n + s + jj;
-      const double2 val = csub(*p, v);
+      const double2 val = v;
       if (!store) {
-        *p = val;
+        S.MS[(int64_t)(s + i) * n + s + jj] = val;
       } else if (!mirror) {
         out[(int64_t)rank[i] * b + rank[jj]] = val;
       } else if (i >= jj) {
