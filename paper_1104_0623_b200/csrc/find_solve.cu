@@ -831,11 +831,20 @@ __device__ void gather_body(const SolveParams& P, const Task& t, int e) {
   const double2* rb = child_block(P, d, e, false, SIGMA);
   const double2* vals = SIGMA ? P.s_vals + (P.s_broadcast ? 0 : (int64_t)e * P.nnz) : P.a_vals + (int64_t)e * P.nnz;
   const int r0 = t.a, nr = t.b;
+  // flat (row, column) walk over the chunk with the position stepped incrementally (one
+  // division per thread instead of one per element)
+  const int istep = kThreads / n, jstep = kThreads % n;
+  int i = r0 + threadIdx.x / n, j = threadIdx.x % n;
   for (int q = threadIdx.x; q < nr * n; q += kThreads) {
-    const int i = r0 + q / n, j = q % n;
     const int mi = map[(SIGMA && i < s) ? S.SIG[i] : i];
     const int mj = map[(SIGMA && j < s) ? S.SIG[j] : j];
     dst[(int64_t)i * n + j] = block_entry(d, lb, rb, mi, mj);
+    i += istep;
+    j += jstep;
+    if (j >= n) {
+      j -= n;
+      ++i;
+    }
   }
   __syncthreads();
   const SparseEntry* sp = P.sparse + d.sparse_off;
