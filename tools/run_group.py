@@ -1,5 +1,6 @@
 """One full cfg solve (inputs, arenas), then the launch groups given by --groups run alone:
-the target of a focused ncu capture (`-k regex:<kernel> -s <launches of that kernel per solve>`).
+the target of a focused ncu capture (`-k regex:<kernel> -s <launches of that kernel per solve>`);
+without --groups, one solve (the launch list of `ncu --metrics ...`).
 
     python tools/run_group.py --config 1 --groups 104 108
 """
@@ -16,7 +17,7 @@ from paper_1104_0623_b200.plan import plan_for  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=1)
-ap.add_argument("--groups", type=int, nargs="+", required=True)
+ap.add_argument("--groups", type=int, nargs="*", default=[])
 ap.add_argument("--no-full", action="store_true", help="skip the full solve (inputs of the groups then stale)")
 a = ap.parse_args()
 p = config_problem(a.config)
