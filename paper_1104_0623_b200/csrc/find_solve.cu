@@ -144,7 +144,7 @@ __device__ __forceinline__ double2 block_entry(const ElimDesc& d, const double2*
 
 // ================================================================== small path
 // One warp per (elimination, energy); merged size n <= 32.
-constexpr int kSmallWarps = 4;
+constexpr int kSmallWarps = 1;
 
 __device__ void warp_gj_inverse(double2* a, int lda, int c, int lane, bool* singular) {
   // In-place Gauss-Jordan inversion with partial pivoting (row interchanges),

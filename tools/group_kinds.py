@@ -74,7 +74,14 @@ for r in rows:
     for k, v in r["kinds"].items():
         by_kind[k] = by_kind.get(k, 0.0) + v
 print("by kind:", json.dumps({k: round(v, 2) for k, v in sorted(by_kind.items(), key=lambda x: -x[1])}))
+near = [r for r in rows if r["level"] <= 4 and r["pass"] in (0, 1)]
+near_ms = sum(r["ms"] for r in near)
+near_tf = sum(r["tflops"] * r["ms"] for r in near) / near_ms if near_ms else 0.0
+near_root = {"config": a.config, "energies": ne, "levels": "upward 1-4 + downward 1-4", "groups": len(near),
+             "ms_serialized": round(near_ms, 3), "tflops": round(near_tf, 3), "frac_fp64_peak": round(near_tf / 37.19, 4)}
+print("near_root", json.dumps(near_root))
 for r in sorted(rows, key=lambda r: -r["ms"])[: a.top]:
     print(json.dumps(r))
 if a.out:
-    Path(a.out).write_text(json.dumps({"total_ms": total, "by_kind": by_kind, "groups": rows}, indent=1))
+    Path(a.out).write_text(json.dumps({"total_ms": total, "by_kind": by_kind, "near_root": near_root, "groups": rows},
+                                      indent=1))
