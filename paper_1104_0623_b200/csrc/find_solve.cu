@@ -1732,17 +1732,19 @@ __device__ void trsm_body(const SolveParams& P, const Task& t, int e, int j, dou
     // t.c-wide strip of the next panel of a wide block: all moved rows are read before any is written
     const int c0 = t.b, cn = min(t.c > 0 ? t.c : kTile, (t.a == 2 ? j0 : n) - c0);
     const int nd = S.PERM[0];
-    double2* st = smem;  // [2 NB][64]
-    for (int q = threadIdx.x; q < nd * kTile; q += kThreads) {
-      const int k = q / kTile, c = q % kTile;
-      if (c < cn) st[q] = M[(int64_t)(j0 + S.PERM[1 + k]) * n + c0 + c];
+    if (nd > 0) {  // (uniform over the CTA)
+      double2* st = smem;  // [2 NB][64]
+      for (int q = threadIdx.x; q < nd * kTile; q += kThreads) {
+        const int k = q / kTile, c = q % kTile;
+        if (c < cn) st[q] = M[(int64_t)(j0 + S.PERM[1 + k]) * n + c0 + c];
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < nd * kTile; q += kThreads) {
+        const int k = q / kTile, c = q % kTile;
+        if (c < cn) M[(int64_t)(j0 + S.PERM[1 + 2 * NB + k]) * n + c0 + c] = st[q];
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    for (int q = threadIdx.x; q < nd * kTile; q += kThreads) {
-      const int k = q / kTile, c = q % kTile;
-      if (c < cn) M[(int64_t)(j0 + S.PERM[1 + 2 * NB + k]) * n + c0 + c] = st[q];
-    }
-    __syncthreads();
     if (t.a == 2) return;
   }
   if (!inv_ready) {  // the diagonal block's inverse this tile needs (L for U12 tiles, U for L21 tiles),

@@ -386,18 +386,6 @@ def _offdiag_dict(pairs: np.ndarray, vals: np.ndarray) -> dict:
     return dict(zip(map(tuple, pairs.tolist()), vals.tolist()))
 
 
-_PACK_THREADS = 4
-_POOL = []
-
-
-def _pack_pool():
-    if not _POOL:
-        from concurrent.futures import ThreadPoolExecutor
-
-        _POOL.append(ThreadPoolExecutor(_PACK_THREADS, thread_name_prefix="find-pack"))
-    return _POOL[0]
-
-
 def _prepare(mesh, a_list, sigma, config):
     """Validation (solver.py:591-608), cached plan, values packed into a reused pinned buffer."""
     if not a_list:
@@ -407,21 +395,15 @@ def _prepare(mesh, a_list, sigma, config):
     am0 = _csr_sorted(a_list[0].matrix)
     plan, _ = plan_for(mesh.nx, mesh.ny, am0.indptr, am0.indices, config.leaf_max)
     _validate(mesh, a_list[0], sigma, config, plan.cache)
+    import torch
+
     vals = plan.host_values(len(a_list))
-    mats = [am0] + [_csr_sorted(a.matrix) for a in a_list[1:]]
-
-    def pack(ks):  # pattern check and value copy of operators ks (memcmp / copyto run without the GIL)
-        for k in ks:
-            am = mats[k]
-            if am.nnz != am0.nnz or not same_array(am.indptr, am0.indptr) or not same_array(am.indices, am0.indices):
-                return False
-            np.copyto(vals[k], am.data, casting="same_kind")
-        return True
-
-    parts = [range(k, len(mats), _PACK_THREADS) for k in range(min(_PACK_THREADS, len(mats)))]
-    ok = all(_pack_pool().map(pack, parts)) if len(parts) > 1 else pack(parts[0])
-    if not ok:
-        raise ValueError("all operators of a batch must share one sparsity pattern")
+    vt = plan.pinned_tensor(vals)  # the same pinned buffer as a tensor: torch's multi-threaded copies
+    for k, a in enumerate(a_list):
+        am = am0 if k == 0 else _csr_sorted(a.matrix)
+        if am.nnz != am0.nnz or not same_array(am.indptr, am0.indptr) or not same_array(am.indices, am0.indices):
+            raise ValueError("all operators of a batch must share one sparsity pattern")
+        vt[k].copy_(torch.from_numpy(np.ascontiguousarray(am.data)))
     s_vals, ssym, sherm = (None, 0, False)
     if config.compute_gless:
         s_vals, ssym, sherm = _sigma_prepare(plan, am0, sigma)
