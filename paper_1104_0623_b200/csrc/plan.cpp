@@ -116,7 +116,7 @@ bool xsolve16_enabled() {
 // Groups whose largest S exceeds this use wide (K = 64) trailing updates (FIND_B200_WIDE_MIN_S).
 int wide_min_s() {
   const char* f = std::getenv("FIND_B200_WIDE_MIN_S");
-  return f ? std::atoi(f) : 288;
+  return f ? std::atoi(f) : 200;
 }
 
 void find_build_tasks(find_plan* P) {
