@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kMidThreads) mid_elim_kernel(SolveParams P, in
   const int ld = nmax + 1;
   double2* MA = reinterpret_cast<double2*>(smem_raw);
   double2* XC = MA + nmax * ld;
-  double2* LC = XC + xcap;  // multipliers of the current column [64]
+  double2* LC = XC + xcap;  // spare [64] (layout of mid_smem_elems)
   int* piv = reinterpret_cast<int*>(LC + kMidMaxN);
   int* sig = piv + kMidMaxN;
   int* isg = sig + kMidMaxN;
@@ -506,20 +506,17 @@ __global__ void __launch_bounds__(kMidThreads) mid_elim_kernel(SolveParams P, in
     __syncthreads();
     const double2 uinv = s_uinv;
     const int rows = n - k - 1;
-    for (int r = tid; r < rows; r += NT) {
-      const double2 l = cmul(MA[(k + 1 + r) * ld + k], uinv);
-      LC[r] = l;
-      MA[(k + 1 + r) * ld + k] = l;
-    }
-    __syncthreads();
-    {  // rank-1 update: warp = row (stride 4), lane = column (rows <= 63: two columns per lane)
+    {  // multiplier and rank-1 update: warp = row (stride 4), lane = column (rows <= 63: two columns
+       // per lane); every lane forms its row's multiplier from the broadcast column-k entry
       const int warp = tid >> 5, lane = tid & 31;
       const double2* pr_row = MA + k * ld + k + 1;
       const double2 u0 = lane < rows ? pr_row[lane] : cz();
       const double2 u1 = lane + 32 < rows ? pr_row[lane + 32] : cz();
       for (int r = warp; r < rows; r += NT / 32) {
         double2* row = MA + (k + 1 + r) * ld + k + 1;
-        const double2 l = LC[r];
+        const double2 l = cmul(row[-1], uinv);
+        __syncwarp();
+        if (lane == 0) row[-1] = l;
         if (lane < rows) row[lane] = cfms(row[lane], l, u0);
         if (lane + 32 < rows) row[lane + 32] = cfms(row[lane + 32], l, u1);
       }
