@@ -2888,7 +2888,8 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           p.elims = prm.elims + L.task_off;
           p.elim_base = L.task_off;
           const int nmax = std::max(1, G.max_n), ld = nmax + 1;
-          const int xcap = G.max_b * G.max_s + G.max_b * G.max_b;
+          // X [b][s], plus U_f [b][b] for final steps (pass 2 groups hold exactly those)
+          const int xcap = G.max_b * G.max_s + (G.pass == 2 ? G.max_b * G.max_b : 0);
           const size_t smem = (size_t)kSmallWarps * small_warp_elems(nmax, ld, xcap) * sizeof(double2);
           launch_k(small_elim_kernel, dim3((unsigned)((L.task_count + kSmallWarps - 1) / kSmallWarps), (unsigned)nE), kSmallWarps * 32, smem, stream, p, L.task_count, nmax, ld, xcap);
           break;
@@ -2898,7 +2899,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           p.elims = prm.elims + L.task_off;
           p.elim_base = L.task_off;
           const int nmax = std::max(1, G.max_n);
-          const int xcap = G.max_b * G.max_s + G.max_b * G.max_b;
+          const int xcap = G.max_b * G.max_s + (G.pass == 2 ? G.max_b * G.max_b : 0);  // X, U_f of final steps
           const size_t smem = (size_t)mid_smem_elems(nmax, xcap) * sizeof(double2);
           launch_k(mid_elim_kernel, dim3((unsigned)L.task_count, (unsigned)nE), kMidThreads, smem, stream, p, L.task_count, nmax,
                                                                                                    xcap);
