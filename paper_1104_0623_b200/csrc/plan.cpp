@@ -112,6 +112,10 @@ bool xsolve16_enabled() {
   const char* f = std::getenv("FIND_B200_XS16");
   return !(f && f[0] == '0');
 }
+int xsolve16_min_s() {  // groups with a larger S qualify (FIND_B200_XS16_MIN_S)
+  const char* f = std::getenv("FIND_B200_XS16_MIN_S");
+  return f ? std::atoi(f) : 288;
+}
 
 // Groups whose largest S exceeds this use wide (K = 64) trailing updates (FIND_B200_WIDE_MIN_S).
 int wide_min_s() {
@@ -222,7 +226,7 @@ void find_build_tasks(find_plan* P) {
       int64_t tiles = 0;  // few 64-row tiles (large-S groups): 16-row tiles, 4x the parallelism
       for (int64_t e = G.begin; e < G.end; ++e)
         if (P->elims[e].s > 0) tiles += (P->elims[e].b + kTile - 1) / kTile;
-      const int rows = (nb == 32 && tiles < 148 && G.max_s > 288 && xsolve16_enabled()) ? 16 : kTile;
+      const int rows = (nb == 32 && tiles < 148 && G.max_s > xsolve16_min_s() && xsolve16_enabled()) ? 16 : kTile;
       for (int64_t e = G.begin; e < G.end; ++e) {
         const ElimDesc& d = P->elims[e];
         if (d.s == 0 || d.b == 0) continue;
