@@ -423,7 +423,9 @@ __device__ void block_argmax(double& v, int& vi, double* cv, int* ci) {
 // algorithm, CTA-wide).
 constexpr int kMidThreads = 128;
 constexpr int kMidMaxN = 64;
-__host__ __device__ constexpr int mid_smem_elems(int nmax, int xcap) { return nmax * (nmax + 1) + xcap + 3 * kMidMaxN / 4 + 2 * kMidMaxN + 16; }
+// M [nmax][nmax+1], XC [xcap], then piv / sig / isg (3 x 64 ints); sized tightly (occupancy
+// of the mid path is set by this shared-memory footprint)
+__host__ __device__ constexpr int mid_smem_elems(int nmax, int xcap) { return nmax * (nmax + 1) + xcap + 3 * kMidMaxN / 4; }
 
 template <int NT>
 __device__ __forceinline__ void block_max(double& v, double* cv) {
@@ -453,8 +455,7 @@ __global__ void __launch_bounds__(kMidThreads) mid_elim_kernel(SolveParams P, in
   const int ld = nmax + 1;
   double2* MA = reinterpret_cast<double2*>(smem_raw);
   double2* XC = MA + nmax * ld;
-  double2* LC = XC + xcap;  // spare [64] (layout of mid_smem_elems)
-  int* piv = reinterpret_cast<int*>(LC + kMidMaxN);
+  int* piv = reinterpret_cast<int*>(XC + xcap);
   int* sig = piv + kMidMaxN;
   int* isg = sig + kMidMaxN;
   const int32_t* map = P.i32 + d.map_off;
