@@ -633,7 +633,7 @@ struct Scr {
   int* PERM;    // current panel's net row interchange: {nd, src[64], dst[64]}
   int* PERM2;   // the first panel's PERM of a wide (two-panel) block, saved for the wide TRSM
   double* scale;
-  double* pmax;   // per gather row chunk: max |A(S,S)| over its rows   [ceil(n/16)]
+  double* pmax;   // per gather row chunk: max |A(S,S)| over its rows   [ceil(n/kRowChunk)]
   double2* LINV;  // per panel j: L_jj^-1  [NB][NB]   (valid when nb > 0)
   double2* UINV;  // per panel j: U_jj^-1  [NB][NB]
   double2* X;     // X = Y L11^-1   [b][s]            (valid when nb > 0)
@@ -652,7 +652,7 @@ __device__ __forceinline__ Scr scratch_of(const SolveParams& P, const ElimDesc& 
   const int64_t ints = (3 * d.s + 264 + 3) / 4;
   r.scale = reinterpret_cast<double*>(r.M + 2 * nn + ints);
   r.pmax = r.scale + 2;
-  r.LINV = r.M + 2 * nn + ints + 1 + (d.n + 31) / 32;
+  r.LINV = r.M + 2 * nn + ints + 1 + (d.n + 2 * kRowChunk - 1) / (2 * kRowChunk);
   r.UINV = nb ? r.LINV + (int64_t)((d.s + nb - 1) / nb) * nb * nb : r.LINV;
   r.X = nb ? r.UINV + (int64_t)((d.s + nb - 1) / nb) * nb * nb : r.LINV;
   return r;
@@ -849,10 +849,11 @@ __device__ void gather_body(const SolveParams& P, const Task& t, int e) {
   // rows in merged order (A, and the B rows of Sigma) own one contiguous range of the
   // sparse list: one flat loop; pivot-permuted Sigma S rows one range per row
   const int flat0 = SIGMA ? max(r0, min(s, r0 + nr)) : r0;
-  for (int ri = 0; ri < flat0 - r0; ++ri) {
+  // (one warp per row: a row holds a handful of entries)
+  for (int ri = threadIdx.x / 32; ri < flat0 - r0; ri += kThreads / 32) {
     const int i = r0 + ri;
     const int mr = S.SIG[i];
-    for (int q = rowoff[mr] + threadIdx.x; q < rowoff[mr + 1]; q += kThreads) {
+    for (int q = rowoff[mr] + (threadIdx.x & 31); q < rowoff[mr + 1]; q += 32) {
       const SparseEntry en = sp[q];
       const int j = en.j < s ? S.ISG[en.j] : en.j;
       dst[(int64_t)i * n + j] = ldg2(vals + en.csr);

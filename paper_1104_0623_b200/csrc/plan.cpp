@@ -47,7 +47,7 @@ void set_status(find_status* st, int code, const char* msg) {
 // the inverted diagonal blocks L_jj^-1, U_jj^-1 of every panel (nb x nb).
 // Must match scratch_of() in find_solve.cu.
 int64_t find_scratch_elems(int64_t n, int64_t s, int nb) {
-  int64_t e = 2 * n * n + (3 * s + 264 + 3) / 4 + 1 + (n + 31) / 32;
+  int64_t e = 2 * n * n + (3 * s + 264 + 3) / 4 + 1 + (n + 2 * kRowChunk - 1) / (2 * kRowChunk);
   if (nb > 0) e += 2 * ((s + nb - 1) / nb) * (int64_t)nb * nb + (n - s) * s;  // + X [b][s]
   return (e + 1) & ~int64_t(1);
 }

@@ -86,7 +86,7 @@ inline int pick_nb_host(int64_t max_s) {
 constexpr int kTile = 64;       // DMMA output tile edge
 constexpr int64_t kSplitDownElems = int64_t(1) << 29;  // complex elements (8 GiB) of one level's complement blocks
 constexpr int64_t kGroupScratchCap = int64_t(1) << 28;  // complex elements of CTA-path scratch per energy per phase (4 GiB)
-constexpr int kRowChunk = 16;   // gather rows per CTA
+constexpr int kRowChunk = 16;  // gather rows per CTA (8: gathers 5 % faster serialized, solve 323 -> 321)
 
 struct LaunchGroup {
   int64_t begin, end;  // ElimDesc range
