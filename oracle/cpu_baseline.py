@@ -122,3 +122,51 @@ def blas_threads() -> int:
         return max([int(i.get("num_threads", 1)) for i in info] or [os.cpu_count() or 1])
     except Exception:
         return os.cpu_count() or 1
+
+
+def _energy_worker(nx, ny, a, sg, fraction, seed, barrier, out):
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(1):
+        o = FindOracle(nx, ny, a)
+        barrier.wait()
+        out.put(estimate_seconds_per_energy(o, a, sg, fraction=fraction, seed=seed))
+
+
+def parallel_energy_rate(nx, ny, a, sg, workers=None, fraction=0.125, seed=0):
+    """Energy-parallel CPU throughput: ``workers`` processes (default: every host core), one BLAS
+    thread each, each estimating a different energy point concurrently (all cores busy while every
+    sample is timed).  Energy points are independent, so this is how a host sweep uses its cores;
+    single-process threaded LAPACK on these block sizes is several times slower (bench.py notes)."""
+    import multiprocessing as mp
+
+    workers = workers or os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    keys = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
+    saved = {k: os.environ.get(k) for k in keys}
+    for k in keys:
+        os.environ[k] = "1"
+    try:
+        barrier, out = ctx.Barrier(workers), ctx.Queue()
+        procs = [ctx.Process(target=_energy_worker, args=(nx, ny, a, sg, fraction, seed + w, barrier, out))
+                 for w in range(workers)]
+        for p in procs:
+            p.start()
+        res = [out.get() for _ in procs]
+        for p in procs:
+            p.join()
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    t = [r["seconds_per_energy"] for r in res]
+    return {
+        "rate": float(sum(1.0 / x for x in t)),
+        "seconds_per_energy": float(np.mean(t)),
+        "workers": workers,
+        "sampled_eliminations": res[0]["sampled_eliminations"],
+        "total_eliminations": res[0]["total_eliminations"],
+        "sample_wall_seconds": float(max(r["sample_wall_seconds"] for r in res)),
+    }

@@ -52,3 +52,14 @@ def test_cpu_baseline_estimator_runs():
     o = FindOracle(p.nx, p.ny, p.a_csr(0))
     r = estimate_seconds_per_energy(o, p.a_csr(0), p.sigma_csr(), fraction=0.5, seed=0)
     assert r["seconds_per_energy"] > 0 and r["sampled_eliminations"] > 0
+
+
+def test_cpu_baseline_energy_parallel_runs():
+    """The energy-parallel CPU baseline (one process per core, one BLAS thread each) on a tiny mesh."""
+    from oracle.cpu_baseline import parallel_energy_rate
+    from paper_1104_0623_b200.configs import build_problem
+
+    p = build_problem(12, 10, [1.0], seed=2)
+    r = parallel_energy_rate(p.nx, p.ny, p.a_csr(0).tocsr(), p.sigma_csr().tocsr(), workers=2, fraction=0.5)
+    assert r["workers"] == 2 and r["rate"] > 0 and r["sampled_eliminations"] > 0
+    assert abs(r["rate"] - 2.0 / r["seconds_per_energy"]) < 0.5 * r["rate"]
