@@ -1,11 +1,15 @@
 """Benchmark of the FIND selected-inversion hot path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl reference]
 
-Workload (BASELINE.json configs[1]): 130x130 mesh, 5-point stencil with dense
-contact self-energies, 16 energy points solved as one batch; outputs
-diag(G^r) and diag(G^<) per energy.  One "step" = one selected inversion of
-all 16 energy points.  Metric: energy points/s (whole job, all GPUs).
+Workload (default: BASELINE.json configs[4], the largest single-GPU config):
+1024x1024 mesh, 5-point stencil with dense contact self-energies, 8 energy
+points solved as one job; outputs diag(G^r) and diag(G^<) per energy.  One
+"step" = one selected inversion of all the config's energy points (in as many
+find_solve calls as the device memory needs: cfg4 fits 4 energy points per call).
+Metric: energy points/s (whole job, all GPUs).  ``--config 1`` etc. select the
+other BASELINE configs; the cfg1 device number is reported beside the headline
+(``cfg1`` key).
 
 `value`   device throughput, inputs resident in HBM, CUDA events on the solve
           stream, L2 flushed (256 MiB write) between timed steps.
@@ -13,16 +17,19 @@ all 16 energy points.  Metric: energy points/s (whole job, all GPUs).
           (paper_1104_0623_b200.solve_batch on SparseOperator inputs): host
           validation, pinned H2D of the step's A(E_k)/Sigma^< values, kernels,
           D2H of both diagonals; host wall clock per step.
-`roofline` the dominant kernel (by device time) against the measured FP64
-          tensor peak (DMMA microbenchmark, profiles/r01_fp64_probe.txt); work
-          is the reference ledger W (complex mults, kernels.py:88-146) x 8 flop.
-`cpu_baseline` the oracle port of the reference path (oracle/), stratified
-          sample of one energy point's eliminations, extrapolated (rank 0, N=1).
+`roofline` the dominant FP64 tensor-core kernel kind against the measured FP64
+          DMMA peak (profiles/r01_fp64_probe.txt), executed complex MACs x 8 per
+          serialized CUDA-event duration (paper_1104_0623_b200/workmodel.py).
+`cpu_baseline` the oracle port of the reference path (oracle/cpu_baseline.py):
+          bucket-stratified sample of one energy point's eliminations, timed
+          energy-parallel on every host core (rank 0, N=1).
 
---impl reference: times the oracle port (the reference's algorithm and LAPACK
-calls, oracle/find_oracle.py) on the host cores, same metric/config.
-Multi-GPU: replicas (energy sharding, no data-path collective): each rank
-solves its own 16 energy points; value = N*16*K / max-over-ranks time.
+--impl reference: times the same oracle port (the reference's algorithm and
+LAPACK calls per elimination) on the host cores, same metric / config.
+Multi-GPU (--gpus N > 1): self-launches N ranks through torch.distributed.run
+when not already under it; replicas (energy sharding, no data-path
+collective): every rank solves its own energy points; value = N*nE*K / max-over-
+ranks device time.
 """
 
 from __future__ import annotations
@@ -30,6 +37,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -46,18 +54,21 @@ FP64_PEAK_TFLOPS = 37.19  # measured: mma.sync m8n8k4 f64 (DMMA.8x8x4), 148 SMs 
 ZGEMM_TFLOPS = 37.02      # measured: cuBLAS ZGEMM 8192^3 via torch (profiles/r01_blas_probe.txt)
 METRIC = "energy points/sec per mesh (diag G^r + G^<)"
 UNIT = "energy points/s"
+NCU_KERNELS = ROOT / "profiles" / "r02_ncu_kernels.json"  # ncu --set full DRAM bytes per launch (cfg4 run)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg1 side measurement")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="calls of the e2e leg (default: by step time)")
     ap.add_argument("--levels", default="", help="write per-launch-group timings (json) to this path")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -65,6 +76,28 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     return rank, world, local
+
+
+def self_launch(args) -> bool:
+    """--gpus N > 1 outside torchrun: re-run this script under torch.distributed.run with N ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def config_dict(cfg, world):
+    """The workload description both arms print (identical, so the driver can match them)."""
+    return {"workload": f"cfg{cfg.index}: {cfg.nx}x{cfg.ny} {cfg.stencil}-point stencil + dense contacts, "
+                        f"{cfg.n_energies} energy points per GPU, diag G^r + G^<",
+            "mesh": [cfg.nx, cfg.ny], "stencil": cfg.stencil, "n_energies_per_gpu": cfg.n_energies,
+            "parallelism": f"replicas{world} (energy sharding)" if world > 1 else "single GPU",
+            "l2": "flushed (256 MiB write) between timed steps, outside the timed events"}
 
 
 class ClockSampler:
@@ -121,59 +154,153 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline_line(cfg_index, p, fraction=0.125):
-    from oracle.cpu_baseline import parallel_energy_rate
+def cpu_port(cfg_index, steps, warmup):
+    """The oracle port's energy-parallel estimate (oracle/cpu_baseline.py) in a child process: it
+    forks one worker per host core, which must not happen in a process that holds a CUDA context."""
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    out = subprocess.run([sys.executable, "-m", "oracle.cpu_baseline", "--config", str(cfg_index), "--steps",
+                          str(steps), "--warmup", str(warmup)], cwd=str(ROOT), env=env, capture_output=True,
+                         text=True, check=True)
+    return json.loads(out.stdout.strip().splitlines()[-1])
 
-    r = parallel_energy_rate(p.nx, p.ny, p.a_csr(0).tocsr(), p.sigma_csr().tocsr(), fraction=fraction)
-    return {
-        "value": r["rate"],
-        "unit": UNIT,
-        "cores": r["workers"],
-        "kind": "port",
-        "sample": (f"oracle port of reference solve (naive, compute_gless) on cfg{cfg_index}, energy-parallel: "
-                   f"{r['workers']} processes x 1 BLAS thread, each a different energy point, concurrently; per "
-                   f"process a stratified {r['sampled_eliminations']}/{r['total_eliminations']} elimination sample "
-                   f"({r['sample_wall_seconds']:.1f} s wall) extrapolated per (pass, level) group; "
-                   f"{r['seconds_per_energy']:.2f} s per energy point per process; value = sum of per-process rates"),
-    }
+
+PORT_NOTE = ("the port is the reference algorithm with the same LAPACK calls but without its Python set-up "
+             "(O(n * #clusters) sets, per-call O(n) extract_block lookups): at cfg1 it runs one energy point in "
+             "11.8 s on 1 core against the reference's 115 s on 8 threads (SURVEY.md §6, §8(c)), so it favours the CPU")
+
+
+def cpu_baseline_line(cfg_index):
+    r = cpu_port(cfg_index, 1, 0)
+    return {"value": r["steps"][0]["rate"], "unit": UNIT, "cores": r["workers"], "kind": "port",
+            "sample": r["sample"] + "; " + PORT_NOTE, "setup_seconds": round(r["setup_seconds"], 1)}
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_1104_0623_b200.configs import CONFIGS, config_problem
+    from paper_1104_0623_b200.configs import CONFIGS
 
     cfg = CONFIGS[args.config]
-    p = config_problem(args.config, 1)
-    from oracle.cpu_baseline import parallel_energy_rate
-
-    a, sg = p.a_csr(0).tocsr(), p.sigma_csr().tocsr()
-    frac = 0.125 if args.config > 0 else 1.0
-    for w in range(args.warmup):
-        parallel_energy_rate(p.nx, p.ny, a, sg, fraction=min(frac, 0.02), seed=1000 + 100 * w)
-    rates, walls, workers = [], [], 1
-    for k in range(args.steps):
-        r = parallel_energy_rate(p.nx, p.ny, a, sg, fraction=frac, seed=100 * k)
-        rates.append(r["rate"])
-        walls.append(r["sample_wall_seconds"])
-        workers = r["workers"]
+    r = cpu_port(args.config, args.steps, args.warmup)
+    rates = [s["rate"] for s in r["steps"]]
     v = float(np.mean(rates))
-    t = 1.0 / v
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"cfg{args.config}: {cfg.nx}x{cfg.ny} {cfg.stencil}-point, {cfg.n_energies} energy "
-                               f"points, diag G^r + G^<", "mesh": [cfg.nx, cfg.ny], "n_energies": cfg.n_energies},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": (f"per step: oracle port (reference algorithm, scipy LAPACK per elimination), "
-                                    f"energy-parallel: {workers} processes x 1 BLAS thread, each a stratified "
-                                    f"{frac:.3f} sample of a different energy point's eliminations, extrapolated; "
-                                    f"value = sum of per-process rates; mean sample wall {np.mean(walls):.1f} s")},
+        "warmup": args.warmup, "ms_per_step": 1e3 * cfg.n_energies / v, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": config_dict(cfg, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["workers"], "kind": "port",
+                         "sample": "per step: " + r["sample"] + "; " + PORT_NOTE,
+                         "per_step_rates": [round(x, 4) for x in rates],
+                         "setup_seconds": round(r["setup_seconds"], 1)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def device_measure(plan, p, dev, steps, warmup, world, chunk, ssym, flush, with_graph=True):
+    """Device-timed steps of one config: inputs resident, L2 flushed between steps, CUDA events on
+    the solve stream; the timed steps replay the captured launch schedule (CUDA graph)."""
+    import torch
+    import torch.distributed as dist
+
+    n_e = p.energies.size
+    stream = torch.cuda.Stream(dev)
+    a_d = torch.from_numpy(p.a_vals_all()).to(dev)
+    s_d = torch.from_numpy(p.s_vals).to(dev)
+    gr_d = torch.empty((n_e, plan.n), dtype=torch.complex128, device=dev)
+    gl_d = torch.empty((n_e, plan.n), dtype=torch.complex128, device=dev)
+    ws = plan.workspace(chunk, True, dev)
+    torch.cuda.synchronize()
+
+    def step_eager():
+        for k0 in range(0, n_e, chunk):
+            k1 = min(n_e, k0 + chunk)
+            plan.run(a_d[k0:k1], s_d, gr_d[k0:k1], gl_d[k0:k1], ws=ws, stream=stream, sigma_sym=ssym)
+
+    graph = None
+
+    def step():
+        graph.replay() if graph is not None else step_eager()
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(warmup, 3) - 1):
+            step_eager()
+        plan.check_status(ws, chunk, stream)
+        if with_graph and os.environ.get("FIND_B200_GRAPH", "1") != "0":
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                step_eager()
+        step()  # last warm-up step (the graph's first replay)
+        plan.check_status(ws, chunk, stream)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    clocks = ClockSampler(dev.index)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    with torch.cuda.stream(stream):
+        for k in range(steps):
+            flush.fill_(k & 0xff)
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    plan.check_status(ws, chunk, stream)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_max = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    dev_ms = float(t_max.item())
+    return {"dev_ms": dev_ms, "step_ms": step_ms, "clocks": clk, "graph": graph is not None, "stream": stream,
+            "a_d": a_d, "s_d": s_d, "gr_d": gr_d, "gl_d": gl_d, "ws": ws, "graph_obj": graph}
+
+
+def serialized_kinds(plan, m, n_e, chunk, ssym, flush):
+    """One instrumented step with every launch group run ALONE (groups in plan order on the solve
+    stream, so each launch's CUDA-event duration is its own) -> per-kind FP64 rates, live."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1104_0623_b200 import _native
+    from paper_1104_0623_b200.workmodel import KINDS, executed_cmacs
+
+    lib = _native.lib()
+    stream = m["stream"]
+    ngroups = len(plan.groups["count"])
+    c0 = min(chunk, n_e)  # the first call's energy points; per-kind rates are per launch
+    with torch.cuda.stream(stream):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        lib.find_solve_timing_enable(1)
+        for gi in range(ngroups):
+            plan.run(m["a_d"][:c0], m["s_d"], m["gr_d"][:c0], m["gl_d"][:c0], ws=m["ws"], stream=stream,
+                     sigma_sym=ssym, groups=(gi, gi + 1))
+        torch.cuda.synchronize()
+        lib.find_solve_timing_enable(0)
+    nl = int(lib.find_solve_timing_read(None, None, None, 0))
+    kk = (C.c_int32 * nl)()
+    gg = (C.c_int32 * nl)()
+    ms = (C.c_float * nl)()
+    lib.find_solve_timing_read(kk, gg, ms, nl)
+    work = executed_cmacs(plan, ssym)
+    per_kind = {}
+    per_group_ms = np.zeros(ngroups)
+    for i in range(nl):
+        d = per_kind.setdefault(KINDS[kk[i]], {"ms": 0.0, "launches": 0, "groups": set()})
+        d["ms"] += ms[i]
+        d["launches"] += 1
+        d["groups"].add(gg[i])
+        per_group_ms[gg[i]] += ms[i]
+    for name, d in per_kind.items():
+        d["cmacs"] = sum(work.get((gi, name), 0.0) for gi in d["groups"]) * c0
+    raw = [{"kind": KINDS[kk[i]], "group": int(gg[i]), "ms": float(ms[i])} for i in range(nl)]
+    return per_kind, per_group_ms, work, c0, raw
 
 
 def run_b200(args):
@@ -188,113 +315,38 @@ def run_b200(args):
     from paper_1104_0623_b200 import Mesh, SolverConfig, SparseOperator, solve_batch
     from paper_1104_0623_b200.configs import CONFIGS, config_problem
     from paper_1104_0623_b200.plan import plan_for
+    from paper_1104_0623_b200.solver import energy_chunk, sigma_symmetry
+    from paper_1104_0623_b200.workmodel import TENSOR_KINDS
 
     cfg = CONFIGS[args.config]
     p = config_problem(args.config)
     n_e = p.energies.size
+    t0 = time.perf_counter()
     plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
+    plan_s = time.perf_counter() - t0
     W = float(plan.native_work(0))
-    stream = torch.cuda.Stream(dev)
-    a_host = torch.from_numpy(p.a_vals_all()).pin_memory()
-    s_host = torch.from_numpy(p.s_vals).pin_memory()
-    a_d = a_host.to(dev)
-    s_d = s_host.to(dev)
-    gr_d = torch.empty((n_e, plan.n), dtype=torch.complex128, device=dev)
-    gl_d = torch.empty((n_e, plan.n), dtype=torch.complex128, device=dev)
-    ws = plan.workspace(n_e, True, dev)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    torch.cuda.synchronize()
-
-    from paper_1104_0623_b200.solver import sigma_symmetry
-
     ssym = sigma_symmetry(p.sigma_csr())
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    # inputs, outputs and the e2e leg's own buffers stay resident next to the workspace
+    chunk = energy_chunk(plan, n_e, True, dev)
+    reserve = (2 * n_e * plan.nnz + 4 * n_e * plan.n) * 16
+    while chunk > 1 and plan.workspace_bytes(chunk, True) + reserve > 0.85 * torch.cuda.mem_get_info(dev)[0]:
+        chunk -= 1
 
-    def step_eager():
-        plan.run(a_d, s_d, gr_d, gl_d, ws=ws, stream=stream, sigma_sym=ssym)
-
-    # the timed steps replay the solve's launch schedule as one captured CUDA graph (as the public
-    # API does from its second call, Plan.replay_or_run); the instrumented step below runs eagerly
-    graph = None
-
-    def step():
-        graph.replay() if graph is not None else step_eager()
-
-    with torch.cuda.stream(stream):
-        for _ in range(max(args.warmup, 3) - 1):
-            step_eager()
-        plan.check_status(ws, n_e, stream)
-        if os.environ.get("FIND_B200_GRAPH", "1") != "0":
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=stream):
-                step_eager()
-        step()  # last warm-up step (the graph's first replay)
-        plan.check_status(ws, n_e, stream)
-    # ---- timed region: K steps, L2 flushed between steps (outside the events) ----
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clocks = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    with torch.cuda.stream(stream):
-        for k in range(args.steps):
-            flush.fill_(k & 0xff)
-            evs[k][0].record(stream)
-            step()
-            evs[k][1].record(stream)
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    if world > 1:
-        dist.barrier()
-    plan.check_status(ws, n_e, stream)
-    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
-    t_max = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    dev_ms = float(t_max.item())
+    m = device_measure(plan, p, dev, args.steps, args.warmup, world, chunk, ssym, flush)
+    dev_ms = m["dev_ms"]
     ms_per_step = dev_ms / args.steps
     value = world * n_e * args.steps / (dev_ms * 1e-3)
+    step_ms, clocks, graphed = m["step_ms"], m["clocks"], m["graph"]
+    m["graph_obj"] = None
 
-    # ---- per-launch timing: one extra instrumented step with every launch group run ALONE
-    #      (groups in plan order on the solve stream, so each launch's CUDA-event duration is
-    #      its own, not shared with concurrent groups) -> per-kind roofline, live
-    import ctypes as C
-
-    from paper_1104_0623_b200 import _native
-    from paper_1104_0623_b200.workmodel import KINDS, TENSOR_KINDS, executed_cmacs
-
-    lib = _native.lib()
-    ngroups = len(plan.groups["count"])
-    with torch.cuda.stream(stream):
-        flush.fill_(1)
-        torch.cuda.synchronize()
-        lib.find_solve_timing_enable(1)
-        for gi in range(ngroups):
-            plan.run(a_d, s_d, gr_d, gl_d, ws=ws, stream=stream, sigma_sym=ssym, groups=(gi, gi + 1))
-        torch.cuda.synchronize()
-        lib.find_solve_timing_enable(0)
-    nl = int(lib.find_solve_timing_read(None, None, None, 0))
-    kk = (C.c_int32 * nl)()
-    gg = (C.c_int32 * nl)()
-    ms = (C.c_float * nl)()
-    lib.find_solve_timing_read(kk, gg, ms, nl)
-    work = executed_cmacs(plan, ssym)
-    per_kind = {}
-    per_group_ms = np.zeros(ngroups)
-    for i in range(nl):
-        name = KINDS[kk[i]]
-        d = per_kind.setdefault(name, {"ms": 0.0, "launches": 0, "cmacs": 0.0, "groups": set()})
-        d["ms"] += ms[i]
-        d["launches"] += 1
-        d["groups"].add(gg[i])
-        per_group_ms[gg[i]] += ms[i]
-    for name, d in per_kind.items():
-        d["cmacs"] = sum(work.get((gi, name), 0.0) for gi in d["groups"]) * n_e
+    # ---- serialized per-kind roofline ----
+    per_kind, per_group_ms, work, c0, raw = serialized_kinds(plan, m, n_e, chunk, ssym, flush)
     tot_ms = sum(d["ms"] for d in per_kind.values())
 
     def kind_line(d):
         tf = 8 * d["cmacs"] / (d["ms"] * 1e-3) / 1e12 if d["cmacs"] and d["ms"] else None
-        return {"ms_per_step_serialized": round(d["ms"], 3), "share": round(d["ms"] / tot_ms, 4),
+        return {"ms_per_call_serialized": round(d["ms"], 3), "share": round(d["ms"] / tot_ms, 4),
                 "launches": d["launches"], "tflops": round(tf, 3) if tf else None,
                 "frac_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4) if tf else None}
 
@@ -303,43 +355,44 @@ def run_b200(args):
     dk = per_kind[dom]
     achieved = 8 * dk["cmacs"] / (dk["ms"] * 1e-3) / 1e12
     traffic = None
-    prof = ROOT / "profiles" / "r01_ncu_kernels.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get(f"{dom}_kernel", {}).get("dram_bytes_per_launch")
+    if NCU_KERNELS.exists():
+        rec = json.loads(NCU_KERNELS.read_text()).get(f"{dom}_kernel", {})
+        traffic = rec.get("dram_bytes_per_launch")
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-        "kernel": f"{dom}_kernel", "launches_per_step": dk["launches"], "share_of_step": dk["ms"] / tot_ms,
+        "kernel": f"{dom}_kernel", "launches_per_call": dk["launches"], "share_of_step": dk["ms"] / tot_ms,
         "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_fp64_probe.txt); cuBLAS ZGEMM 37.02",
-        "work": "executed complex MACs x 8 of those launches (paper_1104_0623_b200/workmodel.py) / their CUDA-event "
-                "durations with each launch group run alone (serialized instrumented step); dominant = the FP64 "
-                "tensor-core (DMMA) kind with the largest serialized device time; traffic = ncu dram bytes per launch "
-                "of that kernel (profiles/r01_ncu_kernels.json)",
+        "work": (f"executed complex MACs x 8 of those launches (paper_1104_0623_b200/workmodel.py) / their CUDA-event "
+                 f"durations, every launch group run alone on the solve stream (one serialized find_solve call of "
+                 f"{c0} energy points); dominant = the FP64 tensor-core (DMMA) kind with the largest serialized "
+                 f"time; traffic = ncu --set full dram bytes per launch of that kernel ({NCU_KERNELS.name})"),
     }
-    # north-star target: FP64 fraction on the near-root levels (upward levels 1-4, downward 1-4)
     g = plan.groups
+    ngroups = len(g["count"])
     wl = {}
-    for (gi, kname), v in work.items():
+    for (gi, _), v in work.items():
         wl[gi] = wl.get(gi, 0.0) + v
     near = [gi for gi in range(ngroups) if int(g["level"][gi]) <= 4 and int(g["pass"][gi]) in (0, 1)]
     near_ms = float(per_group_ms[near].sum())
-    near_tf = 8 * sum(wl.get(gi, 0.0) for gi in near) * n_e / (near_ms * 1e-3) / 1e12 if near_ms else 0.0
+    near_tf = 8 * sum(wl.get(gi, 0.0) for gi in near) * c0 / (near_ms * 1e-3) / 1e12 if near_ms else 0.0
     near_root = {"levels": "upward 1-4 + downward 1-4", "groups": len(near), "ms_serialized": round(near_ms, 3),
                  "tflops": round(near_tf, 3), "frac_fp64_peak": round(near_tf / FP64_PEAK_TFLOPS, 4)}
     if args.levels and rank == 0:
-        Path(args.levels).write_text(json.dumps({"kernels": kernels, "launches": [
-            {"kind": KINDS[kk[i]], "group": int(gg[i]), "ms": float(ms[i])} for i in range(nl)]}, indent=1))
+        Path(args.levels).write_text(json.dumps({"kernels": kernels, "launches": raw}, indent=1))
+    del m
+    torch.cuda.empty_cache()
 
     # ---- e2e through the public API (host SparseOperators -> diagonals on host) ----
     mesh = Mesh(p.nx, p.ny)
     ops = [SparseOperator(p.a_csr(k)) for k in range(n_e)]
     sig = SparseOperator(p.sigma_csr())
     conf = SolverConfig()
-    # 20 calls, median: the host side sees sporadic 30-100 ms stalls from the box (bursts of a
-    # few calls, with or without Python's GC) while the device time per call stays flat
-    e2e_steps = 20
-    per_step = []
-    parts = []
+    # several calls, median: the host side sees sporadic 30-100 ms stalls from the box while the
+    # device time per call stays flat; heavy configs use fewer calls (bounded bench time)
+    e2e_steps = args.e2e_steps or (args.steps if ms_per_step < 1000 else max(3, min(args.steps, int(60e3 / ms_per_step))))
+    per_step, parts = [], []
+    stream = plan.solve_stream(dev)
     with torch.cuda.stream(stream):
         solve_batch(mesh, ops, sig, conf)  # eager
         solve_batch(mesh, ops, sig, conf)  # captures the level schedule as CUDA graphs
@@ -358,47 +411,66 @@ def run_b200(args):
         dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
     e2e_s = float(t_e.item())
     e2e = {"value": world * n_e / e2e_s, "unit": UNIT, "steps": e2e_steps,
-           "timing": "host wall clock per solve_batch call, median over the steps (max over ranks)",
+           "timing": "host wall clock per solve_batch call, median over the calls (max over ranks)",
            "median_host_prepare_ms": round(1e3 * float(np.median([x[0] for x in parts])), 3),
            "median_device_ms": round(1e3 * float(np.median([x[1] for x in parts])), 3),
            "median_call_ms": round(1e3 * float(np.median([x[2] for x in parts])), 3),
            "call_ms": [round(1e3 * x, 2) for x in per_step],
-           "device_ms": [round(1e3 * x[1], 2) for x in parts],
            "h2d_bytes_per_step": int(n_e * plan.nnz * 16 + plan.nnz * 16),
            "d2h_bytes_per_step": int(2 * n_e * plan.n * 16),
-           "api": "paper_1104_0623_b200.solve_batch(mesh, [SparseOperator]*16, Sigma, SolverConfig())"}
+           "api": f"paper_1104_0623_b200.solve_batch(mesh, [SparseOperator]*{n_e}, Sigma, SolverConfig())"}
+    del ops, res
 
     flops_total = 8.0 * W * n_e * world * args.steps / (dev_ms * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"cfg{args.config}: {cfg.nx}x{cfg.ny} {cfg.stencil}-point stencil + dense contacts, "
-                               f"{n_e} energy points per GPU, diag G^r + G^<",
-                   "mesh": [cfg.nx, cfg.ny], "n_energies_per_gpu": n_e, "stencil": cfg.stencil,
-                   "parallelism": f"replicas{world} (energy sharding)" if world > 1 else "single GPU",
-                   "l2": "flushed (256 MiB write) between timed steps, outside the timed events",
-                   "launch": ("CUDA graph replay of the solve's launch schedule" if graph is not None
-                              else "direct launches")},
+        "config": config_dict(cfg, world),
+        "launch": (("CUDA graph replay of the solve's launch schedule" if graphed else "direct launches") +
+                   f", {-(-n_e // chunk)} find_solve call(s) of <= {chunk} energy points per step"),
+        "step_ms": [round(x, 3) for x in step_ms],
         "fp64_tflops": flops_total, "fp64_frac_of_peak": flops_total / FP64_PEAK_TFLOPS,
         "work_per_energy_mults": W,
         "roofline": roofline,
         "near_root": near_root,
         "kernels": kernels,
         "e2e": e2e,
-        "gpu_launches": int(plan.launch_count(n_e) * args.steps),
-        "clocks": clk,
+        "gpu_launches": int(plan.launch_count(chunk) * -(-n_e // chunk) * args.steps),
+        "plan_build_seconds": round(plan_s, 2),
     }
+    line["clocks"] = clocks
+    if not args.no_extra and args.config != 1:
+        line["cfg1"] = side_config(1, dev, world, flush)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_line(args.config, config_problem(args.config, 1))
+        line["cpu_baseline"] = cpu_baseline_line(args.config)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def side_config(index, dev, world, flush, steps=20):
+    """Device throughput of another BASELINE config (same timing rules), reported beside the headline."""
+    from paper_1104_0623_b200.configs import config_problem
+    from paper_1104_0623_b200.plan import plan_for
+    from paper_1104_0623_b200.solver import energy_chunk, sigma_symmetry
+
+    p = config_problem(index)
+    plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
+    n_e = p.energies.size
+    chunk = energy_chunk(plan, n_e, True, dev)
+    m = device_measure(plan, p, dev, steps, 3, world, chunk, sigma_symmetry(p.sigma_csr()), flush)
+    v = world * n_e * steps / (m["dev_ms"] * 1e-3)
+    W = float(plan.native_work(0))
+    return {"workload": f"cfg{index}: {p.nx}x{p.ny}, {n_e} energy points", "value": v, "unit": UNIT,
+            "steps": steps, "ms_per_step": m["dev_ms"] / steps,
+            "fp64_tflops": 8 * W * n_e * world * steps / (m["dev_ms"] * 1e-3) / 1e12}
+
+
 def main():
     args = parse()
+    self_launch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -83,6 +83,16 @@ int find_plan_elims(const find_plan* plan, int32_t* kind, int32_t* s, int32_t* b
  * the products with Y(B_r, S_l) = 0); otherwise both 0.  Any pointer may be NULL. */
 int find_plan_elim_splits(const find_plan* plan, int32_t* s_left, int32_t* b_left);
 
+/* Per elimination (find_plan_elims order): the arena (-1: none) and complex-element offset of
+ * its output block pair U [b][b], R [b][b] (sorted-B order; R at +b*b) within one energy
+ * point's slice of that arena; the arenas follow the 256-byte status header of the workspace in
+ * order, arena a holding n_energies * arena_elems[a] complex elements (find_plan_arena_elems). */
+int find_plan_elim_out(const find_plan* plan, int32_t* out_arena, int64_t* out_off);
+
+/* Complex elements per energy point of each of the four block arenas (0: upward U/R blocks,
+ * 1-3: downward complement blocks). */
+int find_plan_arena_elems(const find_plan* plan, int64_t* out4);
+
 /* CSR slots of the merge-structure exception entries (kernels.py:192-202,
  * counted into SelectedInverse.stats at solver.py:217-219) for pass 0
  * (upward merges) or 1 (downward merges); an entry counts when its value is

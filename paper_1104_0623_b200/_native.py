@@ -25,7 +25,8 @@ EXPORTED = (
     "find_solve_groups", "find_plan_groups", "find_solve_status", "find_solve_launch_count",
     "find_schur_sigma_update", "find_plan_exception_slots", "find_plan_specs", "find_solve_timing_enable",
     "find_solve_timing_read", "find_plan_group_phases", "find_solve_timing_read2", "find_plan_offdiag_pairs",
-    "find_solve_offdiag", "find_solve_offdiag_groups", "find_plan_elim_splits",
+    "find_solve_offdiag", "find_solve_offdiag_groups", "find_plan_elim_splits", "find_plan_elim_out",
+    "find_plan_arena_elems",
 )
 
 
@@ -74,6 +75,8 @@ def lib():
         "find_solve_groups": (i32, [P, P, P, i32, i32, i32, dbl, P, P, P, sz, i64, i64, P, st]),
         "find_plan_offdiag_pairs": (i64, [P, pi64, pi64, i64]),
         "find_plan_elim_splits": (i32, [P, pi32, pi32]),
+        "find_plan_elim_out": (i32, [P, pi32, pi64]),
+        "find_plan_arena_elems": (i32, [P, pi64]),
         "find_solve_offdiag": (i32, [P, P, P, i32, i32, i32, dbl, P, P, P, P, P, sz, P, st]),
         "find_solve_offdiag_groups": (i32, [P, P, P, i32, i32, i32, dbl, P, P, P, P, P, sz, i64, i64, P, st]),
         "find_plan_groups": (i32, [P, pi32, pi32, pi32, pi64, pi32, pi32, pi32]),

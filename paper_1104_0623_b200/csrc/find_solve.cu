@@ -27,6 +27,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <vector>
 
@@ -2574,9 +2575,18 @@ size_t trsm_smem() {
                   (size_t)3 * NB * (NB + 1) * sizeof(double2));
 }
 
+// The dynamic shared-memory opt-ins are per device: tracked per device index (a process may drive
+// several GPUs, one host thread each).
+constexpr int kMaxDevices = 64;
+bool g_attrs_done[kMaxDevices] = {};
+std::mutex g_attrs_mu;
+
 int set_attrs(find_status* st) {
-  static bool done = false;
-  if (done) return FIND_OK;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail_status(st, FIND_EINVAL, "device index out of range");
+  std::lock_guard<std::mutex> lk(g_attrs_mu);
+  if (g_attrs_done[dev]) return FIND_OK;
   const int mx = (int)kMaxSmem;
   CUDA_TRY(cudaFuncSetAttribute(small_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(mid_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -2614,7 +2624,7 @@ int set_attrs(find_status* st) {
                                 (int)offdiag_small_smem<32>()));
   CUDA_TRY(cudaFuncSetAttribute(offdiag_small_kernel<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)offdiag_small_smem<64>()));
-  done = true;
+  g_attrs_done[dev] = true;
   return FIND_OK;
 }
 
@@ -2632,11 +2642,11 @@ struct SideStreams {
   cudaStream_t joiner = nullptr;     // dependency scheduling: per-phase join events are recorded here
   std::vector<cudaEvent_t> gev, jev;  // per launch group / per phase completion
 };
-SideStreams g_side;
+// one set per device; g_side_mu[dev] is held while a solve enqueues on that device's side streams
+SideStreams g_sides[kMaxDevices];
+std::mutex g_side_mu[kMaxDevices];
 
-int side_init(find_status* st) {
-  int dev = 0;
-  CUDA_TRY(cudaGetDevice(&dev));
+int side_init(SideStreams& g_side, int dev, find_status* st) {
   if (g_side.device == dev) return FIND_OK;
   int least = 0, greatest = 0;
   CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -2754,7 +2764,7 @@ int grow_events(std::vector<cudaEvent_t>& v, size_t n, find_status* st) {
 }
 
 int run_groups_dag(const find_plan* P, const SolveParams& prm, int64_t g_begin, int64_t g_end, int nE,
-                   cudaStream_t stream, find_status* st) {
+                   cudaStream_t stream, SideStreams& g_side, find_status* st) {
   const int np = P->groups.back().phase + 1;
   int rc = grow_events(g_side.gev, P->groups.size(), st);
   if (!rc) rc = grow_events(g_side.jev, (size_t)np, st);
@@ -2799,8 +2809,12 @@ int run_groups(const find_plan* P, const SolveParams& prm, int64_t g_begin, int6
                cudaStream_t stream, find_status* st) {
   int rc = set_attrs(st);
   if (rc) return rc;
-  if ((rc = side_init(st))) return rc;
-  if (P->dag && g_dag && g_end > g_begin) return run_groups_dag(P, prm, g_begin, g_end, nE, stream, st);
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_side_mu[dev]);
+  SideStreams& g_side = g_sides[dev];
+  if ((rc = side_init(g_side, dev, st))) return rc;
+  if (P->dag && g_dag && g_end > g_begin) return run_groups_dag(P, prm, g_begin, g_end, nE, stream, g_side, st);
   int64_t gi = g_begin;
   while (gi < g_end) {
     int64_t ge = gi;
@@ -2856,6 +2870,11 @@ const int g_skip = [] {
   return std::string(f) == "tall" ? 1 : (std::string(f) == "other" ? 2 : 0);
 }();
 
+const bool g_rsym_down = [] {
+  const char* f = std::getenv("FIND_B200_RSYM_DOWN");
+  return f && f[0] == '1';
+}();
+
 int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int nE, cudaStream_t stream,
                   find_status* st) {
   const Task* dtasks = (const Task*)P->d_tasks;
@@ -2870,12 +2889,12 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
     // level after level (2.3e-3 relative at 256x1024, tools/bisect_gl.py), while
     // the upward pass agrees to roundoff.
     SolveParams prm = prm_in;
-    if (G.pass != 0) prm.rsym = 0;
+    if (G.pass != 0 && !g_rsym_down) prm.rsym = 0;
     if (G.path == 1 && G.nb == 0) return fail_status(st, FIND_EINVAL, "elimination block too large for this build");
     const bool fused = use_fused(G, nE);
     for (int64_t si = fused ? G.fspec_begin : G.spec_begin; si < (fused ? G.fspec_end : G.spec_end); ++si) {
       const LaunchSpec& L = P->specs[si];
-      if (!prm.compute_gless && (L.kind == kLGatherS || L.kind == kLTGemm)) continue;
+      if (!prm.compute_gless && (L.kind == kLGatherS || L.kind == kLTGemm || L.kind == kLRGemm)) continue;
       if (L.kind == kLPanelInv && !g_inv_launch) continue;
       // sigma comes from the last panel's inverse launch; the finish launch remains for the
       // unit-test shim's L output (and when the inverse launches are off)

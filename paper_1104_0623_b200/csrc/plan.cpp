@@ -923,6 +923,21 @@ int find_plan_elim_splits(const find_plan* P, int32_t* s_left, int32_t* b_left) 
   return FIND_OK;
 }
 
+int find_plan_arena_elems(const find_plan* P, int64_t* out4) {
+  if (!P || !out4) return FIND_EINVAL;
+  for (int a = 0; a < kNumArenas; ++a) out4[a] = P->arena_elems[a];
+  return FIND_OK;
+}
+
+int find_plan_elim_out(const find_plan* P, int32_t* out_arena, int64_t* out_off) {
+  if (!P) return FIND_EINVAL;
+  for (size_t k = 0; k < P->elims.size(); ++k) {
+    if (out_arena) out_arena[k] = P->elims[k].out_arena;
+    if (out_off) out_off[k] = P->elims[k].out_off;
+  }
+  return FIND_OK;
+}
+
 int64_t find_plan_exception_slots(const find_plan* P, int32_t pass, int64_t* out, int64_t cap) {
   if (!P || pass < 0 || pass > 1) return -1;
   const auto& v = P->exc_slots[pass];

@@ -50,11 +50,17 @@ def solve_batch_sharded(mesh, a_list, sigma, config, group=None, local_solver=No
     if local_solver is None:
         from .solver import solve_batch as local_solver
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if not a_list:
+        raise ValueError("a_list is empty")  # every rank sees the same list: all raise, none blocks
     sl = energy_shard(len(a_list), rank, world)
     n = mesh.n
-    res = local_solver(mesh, a_list[sl], sigma, config)
-    gr = _gather_rows(np.asarray(res.gr_diag).reshape(-1, n), len(a_list), n, group)
-    gl = None
-    if config.compute_gless:
-        gl = _gather_rows(np.asarray(res.gless_diag).reshape(-1, n), len(a_list), n, group)
+    if sl.stop > sl.start:
+        res = local_solver(mesh, a_list[sl], sigma, config)
+        gr_l = np.asarray(res.gr_diag).reshape(-1, n)
+        gl_l = np.asarray(res.gless_diag).reshape(-1, n) if config.compute_gless else None
+    else:  # more ranks than energy points: this rank only joins the gathers
+        gr_l = np.zeros((0, n), np.complex128)
+        gl_l = np.zeros((0, n), np.complex128)
+    gr = _gather_rows(gr_l, len(a_list), n, group)
+    gl = _gather_rows(gl_l, len(a_list), n, group) if config.compute_gless else None
     return gr, gl

@@ -13,7 +13,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import scipy.sparse as sp
 
-from .errors import NativeLibraryError
+from .errors import NativeLibraryError, StructureMismatchError
 from .ledger import BLOCK_KERNELS, HERMITIAN_KERNELS, KERNEL_NAMES, FlopLedger
 from .operators import check_pattern_subset, check_structural_symmetry, is_hermitian
 from .plan import Plan, plan_for, same_array
@@ -195,6 +195,34 @@ def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+MAX_ENERGIES_PER_LAUNCH = 0xFFFF  # grid.y carries the energy index (find_solve rejects more)
+
+
+def balanced_chunk(n_e: int, fit: int) -> int:
+    """Energy points per find_solve call: at most ``fit`` (what the device memory holds) and
+    MAX_ENERGIES_PER_LAUNCH, balanced over the calls (8 points at <= 7 per call -> 4 + 4)."""
+    chunk = max(1, min(n_e, int(fit), MAX_ENERGIES_PER_LAUNCH))
+    return -(-n_e // -(-n_e // chunk))
+
+
+def energy_chunk(plan: Plan, n_e: int, compute_gless: bool, dev, n_pairs: int = 0) -> int:
+    """Energy points per find_solve call that fit in 85 % of the free device memory (the plan's
+    own cached workspace counts as free), inputs / outputs included."""
+    import torch
+
+    per_energy = plan.workspace_bytes(2, compute_gless) - plan.workspace_bytes(1, compute_gless)
+    per_energy += (plan.nnz + 2 * plan.n) * 16 + 2 * n_pairs * 16
+    free, total = torch.cuda.mem_get_info(dev)
+    held = plan._ws.numel() if plan._ws is not None and plan._ws.device == dev else 0
+    if free + held < 0.5 * total:  # other plans' cached workspaces crowd this solve out
+        from .plan import release_workspaces
+
+        release_workspaces(keep=plan)
+        free, total = torch.cuda.mem_get_info(dev)
+    fit = (0.85 * (free + held) - plan.workspace_bytes(1, compute_gless) + per_energy) // per_energy
+    return balanced_chunk(n_e, fit)
+
+
 def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, compute_gless=True, pivot_rtol=1e-12,
                  sigma_sym=0, max_chunk: int | None = None, compute_offdiag=False, offdiag_out: dict | None = None,
                  host_work=None):
@@ -216,21 +244,10 @@ def solve_values(plan: Plan, a_vals: np.ndarray, s_vals: np.ndarray | None, comp
     if compute_gless:
         s_vals = np.ascontiguousarray(s_vals, dtype=np.complex128)
         s_b = s_vals.ndim == 1
-    per_energy = plan.workspace_bytes(2, compute_gless) - plan.workspace_bytes(1, compute_gless)
-    per_energy += (plan.nnz + 2 * plan.n) * 16
     n_pairs = plan.offdiag_pairs().shape[0] if compute_offdiag else 0
-    per_energy += 2 * n_pairs * 16
-    free, total = torch.cuda.mem_get_info(dev)
-    held = plan._ws.numel() if plan._ws is not None and plan._ws.device == dev else 0
-    if free + held < 0.5 * total:  # other plans' cached workspaces crowd this solve out
-        from .plan import release_workspaces
-
-        release_workspaces(keep=plan)
-        free, total = torch.cuda.mem_get_info(dev)
-    chunk = max(1, min(n_e, int((0.85 * (free + held) - plan.workspace_bytes(1, compute_gless) + per_energy) // per_energy)))
+    chunk = energy_chunk(plan, n_e, compute_gless, dev, n_pairs)
     if max_chunk:
-        chunk = min(chunk, max_chunk)
-    chunk = -(-n_e // -(-n_e // chunk))  # balanced chunks (8 points at <= 7 per chunk -> 4 + 4)
+        chunk = balanced_chunk(n_e, min(chunk, max_chunk))
     # the plan's own (non-default) stream, ordered after the caller's current stream; every chunk
     # ends with a host synchronisation, so the caller's stream needs no wait afterwards
     stream = plan.solve_stream(dev)
@@ -412,6 +429,17 @@ def _prepare(mesh, a_list, sigma, config):
     return plan, am0, vals, s_vals, ssym, sherm
 
 
+def _debug_checks(config, stats: dict) -> None:
+    """debug_checks (solver.py:136, 156): the structured kernels refuse upward merges whose
+    inputs violate the merge sparsity structure (kernels.py:350-355 _check_strict)."""
+    if not config.debug_checks:
+        return
+    if config.kernel in BLOCK_KERNELS or config.kernel == "symmetric_sparse":
+        bad = int(stats.get("upward_exception_entries", 0))
+        if bad:
+            raise StructureMismatchError(f"{bad} entries violate the merge sparsity structure")
+
+
 def solve(mesh, a, sigma, config: SolverConfig) -> SelectedInverse:
     """Run the full selected inversion on one operator (solver.py:586-701)."""
     t0 = time.perf_counter()
@@ -422,6 +450,7 @@ def solve(mesh, a, sigma, config: SolverConfig) -> SelectedInverse:
     gr, gl, t_up, t_down = solve_values(plan, vals, s_vals, config.compute_gless, config.pivot_rtol, ssym,
                                         compute_offdiag=config.compute_offdiag, offdiag_out=off,
                                         host_work=lambda: side.update(stats=_stats(plan, am.data)))
+    _debug_checks(config, side["stats"])
     led = _ledger_cached(plan, config, sherm)
     offd = offl = None
     if config.compute_offdiag:
@@ -453,6 +482,7 @@ def solve_batch(mesh, a_list, sigma, config: SolverConfig) -> SelectedInverseBat
                                         compute_offdiag=config.compute_offdiag, offdiag_out=off,
                                         host_work=lambda: side.update(stats=_stats(plan, am0.data),
                                                                       ledger=_ledger_cached(plan, config, sherm)))
+    _debug_checks(config, side["stats"])
     t3 = time.perf_counter()
     res = SelectedInverseBatch(gr, gl, side["ledger"],
                                {"tree": t1 - t0, "upward": t_up, "downward_extract": t_down, "total": t3 - t0},

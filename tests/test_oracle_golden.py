@@ -43,23 +43,45 @@ def test_oracle_matches_dense_small():
 
 
 def test_cpu_baseline_estimator_runs():
-    """bench.py's cpu_baseline / --impl reference leg (oracle/cpu_baseline.py) on a tiny mesh."""
-    from oracle.cpu_baseline import estimate_seconds_per_energy
+    """bench.py's cpu_baseline / --impl reference leg (oracle/cpu_baseline.py) on a tiny mesh: every
+    elimination is in exactly one bucket, one member per bucket is timed."""
+    from oracle.cpu_baseline import buckets_of, elimination_jobs, estimate_step
     from oracle.find_oracle import FindOracle
     from paper_1104_0623_b200.configs import build_problem
 
     p = build_problem(12, 10, [1.0], seed=2)
     o = FindOracle(p.nx, p.ny, p.a_csr(0))
-    r = estimate_seconds_per_energy(o, p.a_csr(0), p.sigma_csr(), fraction=0.5, seed=0)
-    assert r["seconds_per_energy"] > 0 and r["sampled_eliminations"] > 0
+    jobs = elimination_jobs(o)
+    b = buckets_of(jobs)
+    assert sum(len(v) for v in b.values()) == len(jobs)
+    r = estimate_step(o, b, p.a_csr(0).tocsr(), p.sigma_csr().tocsr(), np.random.default_rng(0))
+    assert r["seconds_per_energy"] > 0 and r["sampled_eliminations"] == len(b)
+    # with every member below the cap the estimate is the timed part alone
+    assert r["rate_part_seconds"] == 0.0
 
 
-def test_cpu_baseline_energy_parallel_runs():
-    """The energy-parallel CPU baseline (one process per core, one BLAS thread each) on a tiny mesh."""
-    from oracle.cpu_baseline import parallel_energy_rate
+def test_cpu_baseline_rate_part():
+    """Members above the cap are charged at the measured BLAS rate."""
+    from oracle.cpu_baseline import buckets_of, elimination_jobs, estimate_step
+    from oracle.find_oracle import FindOracle
     from paper_1104_0623_b200.configs import build_problem
 
     p = build_problem(12, 10, [1.0], seed=2)
-    r = parallel_energy_rate(p.nx, p.ny, p.a_csr(0).tocsr(), p.sigma_csr().tocsr(), workers=2, fraction=0.5)
-    assert r["workers"] == 2 and r["rate"] > 0 and r["sampled_eliminations"] > 0
-    assert abs(r["rate"] - 2.0 / r["seconds_per_energy"]) < 0.5 * r["rate"]
+    o = FindOracle(p.nx, p.ny, p.a_csr(0))
+    b = buckets_of(elimination_jobs(o))
+    wmax = max(j[4] for v in b.values() for j in v)
+    r = estimate_step(o, b, p.a_csr(0).tocsr(), p.sigma_csr().tocsr(), np.random.default_rng(0), cap=wmax / 2)
+    assert r["rate_part_seconds"] > 0 and r["blas_rate_cmults_per_s"] > 0
+
+
+def test_cpu_baseline_energy_parallel_runs():
+    """The energy-parallel CPU baseline (forked processes, one BLAS thread each) on a tiny mesh."""
+    from oracle.cpu_baseline import energy_parallel
+    from paper_1104_0623_b200.configs import build_problem
+
+    p = build_problem(12, 10, [1.0, 2.0], seed=2)
+    r = energy_parallel(0, steps=2, warmup=1, workers=2, problem=p)
+    assert r["workers"] == 2 and len(r["steps"]) == 2
+    for st in r["steps"]:
+        assert st["rate"] > 0 and st["sampled"] > 0
+        assert abs(st["rate"] - 2.0 / st["seconds_per_energy"]) < 0.5 * st["rate"]

@@ -1,0 +1,193 @@
+// Standalone benchmark of the TMA-fed DMMA tile engine (paper_1104_0623_b200/csrc/dmma_engine.cuh)
+// on the FIND launch shapes: batched complex C -= A op(B), persistent CTAs over the tiles.
+// Correctness against a naive FP64 kernel; cuBLAS ZGEMM (strided batched) as the ceiling.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -I paper_1104_0623_b200/csrc \
+//        tools/dmma_bench.cu -lcublas -o tools/dmma_bench && tools/dmma_bench
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "dmma_engine.cuh"
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e = (x);                                                             \
+    if (e != cudaSuccess) {                                                          \
+      std::printf("%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e)); \
+      std::exit(1);                                                                  \
+    }                                                                                \
+  } while (0)
+
+struct Prob {
+  int batch, M, N, K, nseg, bt2;  // segment 2 (if nseg == 2): conj-transposed B of shape [N][K]
+};
+
+template <class E>
+__global__ void __launch_bounds__(E::THREADS, 1) eng_kernel(Prob p, const double2* A, const double2* B,
+                                                            const double2* A2, const double2* B2, double2* C) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  E eng;
+  eng.init(smem_raw);
+  const int tm = (p.M + E::BM - 1) / E::BM, tn = (p.N + E::BN - 1) / E::BN;
+  const int ntiles = p.batch * tm * tn;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int bi = t / (tm * tn), r = t % (tm * tn);
+    const int i0 = (r / tn) * E::BM, c0 = (r % tn) * E::BN;
+    const int mv = min(E::BM, p.M - i0), nv = min(E::BN, p.N - c0);
+    dmma::Seg seg[2];
+    seg[0] = {A + (int64_t)bi * p.M * p.K + (int64_t)i0 * p.K, B + (int64_t)bi * p.K * p.N + c0, p.K, p.N, p.K, 0};
+    seg[1] = {A2 + (int64_t)bi * p.M * p.K + (int64_t)i0 * p.K, B2 + (int64_t)bi * p.N * p.K + (int64_t)c0 * p.K, p.K,
+              p.K, p.K, 1};
+    double2* Cb = C + (int64_t)bi * p.M * p.N + (int64_t)i0 * p.N + c0;
+    if (E::producer()) {
+      eng.produce(seg, p.nseg, mv, nv);
+    } else {
+      eng.load_c(Cb, p.N, mv, nv);
+      eng.template consume<true>(seg, p.nseg, mv, nv);
+      eng.for_each([&](int r, int c, double2 v) {
+        if (r < mv && c < nv) Cb[(int64_t)r * p.N + c] = v;
+      });
+    }
+  }
+}
+
+__global__ void naive_kernel(Prob p, const double2* A, const double2* B, const double2* A2, const double2* B2,
+                             double2* C) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= (int64_t)p.batch * p.M * p.N) return;
+  const int bi = q / ((int64_t)p.M * p.N), r = (q / p.N) % p.M, c = q % p.N;
+  double2 acc = C[q];
+  for (int k = 0; k < p.K; ++k) {
+    const double2 a = A[(int64_t)bi * p.M * p.K + (int64_t)r * p.K + k], b = B[(int64_t)bi * p.K * p.N + (int64_t)k * p.N + c];
+    acc.x -= a.x * b.x - a.y * b.y;
+    acc.y -= a.x * b.y + a.y * b.x;
+  }
+  if (p.nseg == 2)
+    for (int k = 0; k < p.K; ++k) {
+      const double2 a = A2[(int64_t)bi * p.M * p.K + (int64_t)r * p.K + k],
+                    b0 = B2[(int64_t)bi * p.N * p.K + (int64_t)c * p.K + k];
+      const double2 b = make_double2(b0.x, -b0.y);
+      acc.x -= a.x * b.x - a.y * b.y;
+      acc.y -= a.x * b.y + a.y * b.x;
+    }
+  C[q] = acc;
+}
+
+template <class E>
+void run(const char* name, Prob p, int sms, bool check) {
+  const size_t na = (size_t)p.batch * p.M * p.K, nb = (size_t)p.batch * p.K * p.N, nc = (size_t)p.batch * p.M * p.N;
+  std::vector<double2> h(std::max(std::max(na, nb), nc));
+  double2 *A, *B, *A2, *B2, *C, *C0, *Cr;
+  CK(cudaMalloc(&A, na * 16));
+  CK(cudaMalloc(&B, nb * 16));
+  CK(cudaMalloc(&A2, na * 16));
+  CK(cudaMalloc(&B2, nb * 16));
+  CK(cudaMalloc(&C, nc * 16));
+  CK(cudaMalloc(&C0, nc * 16));
+  CK(cudaMalloc(&Cr, nc * 16));
+  auto fill = [&](double2* d, size_t n, int seed) {
+    srand(seed);
+    for (size_t i = 0; i < n; ++i) h[i] = make_double2(rand() / (double)RAND_MAX - 0.5, rand() / (double)RAND_MAX - 0.5);
+    CK(cudaMemcpy(d, h.data(), n * 16, cudaMemcpyHostToDevice));
+  };
+  fill(A, na, 1);
+  fill(B, nb, 2);
+  fill(A2, na, 3);
+  fill(B2, nb, 4);
+  fill(C0, nc, 5);
+  CK(cudaFuncSetAttribute(eng_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E::SMEM));
+  const int tiles = p.batch * ((p.M + E::BM - 1) / E::BM) * ((p.N + E::BN - 1) / E::BN);
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eng_kernel<E>, E::THREADS, E::SMEM));
+  const int grid = std::min(tiles, sms * std::max(per_sm, 1));
+  if (check) {
+    CK(cudaMemcpy(C, C0, nc * 16, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(Cr, C0, nc * 16, cudaMemcpyDeviceToDevice));
+    eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, A, B, A2, B2, C);
+    CK(cudaGetLastError());
+    naive_kernel<<<(unsigned)((nc + 255) / 256), 256>>>(p, A, B, A2, B2, Cr);
+    CK(cudaDeviceSynchronize());
+    std::vector<double2> hc(nc), hr(nc);
+    CK(cudaMemcpy(hc.data(), C, nc * 16, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hr.data(), Cr, nc * 16, cudaMemcpyDeviceToHost));
+    double md = 0, mr = 0;
+    for (size_t i = 0; i < nc; ++i) {
+      md = std::max(md, std::hypot(hc[i].x - hr[i].x, hc[i].y - hr[i].y));
+      mr = std::max(mr, std::hypot(hr[i].x, hr[i].y));
+    }
+    std::printf("  check %s: max|d|/max|ref| = %.2e\n", name, md / mr);
+  }
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const int reps = 10;
+  eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, A, B, A2, B2, C);
+  CK(cudaEventRecord(e0));
+  for (int r = 0; r < reps; ++r) eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, A, B, A2, B2, C);
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  const double flops = 8.0 * p.batch * (double)p.M * p.N * p.K * p.nseg;
+  std::printf("%-28s BMxBN %3dx%-3d S=%d grid %5d (%d/SM) tiles %6d: %8.3f ms  %6.2f TFLOP/s\n", name, E::BM, E::BN, 0, grid,
+              per_sm, tiles, ms / reps, flops / (ms / reps * 1e-3) / 1e12);
+  // cuBLAS ceiling for the first segment
+  cublasHandle_t hd;
+  cublasCreate(&hd);
+  const cuDoubleComplex one = {1.0, 0.0}, mone = {-1.0, 0.0};
+  // row-major C[M][N] -= A[M][K] B[K][N]  ==  col-major C^T[N][M] -= B^T[N][K] A^T[K][M]
+  auto zg = [&]() {
+    cublasZgemmStridedBatched(hd, CUBLAS_OP_N, CUBLAS_OP_N, p.N, p.M, p.K, &mone, (const cuDoubleComplex*)B, p.N,
+                              (long long)p.K * p.N, (const cuDoubleComplex*)A, p.K, (long long)p.M * p.K, &one,
+                              (cuDoubleComplex*)C, p.N, (long long)p.M * p.N, p.batch);
+  };
+  zg();
+  CK(cudaEventRecord(e0));
+  for (int r = 0; r < reps; ++r) zg();
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  std::printf("%-28s cuBLAS ZGEMM (one segment)                   : %8.3f ms  %6.2f TFLOP/s\n", name, ms / reps,
+              8.0 * p.batch * (double)p.M * p.N * p.K / (ms / reps * 1e-3) / 1e12);
+  cublasDestroy(hd);
+  cudaFree(A);
+  cudaFree(B);
+  cudaFree(A2);
+  cudaFree(B2);
+  cudaFree(C);
+  cudaFree(C0);
+  cudaFree(Cr);
+}
+
+using E64x64s4 = dmma::Engine<2, 4, 4, 2, 4>;
+using E64x64s2 = dmma::Engine<2, 4, 4, 2, 2>;
+using E128x64s3 = dmma::Engine<4, 2, 4, 4, 3>;
+using E64x128s3 = dmma::Engine<2, 4, 4, 4, 3>;
+
+int main() {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  std::printf("SMs %d\n", sms);
+  const Prob trail{4, 3000, 3000, 64, 1, 0}, rgemm{4, 1535, 1535, 2045, 2, 1}, schur{4, 1535, 1535, 2045, 1, 0},
+      small{64, 256, 256, 256, 1, 0}, trail_small{64, 200, 200, 32, 1, 0};
+  run<E64x64s4>("trail 4x3000^2 K64", trail, sms, true);
+  run<E64x64s2>("trail 4x3000^2 K64", trail, sms, false);
+  run<E128x64s3>("trail 4x3000^2 K64", trail, sms, true);
+  run<E64x128s3>("trail 4x3000^2 K64", trail, sms, true);
+  run<E64x64s4>("rgemm 4x1535^2 K2045x2", rgemm, sms, true);
+  run<E128x64s3>("rgemm 4x1535^2 K2045x2", rgemm, sms, true);
+  run<E64x128s3>("rgemm 4x1535^2 K2045x2", rgemm, sms, false);
+  run<E64x64s4>("schur 4x1535^2 K2045", schur, sms, false);
+  run<E128x64s3>("schur 4x1535^2 K2045", schur, sms, false);
+  run<E64x64s4>("cfg1 64x256^2 K256", small, sms, true);
+  run<E64x64s2>("cfg1 64x256^2 K256", small, sms, false);
+  run<E128x64s3>("cfg1 64x256^2 K256", small, sms, false);
+  run<E64x64s4>("trail cfg1 64x200^2 K32", trail_small, sms, true);
+  run<E64x64s2>("trail cfg1 64x200^2 K32", trail_small, sms, false);
+  return 0;
+}
