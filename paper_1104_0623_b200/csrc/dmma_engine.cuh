@@ -1,32 +1,39 @@
 // TMA-fed FP64 tensor-core (DMMA) tile engine for sm_100a.
 //
-// One CTA computes BM x BN complex output tiles, acc (+/-)= A[M x K] op(B)[K x N], over a
-// sequence of product segments.  Operands are streamed global -> shared memory by the TMA
-// bulk-copy engine (cp.async.bulk ... mbarrier::complete_tx, SASS UBLKCP): one PRODUCER warp
-// issues one bulk copy per operand row of every K chunk into an S-stage ring of shared-memory
-// buffers guarded by full / empty mbarriers; the CONSUMER warps wait on the full barrier of a
-// stage, run the DMMA fragments (mma.sync m8n8k4 f64 -> DMMA.8x8x4; B200 has no tcgen05 f64
-// kind) and release the stage on its empty barrier.  The producer therefore runs up to S chunks
-// ahead, across tile boundaries of a persistent CTA (the next tile's operands arrive while the
-// consumers run the previous tile's epilogue).
+// One persistent CTA computes BM x BN complex output tiles, acc (+/-)= A[M x K] op(B)[K x N]
+// summed over up to two product segments.  One PRODUCER warp streams the operands global ->
+// shared memory with the TMA unit into an S-stage ring guarded by full / empty mbarriers; the
+// CONSUMER warps wait on a stage's full barrier, run the DMMA fragments (mma.sync m8n8k4 f64 ->
+// SASS DMMA.8x8x4: B200 has no tcgen05 f64 kind) and release the stage on its empty barrier.
+// The producer runs up to S chunks ahead, across tile boundaries (the next tile's operands and an
+// L2 prefetch of its C block arrive while the consumers run the previous tile's epilogue).
 //
-// Shared-memory layouts (padded rows; TMA writes each row at any 16-byte aligned address):
-//   A and conjugated B ("BT", given as B[n][k]): [rows][KC + 4] complex (row stride 320 B:
-//       the eight rows of a fragment start 64 B apart -> conflict-free 16-byte fragment loads)
-//   B given as B[k][n]: [KC][BN + 2] complex (row stride = 32 B mod 128 -> conflict-free)
-// Stale shared memory outside the valid rows / K range is never multiplied into a stored
-// output: fragments beyond the valid K are zeroed in registers (both operands), fragments of
-// rows / columns beyond the valid range only feed outputs that are not stored.
+//   A operand (rows x K, row-major complex) and a conjugated B given as B^T[n][k] ("bt"):
+//       cp.async.bulk.tensor.3d (SASS UTMALDG) from a per-matrix 3-D tensor map
+//       {2*cols doubles, rows, energy}, box {8 complex, 64 rows}, SWIZZLE_128B: two boxes per
+//       K chunk, each a [64][8] complex sub-tile with 128-byte rows whose 16-byte chunks are
+//       XOR-ed with (row & 7).
+//   B given as B[k][n] (rows of the scratch matrices): one cp.async.bulk (SASS UBLKCP) per k row
+//       (BN complex, 1 KB) into a padded [KC][BN + 1] layout (row stride = 16 B mod 128).
+//
+// Fragment rows / columns are permuted within each group of 8 by rho(x) = (x >> 1) | (x & 1) << 2
+// so that the eight lanes of a quarter warp hit eight distinct 16-byte bank groups in every
+// layout above (conflict-free 16-byte fragment loads); the accumulator's rows and columns carry
+// the same permutation, which load_c / for_each undo.
+// Shared memory outside the valid K range is never multiplied: fragments beyond the valid K are
+// zeroed in registers (both operands); rows / columns beyond the valid range (TMA zero-fills
+// outside the tensor, stale data inside it) only feed outputs that are not stored.
 #pragma once
 
 #include <cstdint>
 
 namespace dmma {
 
-constexpr int KC = 16;        // complex per K chunk
-constexpr int SKA = KC + 4;   // A / BT row stride (complex)
+constexpr int KC = 16;  // complex per K chunk (two 8-complex TMA boxes)
+constexpr int BOXR = 64;  // rows per TMA box (the tensor maps' box)
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ int rho(int x) { return (x >> 1) | ((x & 1) << 2); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
@@ -52,12 +59,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
         : "memory");
   } while (!ok);
 }
-// TMA bulk copy global -> this CTA's shared memory, completion counted on the mbarrier
+// TMA bulk copy global -> this CTA's shared memory (UBLKCP), completion counted on the mbarrier
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// TMA tensor tile load (UTMALDG): box at element coordinates {x, y, z} of a 3-D tensor map in global memory
+__device__ __forceinline__ void tensor_g2s(void* dst, const void* tmap, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tensor_prefetch_l2(const void* tmap, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(tmap), "r"(x), "r"(y), "r"(z)
+               : "memory");
 }
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
@@ -66,39 +85,43 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
       : "d"(a), "d"(b));
 }
 
-// One product segment: acc +/-= A op(B), A [Mv x K] row stride lda; op(B)[k][c] = B[k*ldb + c]
-// (bt = false) or conj(B[c*ldb + k]) (bt = true).
+// One product segment of a tile: acc +/-= A op(B) over K.
+//   A: rows [ar, ar + BM) x complex columns [ac, ac + K) of the matrix behind tensor map amap
+//   op(B)[k][c]: bt ? conj(B^T[bc_row + c][bk + k]) from tensor map bmap
+//                   : B[(k) * ldb + c] read from the pointer B (row k of the K range)
 struct Seg {
-  const double2* A;
+  const void* amap;
+  const void* bmap;
   const double2* B;
-  int64_t lda, ldb;
-  int K;
-  int bt;
+  int64_t ldb;
+  int ar, ac, br, bk;
+  int K, bt;
 };
 
-// WM x WN consumer warps, each MT x NT 8x8 fragments; S stages.
+// WM x WN consumer warps (8), each MT x NT 8x8 fragments; S stages.
 template <int WM, int WN, int MT, int NT, int S>
 struct Engine {
-  static constexpr int NW = WM * WN;              // consumer warps
-  static constexpr int THREADS = (NW + 1) * 32;   // + one producer warp
+  static constexpr int NW = WM * WN;
+  static constexpr int THREADS = (NW + 1) * 32;  // + one producer warp
   static constexpr int BM = WM * MT * 8, BN = WN * NT * 8;
-  static constexpr int SKB = BN + 2;              // B[k][n] row stride (complex)
-  static constexpr int A_ELEMS = BM * SKA;
-  static constexpr int B_ELEMS = (BN * SKA > KC * SKB) ? BN * SKA : KC * SKB;
-  static constexpr int STAGE = A_ELEMS + B_ELEMS;
-  static constexpr size_t SMEM = (size_t)S * STAGE * 16 + 2 * S * sizeof(uint64_t) + 16;
+  static_assert(BM == BOXR && BN == BOXR, "tiles are one TMA box tall and wide");
+  static constexpr int SKB = BN + 1;                   // B[k][n] row stride (complex): 16 B mod 128
+  static constexpr int A_BYTES = BM * KC * 16;         // two swizzled [BM][8] sub-tiles
+  static constexpr int B_BYTES_RAW = (BN * KC > KC * SKB ? BN * KC : KC * SKB) * 16;
+  static constexpr int B_BYTES = (B_BYTES_RAW + 1023) & ~1023;
+  static constexpr int STAGE = A_BYTES + B_BYTES;      // multiple of 1024 (swizzle-128B alignment)
+  static constexpr size_t SMEM = (size_t)S * STAGE + 1024 + 2 * S * sizeof(uint64_t);
 
-  double2* st;        // S stages
-  uint64_t* full;     // [S]
-  uint64_t* empty;    // [S]
-  unsigned pchunk;    // producer's running chunk counter
-  unsigned cchunk;    // consumer's running chunk counter
+  unsigned char* st;  // S stages, 1024-byte aligned
+  uint64_t* full;
+  uint64_t* empty;
+  unsigned chunk;  // running chunk counter (producer and consumers each keep their own copy)
 
   __device__ __forceinline__ void init(unsigned char* smem_raw) {
-    st = reinterpret_cast<double2*>(smem_raw);
-    full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)S * STAGE * 16);
+    st = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    full = reinterpret_cast<uint64_t*>(st + (size_t)S * STAGE);
     empty = full + S;
-    pchunk = cchunk = 0;
+    chunk = 0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < S; ++i) {
         mbar_init(&full[i], 1);
@@ -111,37 +134,55 @@ struct Engine {
 
   __device__ __forceinline__ static bool producer() { return threadIdx.x >= NW * 32; }
 
-  // ---- producer warp: stream every K chunk of the segments of one tile
-  __device__ __forceinline__ void produce(const Seg* seg, int nseg, int Mv, int Nv) {
+  // ---- producer warp: every K chunk of the segments of one tile (Nv: valid B columns)
+  __device__ __forceinline__ void produce(const Seg* seg, int nseg, int e, int Nv) {
     const int lane = threadIdx.x & 31;
-    const int mv = Mv < BM ? Mv : BM, nv = Nv < BN ? Nv : BN;
+    const int nv = Nv < BN ? Nv : BN;
+#pragma unroll 1
     for (int g = 0; g < nseg; ++g) {
       const Seg sg = seg[g];
+#pragma unroll 1
       for (int k0 = 0; k0 < sg.K; k0 += KC) {
         const int kv = (sg.K - k0) < KC ? (sg.K - k0) : KC;
-        const unsigned stage = pchunk % S, round = pchunk / S;
-        ++pchunk;
+        const unsigned stage = chunk % S, round = chunk / S;
+        ++chunk;
         mbar_wait(&empty[stage], (round & 1) ^ 1);
-        double2* As = st + (size_t)stage * STAGE;
-        double2* Bs = As + A_ELEMS;
-        const unsigned bytes = (unsigned)(mv * kv + (sg.bt ? nv * kv : kv * nv)) * 16u;
-        if (lane == 0) mbar_expect_tx(&full[stage], bytes);
-        __syncwarp();
-        for (int r = lane; r < mv; r += 32)
-          bulk_g2s(As + r * SKA, sg.A + (int64_t)r * sg.lda + k0, (unsigned)kv * 16u, &full[stage]);
-        if (sg.bt) {
-          for (int c = lane; c < nv; c += 32)
-            bulk_g2s(Bs + c * SKA, sg.B + (int64_t)c * sg.ldb + k0, (unsigned)kv * 16u, &full[stage]);
-        } else {
-          for (int k = lane; k < kv; k += 32)
-            bulk_g2s(Bs + k * SKB, sg.B + (int64_t)(k0 + k) * sg.ldb, (unsigned)nv * 16u, &full[stage]);
+        unsigned char* As = st + (size_t)stage * STAGE;
+        unsigned char* Bs = As + A_BYTES;
+        const int nbox = kv > 8 ? 2 : 1;  // 8-complex boxes the valid K range touches
+        const unsigned bytes = (unsigned)nbox * BOXR * 128u + (sg.bt ? (unsigned)nbox * BOXR * 128u : (unsigned)(kv * nv) * 16u);
+        if (lane == 0) {
+          mbar_expect_tx(&full[stage], bytes);
+          for (int h = 0; h < nbox; ++h) {
+            tensor_g2s(As + h * (BM * 128), sg.amap, 2 * (sg.ac + k0 + 8 * h), sg.ar, e, &full[stage]);
+            if (sg.bt) tensor_g2s(Bs + h * (BN * 128), sg.bmap, 2 * (sg.bk + k0 + 8 * h), sg.br, e, &full[stage]);
+          }
         }
+        __syncwarp();
+        if (!sg.bt)
+          for (int k = lane; k < kv; k += 32)
+            bulk_g2s(Bs + k * SKB * 16, sg.B + (int64_t)(k0 + k) * sg.ldb, (unsigned)nv * 16u, &full[stage]);
       }
     }
   }
 
+  // L2 prefetch of a C block [r0, r0 + 64) x [c0, c0 + 64) through its matrix's tensor map
+  __device__ __forceinline__ static void prefetch_c(const void* cmap, int r0, int c0, int e) {
+    const int lane = threadIdx.x & 31;
+    if (lane < 8) tensor_prefetch_l2(cmap, 2 * (c0 + 8 * lane), r0, e);
+  }
+
   // ---- consumer warps
   double acc[MT][NT][2][2];
+
+  __device__ __forceinline__ static int row_of(int mt, int fr) {
+    const int warp = threadIdx.x >> 5;
+    return (warp % WM) * MT * 8 + mt * 8 + rho(fr);
+  }
+  __device__ __forceinline__ static int col_of(int nt, int x) {
+    const int warp = threadIdx.x >> 5;
+    return (warp / WM) * NT * 8 + nt * 8 + rho(x);
+  }
 
   __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -152,8 +193,7 @@ struct Engine {
 
   // acc = C (this thread's elements of C[Mv x Nv], zero outside)
   __device__ __forceinline__ void load_c(const double2* C, int64_t ld, int Mv, int Nv) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = warp % WM, wn = warp / WM;
+    const int lane = threadIdx.x & 31;
     const int fr = lane >> 2, fc = lane & 3;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
@@ -161,50 +201,55 @@ struct Engine {
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          const int r = wm * MT * 8 + mt * 8 + fr, c = wn * NT * 8 + nt * 8 + 2 * fc + i;
+          const int r = row_of(mt, fr), c = col_of(nt, 2 * fc + i);
           const double2 v = (r < Mv && c < Nv) ? C[(int64_t)r * ld + c] : make_double2(0.0, 0.0);
           acc[mt][nt][0][i] = v.x;
           acc[mt][nt][1][i] = v.y;
         }
   }
 
-  // consume the chunks of the segments (same sequence as produce); NEG: acc -= A op(B)
+  // the chunks of the segments (same sequence as produce); NEG: acc -= A op(B)
   template <bool NEG>
   __device__ __forceinline__ void consume(const Seg* seg, int nseg, int Mv, int Nv) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = warp % WM, wn = warp / WM;
-    const int fr = lane >> 2, fc = lane & 3;
+    const int fr = lane >> 2, fc = lane & 3, rf = rho(fr);
     const int mtv = min(MT, max(0, (Mv - wm * MT * 8 + 7) / 8));
     const int ntv = min(NT, max(0, (Nv - wn * NT * 8 + 7) / 8));
+#pragma unroll 1
     for (int g = 0; g < nseg; ++g) {
       const int K = seg[g].K;
       const bool bt = seg[g].bt != 0;
+#pragma unroll 1
       for (int k0 = 0; k0 < K; k0 += KC) {
         const int kv = (K - k0) < KC ? (K - k0) : KC;
-        const unsigned stage = cchunk % S, round = cchunk / S;
-        ++cchunk;
+        const unsigned stage = chunk % S, round = chunk / S;
+        ++chunk;
         mbar_wait(&full[stage], round & 1);
-        const double2* As = st + (size_t)stage * STAGE;
-        const double2* Bs = As + A_ELEMS;
+        const unsigned char* As = st + (size_t)stage * STAGE;
+        const unsigned char* Bs = As + A_BYTES;
         if (mtv > 0 && ntv > 0) {
 #pragma unroll
           for (int kk = 0; kk < KC; kk += 4) {
             if (kk >= kv) break;
-            const bool kok = kk + fc < kv;
+            const int k = kk + fc;
+            const bool kok = k < kv;
+            // swizzled sub-tile offsets: row r (r & 7 == rf), 16-byte chunk (k & 7) ^ rf
+            const int soff = (k >> 3) * (BOXR * 128) + ((((k & 7) ^ rf)) << 4);
             double2 a[MT], b[NT];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-              a[mt] = As[(wm * MT * 8 + mt * 8 + fr) * SKA + kk + fc];
+              a[mt] = *reinterpret_cast<const double2*>(As + soff + (wm * MT * 8 + mt * 8 + rf) * 128);
               if (!kok) a[mt] = make_double2(0.0, 0.0);
             }
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-              const int col = wn * NT * 8 + nt * 8 + fr;
+              const int col = wn * NT * 8 + nt * 8 + rf;
               if (bt) {
-                b[nt] = Bs[col * SKA + kk + fc];
+                b[nt] = *reinterpret_cast<const double2*>(Bs + soff + col * 128);
                 b[nt].y = -b[nt].y;
               } else {
-                b[nt] = Bs[(kk + fc) * SKB + col];
+                b[nt] = *reinterpret_cast<const double2*>(Bs + (k * SKB + col) * 16);
               }
               if (!kok) b[nt] = make_double2(0.0, 0.0);
             }
@@ -216,8 +261,8 @@ struct Engine {
               for (int nt = 0; nt < NT; ++nt) {
                 if (nt >= ntv) break;
                 dmma884(acc[mt][nt][0][0], acc[mt][nt][0][1], ax, b[nt].x);
-                dmma884(acc[mt][nt][0][0], acc[mt][nt][0][1], nai, b[nt].y);
                 dmma884(acc[mt][nt][1][0], acc[mt][nt][1][1], ax, b[nt].y);
+                dmma884(acc[mt][nt][0][0], acc[mt][nt][0][1], nai, b[nt].y);
                 dmma884(acc[mt][nt][1][0], acc[mt][nt][1][1], ay, b[nt].x);
               }
             }
@@ -229,10 +274,10 @@ struct Engine {
     }
   }
 
+  // f(tile row, tile col, value) for this thread's accumulator elements
   template <class F>
   __device__ __forceinline__ void for_each(F f) const {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = warp % WM, wn = warp / WM;
+    const int lane = threadIdx.x & 31;
     const int fr = lane >> 2, fc = lane & 3;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
@@ -240,9 +285,10 @@ struct Engine {
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int i = 0; i < 2; ++i)
-          f(wm * MT * 8 + mt * 8 + fr, wn * NT * 8 + nt * 8 + 2 * fc + i,
-            make_double2(acc[mt][nt][0][i], acc[mt][nt][1][i]));
+          f(row_of(mt, fr), col_of(nt, 2 * fc + i), make_double2(acc[mt][nt][0][i], acc[mt][nt][1][i]));
   }
 };
+
+using Eng64 = Engine<2, 4, 4, 2, 4>;
 
 }  // namespace dmma

@@ -32,7 +32,9 @@
 #include <vector>
 
 #include "../../include/find_b200.h"
+#include "dmma_engine.cuh"
 #include "plan.h"
+#include "tmap_host.h"
 
 using namespace findb200;
 
@@ -120,6 +122,8 @@ struct SolveParams {
   int64_t n_pairs;
   int32_t off_sym;  // +1 / -1: Sigma^< exactly Hermitian / skew-Hermitian (then G^< is too), 0 general
   int32_t zskip;    // skip the products of structurally zero (B_r, S_l) blocks (ElimDesc::zsplit)
+  int32_t use_tma;  // DMMA tiles of trail / Schur / T / R through the TMA engine (tmaps valid)
+  const CUtensorMap* tmaps;  // [n_tmap][3]: M, MS, X of each CTA-path elimination (ElimDesc::tmap)
 };
 
 __device__ __forceinline__ void report_bad(const SolveParams& P, int64_t elim_global, int e, int pos) {
@@ -1646,6 +1650,194 @@ __global__ void __launch_bounds__(kThreads) panel_cluster_kernel(SolveParams P, 
   }
 }
 
+// ---- NB = 32 panel step over a thread-block cluster with the rows in REGISTERS (panel1_kernel's
+// scheme spread over CS <= 8 CTAs of T threads, one S row per thread): per column every warp
+// reduces its best candidate (max |re|+|im|, lowest logical position on ties) and that lane posts
+// its live row and 1/u to a per-warp slot; after one CTA barrier every CTA posts its best (value,
+// position, row) to every CTA of the cluster through DSMEM (double-buffered by column parity);
+// after one cluster barrier all threads pick the same winner from their local copies and update
+// their own row in registers.  Interchanges only swap logical positions; every row is written once,
+// to its final position, at the end.  Same pivots and arithmetic as panel1_kernel (the rank-1
+// update of the panel rows runs out of registers instead of shared memory).
+constexpr int kRegClusterRows = 256;  // rows per CTA (T <= 256 threads)
+template <int T>
+__global__ void __launch_bounds__(T, 1) panel_cluster_reg_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
+  namespace cg = cooperative_groups;
+  constexpr int NB = 32, NW = T / 32;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CS = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  __shared__ double2 wrow[2][NW][NB + 1];           // per-warp candidate rows (+ 1/u)
+  __shared__ double wv[2][NW];
+  __shared__ int wp[2][NW];
+  __shared__ double2 crow[2][kClusterMax][NB + 1];  // every CTA's candidate row, posted by its owner CTA
+  __shared__ double cv[2][kClusterMax];
+  __shared__ int cp[2][kClusterMax];
+  __shared__ int s_bad, s_nd;
+  __shared__ double2 s_pval[NB];
+  __shared__ int s_piv[NB];
+  __shared__ double s_scale[NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Task t = tasks[blockIdx.x / CS];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, j = t.a;
+  const int j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
+  const int chunk = (R + CS - 1) / CS;
+  const int r_lo = min(R, rank * chunk), r_hi = min(R, r_lo + chunk);
+  const int gr = r_lo + tid;  // this thread's panel row (physical, = its initial logical position)
+  const Scr S = scratch_of(P, d, e, NB);
+  double2* M = S.M;
+  double2* Lst = S.MS + (int64_t)gr * NB;
+  const bool has = gr < r_hi;
+  int pos = gr;
+  double2 row[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) row[c] = (has && c < jb) ? M[(int64_t)(j0 + gr) * n + j0 + c] : cz();
+  if (tid == 0) { s_bad = INT32_MAX; s_nd = 0; }
+  if (rank == 0 && j == 0) {
+    double sc = 0.0;
+    for (int q = tid; q < (s + kRowChunk - 1) / kRowChunk; q += T) sc = fmax(sc, S.pmax[q]);
+    for (int o = 16; o; o >>= 1) sc = fmax(sc, __shfl_xor_sync(0xffffffffu, sc, o));
+    if (lane == 0) s_scale[warp] = sc;
+    __syncthreads();
+    sc = s_scale[0];
+    for (int w = 1; w < NW; ++w) sc = fmax(sc, s_scale[w]);
+    if (tid == 0) {
+      *S.scale = sc;
+      if (sc == 0.0) s_bad = 0;
+    }
+  }
+  cluster.sync();
+  const double scale = *reinterpret_cast<volatile double*>(S.scale);
+#pragma unroll 1
+  for (int jj = 0; jj < jb; ++jj) {
+    const int buf = jj & 1;
+    const int rem = jb - jj - 1;
+    const bool act = has && pos >= jj;
+    const double2 rinv = crcp(row[0]);
+    const double v0 = cabs1(row[0]);
+    const double v = v0 >= 0.0 ? v0 : 0.0;  // NaN ranks lowest
+    const int vhi = act ? __double2hiint(v) : -1;
+    const int mhi = __reduce_max_sync(0xffffffffu, vhi);
+    const unsigned vlo = (unsigned)__double2loint(v);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, vhi == mhi ? vlo : 0u);
+    const bool best = act && vhi == mhi && vlo == mlo;
+    const int wpos = (int)__reduce_min_sync(0xffffffffu, (unsigned)(best ? pos : INT32_MAX));
+    if (best && pos == wpos) {  // the warp's candidate posts its live row and pivot inverse
+      double2* slot = wrow[buf][warp];
+      slot[NB] = rinv;
+#pragma unroll
+      for (int c0 = 0; c0 < NB; c0 += 4)
+        if (c0 <= rem) {
+#pragma unroll
+          for (int c = c0; c < c0 + 4; ++c) slot[c] = row[c];
+        }
+    }
+    if (lane == 0) {
+      wv[buf][warp] = mhi < 0 ? -1.0 : __hiloint2double(mhi, (int)mlo);
+      wp[buf][warp] = wpos;
+    }
+    __syncthreads();
+    // CTA candidate (every thread computes it) -> posted to every CTA of the cluster
+    double bv = -1.0;
+    int bp = INT32_MAX, bw = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const double ov = wv[buf][w];
+      const int op = wp[buf][w];
+      if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; bw = w; }
+    }
+    for (int q = tid; q < CS * (NB + 2); q += T) {
+      const int dst = q / (NB + 2), c = q % (NB + 2);
+      if (c == NB + 1) {
+        *cluster.map_shared_rank(&cv[buf][rank], dst) = bv;
+        *cluster.map_shared_rank(&cp[buf][rank], dst) = bp;
+      } else if (bp != INT32_MAX && (c == NB || c <= rem)) {
+        cluster.map_shared_rank(&crow[buf][rank][0], dst)[c] = wrow[buf][bw][c];
+      }
+    }
+    cluster.sync();
+    double gv = -1.0;
+    int pr0 = INT32_MAX, pk = 0;
+    for (int k = 0; k < CS; ++k) {
+      const double ov = cv[buf][k];
+      const int op = cp[buf][k];
+      if (ov > gv || (ov == gv && op < pr0)) { gv = ov; pr0 = op; pk = k; }
+    }
+    const bool valid = pr0 >= jj && pr0 < R;  // NaN / Inf entries: no interchange (row jj pivots)
+    const int pr = valid ? pr0 : jj;
+    const double2* prow = crow[buf][pk];
+    if (!valid) {
+      // the row at logical position jj is this column's pivot: its owner has not posted it; every
+      // thread reads it through its owner's candidate slot after a second exchange (rare path)
+      __syncthreads();
+      if (has && pos == jj) {
+        for (int dst = 0; dst < CS; ++dst) {
+          double2* o = cluster.map_shared_rank(&crow[buf][0][0], dst);
+#pragma unroll
+          for (int c = 0; c < NB; ++c) o[c] = row[c];
+          o[NB] = rinv;
+        }
+      }
+      cluster.sync();
+      prow = crow[buf][0];
+    }
+    if (rank == 0 && tid == 0) {
+      s_piv[jj] = pr;
+      s_pval[jj] = prow[0];
+    }
+    if (has && pos == pr) pos = -1 - jj;  // pivot row of column jj (final position jj)
+    else if (has && pos == jj) pos = pr;
+    if (has && pos > jj) {
+      const double2 l = cmul(row[0], prow[NB]);
+      Lst[jj] = l;
+#pragma unroll
+      for (int c0 = 1; c0 < NB; c0 += 8)
+        if (c0 <= rem) {
+          double2 pv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c0 + q < NB) pv[q] = prow[c0 + q];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c0 + q < NB) row[c0 + q - 1] = cfms(row[c0 + q], l, pv[q]);
+        }
+    }
+  }
+  // final positions: pivot rows (pos = -1 - jj) hold U row jj shifted by jj
+  const int fp = pos < 0 ? -1 - pos : pos;
+  if (has) {
+    double2* dst = M + (int64_t)(j0 + fp) * n + j0;
+    const int nl = min(fp, jb);
+#pragma unroll 8
+    for (int c = 0; c < nl; ++c) dst[c] = Lst[c];
+    if (pos < 0) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (fp + c < jb) dst[fp + c] = row[c];
+    }
+    if (fp != gr) {  // net interchange entry, counted on rank 0's counter
+      const int k = atomicAdd(cluster.map_shared_rank(&s_nd, 0), 1);
+      S.PERM[1 + k] = gr;
+      S.PERM[1 + 2 * NB + k] = fp;
+    }
+  }
+  cluster.sync();
+  if (rank == 0) {
+    for (int k = tid; k < jb; k += T) {  // pivot rows and the pivot test of kernels.py:241
+      S.PIV[j0 + k] = j0 + s_piv[k];
+      if (cabs(s_pval[k]) < P.rtol * scale) atomicMin(&s_bad, j0 + k);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      S.PERM[0] = s_nd;
+      if (s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
+    }
+  }
+}
+
 template <int NB>
 struct TrsmTiles;
 template <>
@@ -2160,6 +2352,156 @@ __global__ void __launch_bounds__(kThreads, 2) rgemm_kernel(SolveParams P, const
   rgemm_body(P, tasks[blockIdx.x], blockIdx.y, nb, reinterpret_cast<double2*>(smem_raw));
 }
 
+// ---- the same four DMMA tile kinds (trailing update, Schur, T_S, R) through the TMA engine
+// (dmma_engine.cuh): one persistent CTA per SM walks the launch's (task, energy) tiles in order;
+// a producer warp streams the operands (UTMALDG boxes of the A / X^H operands through the
+// elimination's tensor maps, UBLKCP rows of the [k][n] operands) into a 4-stage mbarrier ring
+// and prefetches the next tile's C block into L2; eight consumer warps run the DMMA fragments.
+// Same products, operand order and epilogues as trail_body / schur_body / tgemm_body /
+// rgemm_body (bit-identical results).
+using TmaEng = dmma::Eng64;
+
+struct TileJob {
+  dmma::Seg seg[2];
+  int nseg;
+  double2* C;     // C block (row stride n)
+  int mv, nv;     // valid rows / columns of the tile
+  const CUtensorMap* cmap;
+  int cr, cc;     // C block origin in cmap's matrix
+};
+
+template <int KIND>
+__device__ __forceinline__ bool tile_job(const SolveParams& P, const Task& t, int e, int j, int nb, TileJob& J) {
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, b = d.b;
+  const CUtensorMap* tm = P.tmaps + 3 * (int64_t)d.tmap;
+  double2* M = scratch_of(P, d, e).M;
+  double2* MS = M + (int64_t)n * n;
+  if (KIND == kLTrail) {
+    const int j0 = (t.c == 1 ? j - 1 : j) * nb, j1 = min(s, (j + 1) * nb), jb = j1 - j0;
+    const int r0 = j1 + t.a * kTile, c0 = j1 + t.b * kTile;
+    const int cw = t.c == 2 ? min(nb, s - j1) : kTile;
+    if (P.zskip && d.zsplit && j1 <= (d.zsplit & 0xffff) && r0 >= s + (d.zsplit >> 16)) return false;
+    J.seg[0] = {tm + 0, nullptr, M + (int64_t)j0 * n + c0, n, r0, j0, 0, 0, jb, 0};
+    J.nseg = 1;
+    J.C = M + (int64_t)r0 * n + c0;
+    J.mv = min(kTile, n - r0);
+    J.nv = min(cw, n - c0);
+    J.cmap = tm + 0;
+    J.cr = r0;
+    J.cc = c0;
+  } else if (KIND == kLSchur) {
+    const int i0 = t.a * kTile, c0 = t.b * kTile;
+    const int k0 = (P.zskip && d.zsplit && i0 >= (d.zsplit >> 16)) ? ((d.zsplit & 0xffff) / kKC) * kKC : 0;
+    J.seg[0] = {tm + 0, nullptr, M + (int64_t)k0 * n + s + c0, n, s + i0, k0, 0, 0, s - k0, 0};
+    J.nseg = 1;
+    J.C = M + (int64_t)(s + i0) * n + s + c0;
+    J.mv = min(kTile, b - i0);
+    J.nv = min(kTile, b - c0);
+    J.cmap = tm + 0;
+    J.cr = s + i0;
+    J.cc = s + c0;
+  } else if (KIND == kLTGemm) {
+    const int i0 = t.a * kTile, c0 = t.b * kTile;
+    J.seg[0] = {tm + 2, nullptr, MS + c0, n, i0, 0, 0, 0, s, 0};
+    J.nseg = 1;
+    J.C = MS + (int64_t)(s + i0) * n + c0;
+    J.mv = min(kTile, b - i0);
+    J.nv = min(kTile, s - c0);
+    J.cmap = tm + 1;
+    J.cr = s + i0;
+    J.cc = c0;
+  } else {  // kLRGemm: R = Sigma'_BB - X Sigma'_SB - T_S X^H
+    if (t.c == 2 && P.rsym != 0) return false;
+    const int i0 = t.a * kTile, c0 = t.b * kTile;
+    J.seg[0] = {tm + 2, nullptr, MS + s + c0, n, i0, 0, 0, 0, s, 0};
+    J.seg[1] = {tm + 1, tm + 2, nullptr, 0, s + i0, 0, c0, 0, s, 1};
+    J.nseg = 2;
+    J.C = MS + (int64_t)(s + i0) * n + s + c0;
+    J.mv = min(kTile, b - i0);
+    J.nv = min(kTile, b - c0);
+    J.cmap = tm + 1;
+    J.cr = s + i0;
+    J.cc = s + c0;
+  }
+  return true;
+}
+
+template <int KIND>
+__device__ __forceinline__ void tile_store(const SolveParams& P, const Task& t, int e, int j, int nb, const TileJob& J,
+                                           const TmaEng& eng) {
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, b = d.b;
+  if (KIND == kLTrail) {
+    const int j1 = min(s, (j + 1) * nb);
+    const int r0 = j1 + t.a * kTile, c0 = j1 + t.b * kTile;
+    const int cw = t.c == 2 ? min(nb, s - j1) : kTile;
+    eng.for_each([&](int r, int c, double2 v) {
+      if (r0 + r < n && c < cw && c0 + c < n && (r0 + r < s || c0 + c < s)) J.C[(int64_t)r * n + c] = v;
+    });
+  } else if (KIND == kLTGemm) {
+    eng.for_each([&](int r, int c, double2 v) {
+      if (r < J.mv && c < J.nv) J.C[(int64_t)r * n + c] = v;
+    });
+  } else {
+    const int i0 = t.a * kTile, c0 = t.b * kTile;
+    const bool store = d.kind != kFinal && d.out_arena >= 0;
+    const int32_t* rank = P.i32 + d.rank_off;
+    if (KIND == kLSchur) {
+      double2* out = store ? P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off : nullptr;
+      eng.for_each([&](int r, int c, double2 v) {
+        const int i = i0 + r, jj = c0 + c;
+        if (i < b && jj < b) {
+          if (store) out[(int64_t)rank[i] * b + rank[jj]] = v;
+          else J.C[(int64_t)r * n + c] = v;
+        }
+      });
+    } else {
+      const bool mirror = store && P.rsym != 0;
+      const double sg = P.rsym < 0 ? -1.0 : 1.0;
+      double2* out = store ? P.arena[d.out_arena] + (int64_t)e * P.arena_elems[d.out_arena] + d.out_off + (int64_t)b * b
+                           : nullptr;
+      eng.for_each([&](int r, int c, double2 v) {
+        const int i = i0 + r, jj = c0 + c;
+        if (i < b && jj < b) {
+          if (!store) {
+            J.C[(int64_t)r * n + c] = v;
+          } else if (!mirror) {
+            out[(int64_t)rank[i] * b + rank[jj]] = v;
+          } else if (i >= jj) {
+            out[(int64_t)rank[i] * b + rank[jj]] = v;
+            if (i != jj) out[(int64_t)rank[jj] * b + rank[i]] = make_double2(sg * v.x, -sg * v.y);
+          }
+        }
+      });
+    }
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(TmaEng::THREADS, 1) tile_tma_kernel(SolveParams P, const Task* tasks, int64_t cnt,
+                                                                     int nE, int j, int nb) {
+  pdl_entry();
+  extern __shared__ __align__(16) unsigned char smem_raw[];  // Engine::init aligns to 1024
+  TmaEng eng;
+  eng.init(smem_raw);
+  const int64_t total = cnt * nE;
+  for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
+    const int e = (int)(q / cnt);
+    const Task t = tasks[q % cnt];
+    TileJob J;
+    if (!tile_job<KIND>(P, t, e, j, nb, J)) continue;
+    if (TmaEng::producer()) {
+      TmaEng::prefetch_c(J.cmap, J.cr, J.cc, e);
+      eng.produce(J.seg, J.nseg, e, J.nv);
+    } else {
+      eng.load_c(J.C, P.elims[t.e].n, J.mv, J.nv);
+      eng.template consume<true>(J.seg, J.nseg, J.mv, J.nv);
+      tile_store<KIND>(P, t, e, j, nb, J, eng);
+    }
+  }
+}
+
 // ---- final leaf step epilogue, warp per (leaf, energy)
 __device__ void final_body_warp(const SolveParams& P, const Task& t, int e, double2* uf, int cmax, int lane) {
   const ElimDesc d = P.elims[t.e];
@@ -2624,6 +2966,10 @@ int set_attrs(find_status* st) {
                                 (int)offdiag_small_smem<32>()));
   CUDA_TRY(cudaFuncSetAttribute(offdiag_small_kernel<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)offdiag_small_smem<64>()));
+  CUDA_TRY(cudaFuncSetAttribute(tile_tma_kernel<kLTrail>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaEng::SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(tile_tma_kernel<kLSchur>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaEng::SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(tile_tma_kernel<kLTGemm>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaEng::SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(tile_tma_kernel<kLRGemm>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaEng::SMEM));
   g_attrs_done[dev] = true;
   return FIND_OK;
 }
@@ -2870,6 +3216,39 @@ const int g_skip = [] {
   return std::string(f) == "tall" ? 1 : (std::string(f) == "other" ? 2 : 0);
 }();
 
+// persistent grid of the TMA tile kernels: one CTA per SM at most (a CTA holds ~132 KB of smem)
+int g_num_sms[kMaxDevices] = {};
+dim3 tma_grid(unsigned cnt, int nE) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g_num_sms[dev] == 0) cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int64_t total = (int64_t)cnt * nE;
+  return dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(total, g_num_sms[dev])), 1);
+}
+
+// NB = 32 panels of more than kRegPanelMaxS rows on register-row clusters (FIND_B200_CREG=0: the
+// shared-memory-row panel / cluster kernels)
+const bool g_creg = [] {
+  const char* f = std::getenv("FIND_B200_CREG");
+  return !(f && f[0] == '0');
+}();
+
+// TMA engine switch (FIND_B200_TMA=0: the cp.async tile kernels everywhere)
+const bool g_tma = [] {
+  const char* f = std::getenv("FIND_B200_TMA");
+  return !(f && f[0] == '0');
+}();
+// groups that use the engine (persistent 1-CTA/SM grids pay off on long K / many tiles; small
+// launches keep the 2-CTA/SM cp.async kernels that co-reside with the other groups of a phase)
+const int g_tma_min_s = [] {
+  const char* f = std::getenv("FIND_B200_TMA_MIN_S");
+  return f ? std::atoi(f) : 256;
+}();
+const int g_tma_trail_min_n = [] {
+  const char* f = std::getenv("FIND_B200_TMA_TRAIL_MIN_N");
+  return f ? std::atoi(f) : 1024;
+}();
+
 const bool g_rsym_down = [] {
   const char* f = std::getenv("FIND_B200_RSYM_DOWN");
   return f && f[0] == '1';
@@ -2930,7 +3309,22 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         case kLGatherS: launch_k(gather_kernel<true>, grid, kThreads, 0, stream, prm, tk); break;
         case kLPanel: {
           const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
-          if (L.nb == 32 && rmax > (int)kSmemPanelMaxS32) {  // rows over a thread-block cluster
+          if (L.nb == 32 && g_creg && rmax > (int)kRegPanelMaxS && rmax <= kClusterMax * kRegClusterRows) {
+            // register rows over a thread-block cluster of cs CTAs
+            const unsigned cs = (unsigned)((rmax + kRegClusterRows - 1) / kRegClusterRows);
+            const int rows = (rmax + (int)cs - 1) / (int)cs;
+            const dim3 cg(cnt * cs, (unsigned)nE);
+            switch ((rows + 31) / 32) {
+              case 1: launch_cluster(panel_cluster_reg_kernel<32>, cg, 32, cs, 0, stream, prm, tk); break;
+              case 2: launch_cluster(panel_cluster_reg_kernel<64>, cg, 64, cs, 0, stream, prm, tk); break;
+              case 3: launch_cluster(panel_cluster_reg_kernel<96>, cg, 96, cs, 0, stream, prm, tk); break;
+              case 4: launch_cluster(panel_cluster_reg_kernel<128>, cg, 128, cs, 0, stream, prm, tk); break;
+              case 5: launch_cluster(panel_cluster_reg_kernel<160>, cg, 160, cs, 0, stream, prm, tk); break;
+              case 6: launch_cluster(panel_cluster_reg_kernel<192>, cg, 192, cs, 0, stream, prm, tk); break;
+              case 7: launch_cluster(panel_cluster_reg_kernel<224>, cg, 224, cs, 0, stream, prm, tk); break;
+              default: launch_cluster(panel_cluster_reg_kernel<256>, cg, 256, cs, 0, stream, prm, tk); break;
+            }
+          } else if (L.nb == 32 && rmax > (int)kSmemPanelMaxS32) {  // rows over a thread-block cluster
             const unsigned cs = (unsigned)((rmax + kClusterRows - 1) / kClusterRows);
             if (cs > (unsigned)kClusterMax) return fail_status(st, FIND_EINVAL, "panel too tall for one cluster");
             launch_cluster(panel_cluster_kernel, dim3(cnt * cs, (unsigned)nE), kThreads, cs, cluster_panel_smem(), stream,
@@ -2988,7 +3382,13 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           else launch_k(trsm_kernel<4>, grid, kThreads, trsm_smem<4>(), stream, prm, tk, L.step, ir);
           break;
         }
-        case kLTrail: launch_k(trail_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.step, L.nb); break;
+        case kLTrail:
+          if (prm.use_tma && G.max_n >= g_tma_trail_min_n)
+            launch_k(tile_tma_kernel<kLTrail>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
+                     (int64_t)cnt, nE, L.step, L.nb);
+          else
+            launch_k(trail_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.step, L.nb);
+          break;
         case kLXSolve:
           if (L.nb == 32) launch_k(xsolve_kernel<32>, grid, kThreads, xsolve_smem<32>(), stream, prm, tk);
           else if (L.nb == 16) launch_k(xsolve_kernel<16>, grid, kThreads, xsolve_smem<16>(), stream, prm, tk);
@@ -2998,9 +3398,27 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         case kLFinish:
           launch_k(finish_kernel, grid, kThreads, std::max<size_t>((size_t)G.max_s * sizeof(int), 16), stream, prm, tk, L.nb);
           break;
-        case kLTGemm: launch_k(tgemm_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.nb); break;
-        case kLRGemm: launch_k(rgemm_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.nb); break;
-        case kLSchur: launch_k(schur_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk); break;
+        case kLTGemm:
+          if (prm.use_tma && G.max_s >= g_tma_min_s)
+            launch_k(tile_tma_kernel<kLTGemm>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
+                     (int64_t)cnt, nE, 0, L.nb);
+          else
+            launch_k(tgemm_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.nb);
+          break;
+        case kLRGemm:
+          if (prm.use_tma && G.max_s >= g_tma_min_s)
+            launch_k(tile_tma_kernel<kLRGemm>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
+                     (int64_t)cnt, nE, 0, L.nb);
+          else
+            launch_k(rgemm_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.nb);
+          break;
+        case kLSchur:
+          if (prm.use_tma && G.max_s >= g_tma_min_s)
+            launch_k(tile_tma_kernel<kLSchur>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
+                     (int64_t)cnt, nE, 0, L.nb);
+          else
+            launch_k(schur_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk);
+          break;
         case kLLuFused: launch_k(lu_fused_kernel, grid, kFusedT, Tile64::SMEM, stream, prm, tk); break;
         case kLFinal: {
           const int cmax = std::max(1, G.max_b);
@@ -3078,6 +3496,89 @@ SolveParams make_params(const find_plan* P, void* ws, int nE) {
   return prm;
 }
 
+
+// Complex-element offset of X inside an elimination's scratch (scratch_of with the group's nb).
+int64_t x_offset(int64_t n, int64_t s, int nb) {
+  const int64_t nn = n * n, ints = (3 * s + 264 + 3) / 4;
+  const int64_t linv = 2 * nn + ints + 1 + (n + 2 * kRowChunk - 1) / (2 * kRowChunk);
+  const int64_t blocks = nb ? (s + nb - 1) / nb * (int64_t)nb * nb : 0;
+  return linv + 2 * blocks;
+}
+
+// Tensor maps {M, MS, X} of every CTA-path elimination for this scratch base and energy count,
+// cached per plan (a few entries; an entry is never rewritten, so solves in flight on other
+// streams keep valid maps).  The device copy is enqueued on `stream` (a memcpy node when the
+// stream is being captured).  Leaves prm.use_tma = 0 when the maps are unavailable.
+int ensure_tmaps(find_plan* P, SolveParams& prm, int nE, cudaStream_t stream, find_status* st) {
+  prm.use_tma = 0;
+  prm.tmaps = nullptr;
+  if (!g_tma || P->n_tmap == 0) return FIND_OK;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  for (auto& E : P->tmap_cache)
+    if (E.device == dev && E.scratch == prm.scratch && E.n_energies == nE) {
+      E.stamp = ++P->tmap_clock;
+      prm.tmaps = (const CUtensorMap*)E.dev;
+      prm.use_tma = 1;
+      return FIND_OK;
+    }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(stream, &cs));
+  constexpr size_t kMaxEntries = 4;
+  if (P->tmap_cache.size() >= kMaxEntries) {
+    if (cs != cudaStreamCaptureStatusNone) return FIND_OK;  // no eviction inside a capture: cp.async tiles
+    size_t lru = 0;
+    for (size_t i = 1; i < P->tmap_cache.size(); ++i)
+      if (P->tmap_cache[i].stamp < P->tmap_cache[lru].stamp) lru = i;
+    CUDA_TRY(cudaDeviceSynchronize());  // the evicted maps may still be read by queued work
+    auto& E = P->tmap_cache[lru];
+    int cur = dev;
+    if (E.device != dev) cudaSetDevice(E.device);
+    cudaFree(E.dev);
+    cudaFreeHost(E.host);
+    if (E.device != dev) cudaSetDevice(cur);
+    P->tmap_cache.erase(P->tmap_cache.begin() + (std::ptrdiff_t)lru);
+  }
+  const size_t bytes = (size_t)P->n_tmap * 3 * sizeof(CUtensorMap);
+  find_plan::TmapEntry E;
+  E.device = dev;
+  E.scratch = prm.scratch;
+  E.n_energies = nE;
+  CUDA_TRY(cudaMallocHost(&E.host, bytes));
+  if (cudaMalloc(&E.dev, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFreeHost(E.host);
+    return FIND_OK;  // no room: cp.async tiles
+  }
+  CUtensorMap* h = (CUtensorMap*)E.host;
+  bool ok = true;
+  for (const LaunchGroup& G : P->groups) {
+    if (G.path != 1) continue;
+    for (int64_t k = G.begin; k < G.end && ok; ++k) {
+      const ElimDesc& d = P->elims[k];
+      if (d.tmap < 0) continue;
+      const double2* M = prm.scratch + d.ws_off;
+      const int64_t n = d.n, s = d.s, b = d.b;
+      CUtensorMap* t = h + 3 * (int64_t)d.tmap;
+      ok = encode_complex_tmap(t + 0, M, n, n, n, P->ws_elems, nE) &&
+           encode_complex_tmap(t + 1, M + n * n, n, n, n, P->ws_elems, nE) &&
+           encode_complex_tmap(t + 2, M + x_offset(n, s, G.nb), std::max<int64_t>(s, 1), std::max<int64_t>(b, 1),
+                               std::max<int64_t>(s, 1), P->ws_elems, nE);
+    }
+  }
+  if (!ok) {
+    cudaFree(E.dev);
+    cudaFreeHost(E.host);
+    return FIND_OK;
+  }
+  CUDA_TRY(cudaMemcpyAsync(E.dev, E.host, bytes, cudaMemcpyHostToDevice, stream));
+  E.stamp = ++P->tmap_clock;
+  P->tmap_cache.push_back(E);
+  prm.tmaps = (const CUtensorMap*)E.dev;
+  prm.use_tma = 1;
+  return FIND_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -3094,6 +3595,18 @@ void find_plan_free_device(find_plan* P) {
   P->d_off_items = P->d_off_item_off = nullptr;
   P->off_device = -1;
   P->device = -1;
+  if (!P->tmap_cache.empty()) {
+    cudaDeviceSynchronize();
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& E : P->tmap_cache) {
+      cudaSetDevice(E.device);
+      cudaFree(E.dev);
+      cudaFreeHost(E.host);
+    }
+    cudaSetDevice(cur);
+    P->tmap_cache.clear();
+  }
 }
 
 int find_plan_upload(find_plan* P, find_status* st) {
@@ -3103,6 +3616,13 @@ int find_plan_upload(find_plan* P, find_status* st) {
   CUDA_TRY(cudaGetDevice(&dev));
   if (P->d_elims && P->device == dev) return FIND_OK;
   find_plan_free_device(P);
+  // tensor-map slots of the CTA-path eliminations (ensure_tmaps fills them per scratch base)
+  for (auto& d : P->elims) d.tmap = -1;
+  int32_t nt = 0;
+  for (const LaunchGroup& G : P->groups)
+    if (G.path == 1)
+      for (int64_t k = G.begin; k < G.end; ++k) P->elims[k].tmap = nt++;
+  P->n_tmap = nt;
   auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
     cudaError_t e = cudaMalloc(dst, bytes ? bytes : 16);
     if (e != cudaSuccess) return e;
@@ -3197,6 +3717,7 @@ int find_solve_offdiag_groups(find_plan* P, const void* a_vals, const void* s_va
   if (g_begin < 0) g_begin = 0;
   if (g_end < 0 || g_end > (int64_t)P->groups.size()) g_end = (int64_t)P->groups.size();
   if (g_begin == 0) CUDA_TRY(cudaMemsetAsync(ws, 0xff, 8, stream));
+  if ((rc = ensure_tmaps(P, prm, nE, stream, st))) return rc;
   return run_groups(P, prm, g_begin, g_end, nE, stream, st);
 }
 

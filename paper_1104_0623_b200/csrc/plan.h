@@ -36,7 +36,10 @@ struct alignas(16) ElimDesc {
   int64_t ws_off;            // complex-element offset of this elimination's scratch (per energy)
   int64_t slabel_off;        // int64 host-only array: S labels in merged order (error reporting)
   int64_t sprow_off;         // int32[n+1]: per merged row, offsets of its sparse entries (relative)
+  int32_t tmap;              // CTA-path eliminations: index of its tensor-map triple (M, MS, X); else -1
+  int32_t tmap_pad;
 };
+static_assert(sizeof(ElimDesc) == 128, "ElimDesc layout");
 
 // Phase launches of the CTA path (one launch = one kind over a task list).
 enum LaunchKind : int32_t {
@@ -165,4 +168,18 @@ struct find_plan {
   void* d_i32 = nullptr;
   void* d_sparse = nullptr;
   void* d_tasks = nullptr;
+  // TMA tensor maps of the CTA-path scratch matrices (find_solve.cu ensure_tmaps): a few entries,
+  // one per (device, scratch base, energy count) seen, each a pinned host + a device array of
+  // n_tmap x {M, MS, X} CUtensorMap (128 B each)
+  int32_t n_tmap = 0;
+  struct TmapEntry {
+    int device = -1;
+    const void* scratch = nullptr;
+    int32_t n_energies = 0;
+    void* host = nullptr;
+    void* dev = nullptr;
+    uint64_t stamp = 0;
+  };
+  std::vector<TmapEntry> tmap_cache;
+  uint64_t tmap_clock = 0;
 };

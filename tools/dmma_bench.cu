@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "dmma_engine.cuh"
+#include "tmap_host.h"
 
 #define CK(x)                                                                        \
   do {                                                                               \
@@ -27,10 +28,14 @@ struct Prob {
   int batch, M, N, K, nseg, bt2;  // segment 2 (if nseg == 2): conj-transposed B of shape [N][K]
 };
 
+struct Maps {
+  CUtensorMap a, a2, b2;
+};
+
 template <class E>
-__global__ void __launch_bounds__(E::THREADS, 1) eng_kernel(Prob p, const double2* A, const double2* B,
-                                                            const double2* A2, const double2* B2, double2* C) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+__global__ void __launch_bounds__(E::THREADS, 1) eng_kernel(Prob p, const __grid_constant__ Maps maps, const double2* B,
+                                                            double2* C) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   E eng;
   eng.init(smem_raw);
   const int tm = (p.M + E::BM - 1) / E::BM, tn = (p.N + E::BN - 1) / E::BN;
@@ -40,12 +45,11 @@ __global__ void __launch_bounds__(E::THREADS, 1) eng_kernel(Prob p, const double
     const int i0 = (r / tn) * E::BM, c0 = (r % tn) * E::BN;
     const int mv = min(E::BM, p.M - i0), nv = min(E::BN, p.N - c0);
     dmma::Seg seg[2];
-    seg[0] = {A + (int64_t)bi * p.M * p.K + (int64_t)i0 * p.K, B + (int64_t)bi * p.K * p.N + c0, p.K, p.N, p.K, 0};
-    seg[1] = {A2 + (int64_t)bi * p.M * p.K + (int64_t)i0 * p.K, B2 + (int64_t)bi * p.N * p.K + (int64_t)c0 * p.K, p.K,
-              p.K, p.K, 1};
+    seg[0] = {&maps.a, nullptr, B + (int64_t)bi * p.K * p.N + c0, p.N, i0, 0, 0, 0, p.K, 0};
+    seg[1] = {&maps.a2, &maps.b2, nullptr, 0, i0, 0, c0, 0, p.K, 1};
     double2* Cb = C + (int64_t)bi * p.M * p.N + (int64_t)i0 * p.N + c0;
     if (E::producer()) {
-      eng.produce(seg, p.nseg, mv, nv);
+      eng.produce(seg, p.nseg, bi, nv);
     } else {
       eng.load_c(Cb, p.N, mv, nv);
       eng.template consume<true>(seg, p.nseg, mv, nv);
@@ -100,6 +104,13 @@ void run(const char* name, Prob p, int sms, bool check) {
   fill(A2, na, 3);
   fill(B2, nb, 4);
   fill(C0, nc, 5);
+  Maps maps;
+  if (!findb200::encode_complex_tmap(&maps.a, A, p.K, p.M, p.K, (int64_t)p.M * p.K, p.batch) ||
+      !findb200::encode_complex_tmap(&maps.a2, A2, p.K, p.M, p.K, (int64_t)p.M * p.K, p.batch) ||
+      !findb200::encode_complex_tmap(&maps.b2, B2, p.K, p.N, p.K, (int64_t)p.N * p.K, p.batch)) {
+    std::printf("tensor map encoding failed\n");
+    std::exit(1);
+  }
   CK(cudaFuncSetAttribute(eng_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E::SMEM));
   const int tiles = p.batch * ((p.M + E::BM - 1) / E::BM) * ((p.N + E::BN - 1) / E::BN);
   int per_sm = 0;
@@ -108,7 +119,7 @@ void run(const char* name, Prob p, int sms, bool check) {
   if (check) {
     CK(cudaMemcpy(C, C0, nc * 16, cudaMemcpyDeviceToDevice));
     CK(cudaMemcpy(Cr, C0, nc * 16, cudaMemcpyDeviceToDevice));
-    eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, A, B, A2, B2, C);
+    eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, maps, B, C);
     CK(cudaGetLastError());
     naive_kernel<<<(unsigned)((nc + 255) / 256), 256>>>(p, A, B, A2, B2, Cr);
     CK(cudaDeviceSynchronize());
@@ -126,9 +137,9 @@ void run(const char* name, Prob p, int sms, bool check) {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   const int reps = 10;
-  eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, A, B, A2, B2, C);
+  eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, maps, B, C);
   CK(cudaEventRecord(e0));
-  for (int r = 0; r < reps; ++r) eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, A, B, A2, B2, C);
+  for (int r = 0; r < reps; ++r) eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, maps, B, C);
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
@@ -166,8 +177,7 @@ void run(const char* name, Prob p, int sms, bool check) {
 
 using E64x64s4 = dmma::Engine<2, 4, 4, 2, 4>;
 using E64x64s2 = dmma::Engine<2, 4, 4, 2, 2>;
-using E128x64s3 = dmma::Engine<4, 2, 4, 4, 3>;
-using E64x128s3 = dmma::Engine<2, 4, 4, 4, 3>;
+using E64x64s6 = dmma::Engine<2, 4, 4, 2, 6>;
 
 int main() {
   int sms = 0;
@@ -177,17 +187,14 @@ int main() {
       small{64, 256, 256, 256, 1, 0}, trail_small{64, 200, 200, 32, 1, 0};
   run<E64x64s4>("trail 4x3000^2 K64", trail, sms, true);
   run<E64x64s2>("trail 4x3000^2 K64", trail, sms, false);
-  run<E128x64s3>("trail 4x3000^2 K64", trail, sms, true);
-  run<E64x128s3>("trail 4x3000^2 K64", trail, sms, true);
+  run<E64x64s6>("trail 4x3000^2 K64", trail, sms, false);
   run<E64x64s4>("rgemm 4x1535^2 K2045x2", rgemm, sms, true);
-  run<E128x64s3>("rgemm 4x1535^2 K2045x2", rgemm, sms, true);
-  run<E64x128s3>("rgemm 4x1535^2 K2045x2", rgemm, sms, false);
+  run<E64x64s6>("rgemm 4x1535^2 K2045x2", rgemm, sms, false);
   run<E64x64s4>("schur 4x1535^2 K2045", schur, sms, false);
-  run<E128x64s3>("schur 4x1535^2 K2045", schur, sms, false);
   run<E64x64s4>("cfg1 64x256^2 K256", small, sms, true);
-  run<E64x64s2>("cfg1 64x256^2 K256", small, sms, false);
-  run<E128x64s3>("cfg1 64x256^2 K256", small, sms, false);
   run<E64x64s4>("trail cfg1 64x200^2 K32", trail_small, sms, true);
   run<E64x64s2>("trail cfg1 64x200^2 K32", trail_small, sms, false);
+  const Prob odd{3, 1000, 777, 45, 2, 1};
+  run<E64x64s4>("odd 3x1000x777 K45x2", odd, sms, true);
   return 0;
 }
