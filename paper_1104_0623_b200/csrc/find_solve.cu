@@ -3238,15 +3238,18 @@ const bool g_tma = [] {
   const char* f = std::getenv("FIND_B200_TMA");
   return !(f && f[0] == '0');
 }();
-// groups that use the engine (persistent 1-CTA/SM grids pay off on long K / many tiles; small
-// launches keep the 2-CTA/SM cp.async kernels that co-reside with the other groups of a phase)
+// Launch groups that use the engine.  Measured per group on cfg4 / cfg1 (tools/levels_compare.py,
+// profiles/r02_tma_thresholds.txt): the trailing updates (K = 32 / 64, many tiles) gain from the
+// producer running ahead across tiles (cfg4 trail 2092 -> 1989 ms serialized); the long-K
+// Schur / T / R products run faster on the 2-CTA/SM cp.async tiles at every group size, so they
+// keep those unless FIND_B200_TMA_MIN_S lowers the bound.
 const int g_tma_min_s = [] {
   const char* f = std::getenv("FIND_B200_TMA_MIN_S");
-  return f ? std::atoi(f) : 256;
+  return f ? std::atoi(f) : (1 << 30);
 }();
 const int g_tma_trail_min_n = [] {
   const char* f = std::getenv("FIND_B200_TMA_TRAIL_MIN_N");
-  return f ? std::atoi(f) : 1024;
+  return f ? std::atoi(f) : 256;
 }();
 
 const bool g_rsym_down = [] {
