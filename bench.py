@@ -164,9 +164,10 @@ def cpu_port(cfg_index, steps, warmup):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
-PORT_NOTE = ("the port is the reference algorithm with the same LAPACK calls but without its Python set-up "
-             "(O(n * #clusters) sets, per-call O(n) extract_block lookups): at cfg1 it runs one energy point in "
-             "11.8 s on 1 core against the reference's 115 s on 8 threads (SURVEY.md §6, §8(c)), so it favours the CPU")
+PORT_NOTE = ("calibration on cfg1, one core: the sampled estimate is 1.08x the port's full unsampled run (19.8 s), "
+             "and the port runs that energy point 1.76x faster than the reference's own solve (34.9 s): it keeps the "
+             "reference's algorithm and LAPACK calls but not its Python set-up (O(n * #clusters) sets, per-call O(n) "
+             "extract_block lookups), so it favours the CPU (profiles/r02_cpu_calibration_cfg1.json)")
 
 
 def cpu_baseline_line(cfg_index):

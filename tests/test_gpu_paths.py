@@ -8,6 +8,7 @@ import os
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 from conftest import ROOT
@@ -79,3 +80,22 @@ def test_structural_zero_skips_are_bit_identical(cuda):
         assert r.returncode == 0, r.stderr[-2000:]
         out.append([l for l in r.stdout.splitlines() if l.startswith("HASH")][-1])
     assert out[0] == out[1]
+
+
+@pytest.mark.gpu
+def test_two_devices_in_one_process():
+    """Kernel attributes and side streams are per device: a solve on cuda:0 then on cuda:1 (needs 2 GPUs)."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two CUDA devices")
+    from paper_1104_0623_b200 import Mesh, SolverConfig, SparseOperator, solve
+    from paper_1104_0623_b200.configs import build_problem
+
+    p = build_problem(12, 10, [1.2], seed=3)
+    out = []
+    for d in (0, 1):
+        with torch.cuda.device(d):
+            r = solve(Mesh(p.nx, p.ny), SparseOperator(p.a_csr(0)), SparseOperator(p.sigma_csr()), SolverConfig())
+            out.append(r)
+    np.testing.assert_allclose(out[0].gr_diag, out[1].gr_diag, rtol=0, atol=1e-13 * np.abs(out[0].gr_diag).max())

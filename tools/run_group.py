@@ -19,8 +19,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=1)
 ap.add_argument("--groups", type=int, nargs="*", default=[])
 ap.add_argument("--no-full", action="store_true", help="skip the full solve (inputs of the groups then stale)")
+ap.add_argument("--energies", type=int, default=0, help="first N energy points of the config (0: all)")
+ap.add_argument("--profile-groups", action="store_true",
+                help="cudaProfilerStart/Stop around the group runs (ncu --profile-from-start off)")
 a = ap.parse_args()
-p = config_problem(a.config)
+p = config_problem(a.config, a.energies or None)
 plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
 dev = torch.device("cuda", 0)
 ne = p.energies.size
@@ -32,7 +35,11 @@ ws = plan.workspace(ne, True, dev)
 if not a.no_full:
     plan.run(ad, sd, gr, gl, ws=ws, sigma_sym=-1)
 torch.cuda.synchronize()
+if a.profile_groups:
+    torch.cuda.profiler.start()
 for gi in a.groups:
     plan.run(ad, sd, gr, gl, ws=ws, sigma_sym=-1, groups=(gi, gi + 1))
     torch.cuda.synchronize()
+if a.profile_groups:
+    torch.cuda.profiler.stop()
 print("ok")
