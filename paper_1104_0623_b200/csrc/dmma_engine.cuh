@@ -110,29 +110,75 @@ struct Engine {
   static constexpr int B_BYTES_RAW = (BN * KC > KC * SKB ? BN * KC : KC * SKB) * 16;
   static constexpr int B_BYTES = (B_BYTES_RAW + 1023) & ~1023;
   static constexpr int STAGE = A_BYTES + B_BYTES;      // multiple of 1024 (swizzle-128B alignment)
-  static constexpr size_t SMEM = (size_t)S * STAGE + 1024 + 2 * S * sizeof(uint64_t);
+  static constexpr int QD = 2;                         // depth of the dynamic tile queue
+  // stages, then one 1 KB block of barriers / tile-queue slots; + 1 KB alignment slack
+  static constexpr size_t SMEM = (size_t)S * STAGE + 2048;
+  static_assert((2 * S + 2 * QD) * sizeof(uint64_t) + QD * sizeof(long long) <= 1024, "barrier block");
 
   unsigned char* st;  // S stages, 1024-byte aligned
   uint64_t* full;
   uint64_t* empty;
   unsigned chunk;  // running chunk counter (producer and consumers each keep their own copy)
+  // dynamic tile queue (next_tile): the producer warp draws tile indices from a global counter
+  // and hands them to the consumer warps through QD slots guarded by their own barriers
+  uint64_t* qfull;
+  uint64_t* qempty;
+  long long* qslot;
+  unsigned qn;
 
   __device__ __forceinline__ void init(unsigned char* smem_raw) {
     st = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     full = reinterpret_cast<uint64_t*>(st + (size_t)S * STAGE);
     empty = full + S;
+    qfull = empty + S;
+    qempty = qfull + QD;
+    qslot = reinterpret_cast<long long*>(qempty + QD);
     chunk = 0;
+    qn = 0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < S; ++i) {
         mbar_init(&full[i], 1);
         mbar_init(&empty[i], NW);
+      }
+      for (int i = 0; i < QD; ++i) {
+        mbar_init(&qfull[i], 1);
+        mbar_init(&qempty[i], NW);
       }
       mbar_fence_init();
     }
     __syncthreads();
   }
 
-  __device__ __forceinline__ static bool producer() { return threadIdx.x >= NW * 32; }
+  // Next tile index of this group, drawn from the launch's global counter (dynamic scheduling:
+  // tiles differ in K and in skipped work, so a static round-robin leaves SMs idle at the end).
+  // The producer warp draws (next_tile_p) and hands the index to its consumer warps
+  // (next_tile_c); -1 when the counter passed `total`.
+  __device__ __forceinline__ long long next_tile_p(unsigned long long* counter, long long total) {
+    const int lane = threadIdx.x & 31;
+    const unsigned slot = qn % QD, round = qn / QD;
+    ++qn;
+    mbar_wait(&qempty[slot], (round & 1) ^ 1);
+    long long t = 0;
+    if (lane == 0) {
+      t = (long long)atomicAdd(counter, 1ull);
+      if (t >= total) t = -1;
+      qslot[slot] = t;
+      mbar_arrive(&qfull[slot]);
+    }
+    return __shfl_sync(0xffffffffu, t, 0);
+  }
+  __device__ __forceinline__ long long next_tile_c() {
+    const int lane = threadIdx.x & 31;
+    const unsigned slot = qn % QD, round = qn / QD;
+    ++qn;
+    mbar_wait(&qfull[slot], round & 1);
+    const long long t = qslot[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&qempty[slot]);
+    return t;
+  }
+
+  __device__ __forceinline__ static bool producer() { return (int)threadIdx.x >= NW * 32; }
 
   // ---- producer warp: every K chunk of the segments of one tile (Nv: valid B columns)
   __device__ __forceinline__ void produce(const Seg* seg, int nseg, int e, int Nv) {
@@ -176,11 +222,11 @@ struct Engine {
   double acc[MT][NT][2][2];
 
   __device__ __forceinline__ static int row_of(int mt, int fr) {
-    const int warp = threadIdx.x >> 5;
+    const int warp = (int)threadIdx.x >> 5;
     return (warp % WM) * MT * 8 + mt * 8 + rho(fr);
   }
   __device__ __forceinline__ static int col_of(int nt, int x) {
-    const int warp = threadIdx.x >> 5;
+    const int warp = (int)threadIdx.x >> 5;
     return (warp / WM) * NT * 8 + nt * 8 + rho(x);
   }
 
@@ -208,14 +254,65 @@ struct Engine {
         }
   }
 
+  // One full K chunk (KC complex) for a warp whose MT x NT fragments are all valid: no
+  // predicates, constant shared-memory offsets, and the two DMMAs into one accumulator
+  // MT*NT*2 instructions apart (every accumulator chain still sums its products in the same
+  // order as the generic path: ax*bx then -ay*by; ax*by then ay*bx -> bit-identical).
+  template <bool NEG, bool BTc>
+  __device__ __forceinline__ void chunk_full(const unsigned char* a0, const unsigned char* a1, const unsigned char* b0,
+                                             const unsigned char* b1) {
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      const unsigned char* ap = ((kk & 4) ? a1 : a0) + (kk >> 3) * (BOXR * 128);
+      double2 a[MT], b[NT];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) a[mt] = *reinterpret_cast<const double2*>(ap + mt * (8 * 128));
+      if (BTc) {
+        const unsigned char* bp = ((kk & 4) ? b1 : b0) + (kk >> 3) * (BOXR * 128);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          b[nt] = *reinterpret_cast<const double2*>(bp + nt * (8 * 128));
+          b[nt].y = -b[nt].y;
+        }
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = *reinterpret_cast<const double2*>(b0 + (kk * SKB + nt * 8) * 16);
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const double ax = NEG ? -a[mt].x : a[mt].x;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma884(acc[mt][nt][0][0], acc[mt][nt][0][1], ax, b[nt].x);
+          dmma884(acc[mt][nt][1][0], acc[mt][nt][1][1], ax, b[nt].y);
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const double ay = NEG ? -a[mt].y : a[mt].y, nai = -ay;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma884(acc[mt][nt][0][0], acc[mt][nt][0][1], nai, b[nt].y);
+          dmma884(acc[mt][nt][1][0], acc[mt][nt][1][1], ay, b[nt].x);
+        }
+      }
+    }
+  }
+
   // the chunks of the segments (same sequence as produce); NEG: acc -= A op(B)
   template <bool NEG>
   __device__ __forceinline__ void consume(const Seg* seg, int nseg, int Mv, int Nv) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = (int)threadIdx.x >> 5;
     const int wm = warp % WM, wn = warp / WM;
     const int fr = lane >> 2, fc = lane & 3, rf = rho(fr);
     const int mtv = min(MT, max(0, (Mv - wm * MT * 8 + 7) / 8));
     const int ntv = min(NT, max(0, (Nv - wn * NT * 8 + 7) / 8));
+    const bool whole = mtv == MT && ntv == NT;
+    // per-thread fragment offsets inside a stage (fast path): swizzled A / B^T rows, padded B rows
+    const int x0 = (fc ^ rf) << 4, x1 = x0 ^ 64;
+    const int aoff = (wm * MT * 8 + rf) * 128;
+    const int btoff = A_BYTES + (wn * NT * 8 + rf) * 128;
+    const int bnoff = A_BYTES + (fc * SKB + wn * NT * 8 + rf) * 16;
 #pragma unroll 1
     for (int g = 0; g < nseg; ++g) {
       const int K = seg[g].K;
@@ -228,7 +325,12 @@ struct Engine {
         mbar_wait(&full[stage], round & 1);
         const unsigned char* As = st + (size_t)stage * STAGE;
         const unsigned char* Bs = As + A_BYTES;
-        if (mtv > 0 && ntv > 0) {
+        if (whole && kv == KC) {
+          if (bt)
+            chunk_full<NEG, true>(As + aoff + x0, As + aoff + x1, As + btoff + x0, As + btoff + x1);
+          else
+            chunk_full<NEG, false>(As + aoff + x0, As + aoff + x1, As + bnoff, nullptr);
+        } else if (mtv > 0 && ntv > 0) {
 #pragma unroll
           for (int kk = 0; kk < KC; kk += 4) {
             if (kk >= kv) break;
@@ -289,6 +391,6 @@ struct Engine {
   }
 };
 
-using Eng64 = Engine<2, 4, 4, 2, 4>;
+using Eng64 = Engine<2, 4, 4, 2, 4>;   // 8 consumer warps (32 x 16 each), one CTA per SM
 
 }  // namespace dmma

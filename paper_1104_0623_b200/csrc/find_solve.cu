@@ -123,6 +123,7 @@ struct SolveParams {
   int32_t off_sym;  // +1 / -1: Sigma^< exactly Hermitian / skew-Hermitian (then G^< is too), 0 general
   int32_t zskip;    // skip the products of structurally zero (B_r, S_l) blocks (ElimDesc::zsplit)
   int32_t use_tma;  // DMMA tiles of trail / Schur / T / R through the TMA engine (tmaps valid)
+  unsigned long long* tile_ctr;  // one tile counter per launch spec (TMA engine's dynamic tile order)
   const CUtensorMap* tmaps;  // [n_tmap][3]: M, MS, X of each CTA-path elimination (ElimDesc::tmap)
 };
 
@@ -2480,21 +2481,34 @@ __device__ __forceinline__ void tile_store(const SolveParams& P, const Task& t, 
 
 template <int KIND>
 __global__ void __launch_bounds__(TmaEng::THREADS, 1) tile_tma_kernel(SolveParams P, const Task* tasks, int64_t cnt,
-                                                                     int nE, int j, int nb) {
+                                                                     int nE, int j, int nb,
+                                                                     unsigned long long* counter) {
   pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];  // Engine::init aligns to 1024
   TmaEng eng;
   eng.init(smem_raw);
   const int64_t total = cnt * nE;
-  for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
-    const int e = (int)(q / cnt);
-    const Task t = tasks[q % cnt];
-    TileJob J;
-    if (!tile_job<KIND>(P, t, e, j, nb, J)) continue;
-    if (TmaEng::producer()) {
+  // tiles are drawn in order from the launch's counter (zeroed by the solve call): the tiles of
+  // one launch differ in K, in skipped work and in their epilogues
+  if (TmaEng::producer()) {
+    for (;;) {
+      const int64_t q = eng.next_tile_p(counter, total);
+      if (q < 0) break;
+      const int e = (int)(q / cnt);
+      const Task t = tasks[q % cnt];
+      TileJob J;
+      if (!tile_job<KIND>(P, t, e, j, nb, J)) continue;
       TmaEng::prefetch_c(J.cmap, J.cr, J.cc, e);
       eng.produce(J.seg, J.nseg, e, J.nv);
-    } else {
+    }
+  } else {
+    for (;;) {
+      const int64_t q = eng.next_tile_c();
+      if (q < 0) break;
+      const int e = (int)(q / cnt);
+      const Task t = tasks[q % cnt];
+      TileJob J;
+      if (!tile_job<KIND>(P, t, e, j, nb, J)) continue;
       eng.load_c(J.C, P.elims[t.e].n, J.mv, J.nv);
       eng.template consume<true>(J.seg, J.nseg, J.mv, J.nv);
       tile_store<KIND>(P, t, e, j, nb, J, eng);
@@ -2904,6 +2918,8 @@ void launch_cluster(void (*k)(KArgs...), dim3 grid, dim3 block, unsigned cs, siz
 
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;  // dynamic budget (static smem of the kernels < 1 KB)
 size_t ws_header_bytes() { return 256; }
+// tile counters of the TMA engine launches (one per launch spec), at the end of the workspace
+size_t tile_ctr_bytes(const find_plan* P) { return (P->specs.size() * 8 + 255) / 256 * 256 + 256; }
 
 template <int NB>
 size_t xsolve_smem() {
@@ -3238,14 +3254,15 @@ const bool g_tma = [] {
   const char* f = std::getenv("FIND_B200_TMA");
   return !(f && f[0] == '0');
 }();
-// Launch groups that use the engine.  Measured per group on cfg4 / cfg1 (tools/levels_compare.py,
-// profiles/r02_tma_thresholds.txt): the trailing updates (K = 32 / 64, many tiles) gain from the
-// producer running ahead across tiles (cfg4 trail 2092 -> 1989 ms serialized); the long-K
-// Schur / T / R products run faster on the 2-CTA/SM cp.async tiles at every group size, so they
-// keep those unless FIND_B200_TMA_MIN_S lowers the bound.
+// Launch groups that use the engine.  Measured per group on cfg4 / cfg1 (tools/group_kinds.py,
+// gpurun_out/t_gk*: every max_s bucket): with the predicate-free full-chunk path and the dynamic
+// tile order the engine is faster than the 2-CTA/SM cp.async tiles on every Schur / T / R group
+// (cfg4 serialized: rgemm 885 -> 821 ms, schur 522 -> 469, tgemm 391 -> 360) and on the trailing
+// updates (1970 -> 1637 ms), so it runs all of them; FIND_B200_TMA_MIN_S / _TRAIL_MIN_N raise the
+// group-size bounds for A/B runs.
 const int g_tma_min_s = [] {
   const char* f = std::getenv("FIND_B200_TMA_MIN_S");
-  return f ? std::atoi(f) : (1 << 30);
+  return f ? std::atoi(f) : 0;
 }();
 const int g_tma_trail_min_n = [] {
   const char* f = std::getenv("FIND_B200_TMA_TRAIL_MIN_N");
@@ -3388,7 +3405,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         case kLTrail:
           if (prm.use_tma && G.max_n >= g_tma_trail_min_n)
             launch_k(tile_tma_kernel<kLTrail>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
-                     (int64_t)cnt, nE, L.step, L.nb);
+                     (int64_t)cnt, nE, L.step, L.nb, prm.tile_ctr + si);
           else
             launch_k(trail_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.step, L.nb);
           break;
@@ -3404,21 +3421,21 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         case kLTGemm:
           if (prm.use_tma && G.max_s >= g_tma_min_s)
             launch_k(tile_tma_kernel<kLTGemm>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
-                     (int64_t)cnt, nE, 0, L.nb);
+                     (int64_t)cnt, nE, 0, L.nb, prm.tile_ctr + si);
           else
             launch_k(tgemm_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.nb);
           break;
         case kLRGemm:
           if (prm.use_tma && G.max_s >= g_tma_min_s)
             launch_k(tile_tma_kernel<kLRGemm>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
-                     (int64_t)cnt, nE, 0, L.nb);
+                     (int64_t)cnt, nE, 0, L.nb, prm.tile_ctr + si);
           else
             launch_k(rgemm_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.nb);
           break;
         case kLSchur:
           if (prm.use_tma && G.max_s >= g_tma_min_s)
             launch_k(tile_tma_kernel<kLSchur>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
-                     (int64_t)cnt, nE, 0, L.nb);
+                     (int64_t)cnt, nE, 0, L.nb, prm.tile_ctr + si);
           else
             launch_k(schur_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk);
           break;
@@ -3495,6 +3512,8 @@ SolveParams make_params(const find_plan* P, void* ws, int nE) {
   }
   prm.scratch = (double2*)(base + off);
   prm.scratch_elems = P->ws_elems;
+  off += (size_t)nE * P->ws_elems * sizeof(double2);
+  prm.tile_ctr = (unsigned long long*)(base + off);
   prm.n_nodes = P->n;
   return prm;
 }
@@ -3646,6 +3665,7 @@ size_t find_solve_workspace_bytes(const find_plan* P, int32_t nE, int32_t comput
   size_t b = ws_header_bytes();
   for (int a = 0; a < kNumArenas; ++a) b += (size_t)nE * P->arena_elems[a] * sizeof(double2);
   b += (size_t)nE * P->ws_elems * sizeof(double2);
+  b += tile_ctr_bytes(P);
   return b;
 }
 
@@ -3721,6 +3741,7 @@ int find_solve_offdiag_groups(find_plan* P, const void* a_vals, const void* s_va
   if (g_end < 0 || g_end > (int64_t)P->groups.size()) g_end = (int64_t)P->groups.size();
   if (g_begin == 0) CUDA_TRY(cudaMemsetAsync(ws, 0xff, 8, stream));
   if ((rc = ensure_tmaps(P, prm, nE, stream, st))) return rc;
+  if (prm.use_tma) CUDA_TRY(cudaMemsetAsync(prm.tile_ctr, 0, tile_ctr_bytes(P), stream));
   return run_groups(P, prm, g_begin, g_end, nE, stream, st);
 }
 

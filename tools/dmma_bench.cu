@@ -60,6 +60,53 @@ __global__ void __launch_bounds__(E::THREADS, 1) eng_kernel(Prob p, const __grid
   }
 }
 
+// dynamic tile scheduling (global counter), MINB CTAs per SM
+template <class E, int MINB>
+__global__ void __launch_bounds__(E::THREADS, MINB) eng_dyn_kernel(Prob p, const __grid_constant__ Maps maps,
+                                                                   const double2* B, double2* C,
+                                                                   unsigned long long* counter) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  E eng;
+  eng.init(smem_raw);
+  const int tm = (p.M + E::BM - 1) / E::BM, tn = (p.N + E::BN - 1) / E::BN;
+  const long long ntiles = (long long)p.batch * tm * tn;
+  auto job = [&](long long t, dmma::Seg* seg, double2*& Cb, int& bi, int& mv, int& nv) {
+    bi = (int)(t / (tm * tn));
+    const int r = (int)(t % (tm * tn));
+    const int i0 = (r / tn) * E::BM, c0 = (r % tn) * E::BN;
+    mv = min(E::BM, p.M - i0);
+    nv = min(E::BN, p.N - c0);
+    seg[0] = {&maps.a, nullptr, B + (int64_t)bi * p.K * p.N + c0, p.N, i0, 0, 0, 0, p.K, 0};
+    seg[1] = {&maps.a2, &maps.b2, nullptr, 0, i0, 0, c0, 0, p.K, 1};
+    Cb = C + (int64_t)bi * p.M * p.N + (int64_t)i0 * p.N + c0;
+  };
+  if (E::producer()) {
+    for (;;) {
+      const long long t = eng.next_tile_p(counter, ntiles);
+      if (t < 0) break;
+      dmma::Seg seg[2];
+      double2* Cb;
+      int bi, mv, nv;
+      job(t, seg, Cb, bi, mv, nv);
+      eng.produce(seg, p.nseg, bi, nv);
+    }
+  } else {
+    for (;;) {
+      const long long t = eng.next_tile_c();
+      if (t < 0) break;
+      dmma::Seg seg[2];
+      double2* Cb;
+      int bi, mv, nv;
+      job(t, seg, Cb, bi, mv, nv);
+      eng.load_c(Cb, p.N, mv, nv);
+      eng.template consume<true>(seg, p.nseg, mv, nv);
+      eng.for_each([&](int r, int c, double2 v) {
+        if (r < mv && c < nv) Cb[(int64_t)r * p.N + c] = v;
+      });
+    }
+  }
+}
+
 __global__ void naive_kernel(Prob p, const double2* A, const double2* B, const double2* A2, const double2* B2,
                              double2* C) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -82,7 +129,7 @@ __global__ void naive_kernel(Prob p, const double2* A, const double2* B, const d
   C[q] = acc;
 }
 
-template <class E>
+template <class E, int DYN = 0>
 void run(const char* name, Prob p, int sms, bool check) {
   const size_t na = (size_t)p.batch * p.M * p.K, nb = (size_t)p.batch * p.K * p.N, nc = (size_t)p.batch * p.M * p.N;
   std::vector<double2> h(std::max(std::max(na, nb), nc));
@@ -112,14 +159,30 @@ void run(const char* name, Prob p, int sms, bool check) {
     std::exit(1);
   }
   CK(cudaFuncSetAttribute(eng_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)E::SMEM));
+  CK(cudaFuncSetAttribute(eng_dyn_kernel<E, (DYN > 0 ? DYN : 1)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)E::SMEM));
   const int tiles = p.batch * ((p.M + E::BM - 1) / E::BM) * ((p.N + E::BN - 1) / E::BN);
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eng_kernel<E>, E::THREADS, E::SMEM));
+  if (DYN)
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eng_dyn_kernel<E, (DYN > 0 ? DYN : 1)>, E::THREADS,
+                                                     E::SMEM));
+  else
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eng_kernel<E>, E::THREADS, E::SMEM));
   const int grid = std::min(tiles, sms * std::max(per_sm, 1));
+  unsigned long long* counter;
+  CK(cudaMalloc(&counter, 8));
+  auto launch = [&]() {
+    if (DYN) {
+      CK(cudaMemsetAsync(counter, 0, 8));
+      eng_dyn_kernel<E, (DYN > 0 ? DYN : 1)><<<grid, E::THREADS, E::SMEM>>>(p, maps, B, C, counter);
+    } else {
+      eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, maps, B, C);
+    }
+  };
   if (check) {
     CK(cudaMemcpy(C, C0, nc * 16, cudaMemcpyDeviceToDevice));
     CK(cudaMemcpy(Cr, C0, nc * 16, cudaMemcpyDeviceToDevice));
-    eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, maps, B, C);
+    launch();
     CK(cudaGetLastError());
     naive_kernel<<<(unsigned)((nc + 255) / 256), 256>>>(p, A, B, A2, B2, Cr);
     CK(cudaDeviceSynchronize());
@@ -137,16 +200,17 @@ void run(const char* name, Prob p, int sms, bool check) {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   const int reps = 10;
-  eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, maps, B, C);
+  launch();
   CK(cudaEventRecord(e0));
-  for (int r = 0; r < reps; ++r) eng_kernel<E><<<grid, E::THREADS, E::SMEM>>>(p, maps, B, C);
+  for (int r = 0; r < reps; ++r) launch();
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   const double flops = 8.0 * p.batch * (double)p.M * p.N * p.K * p.nseg;
-  std::printf("%-28s BMxBN %3dx%-3d S=%d grid %5d (%d/SM) tiles %6d: %8.3f ms  %6.2f TFLOP/s\n", name, E::BM, E::BN, 0, grid,
-              per_sm, tiles, ms / reps, flops / (ms / reps * 1e-3) / 1e12);
+  std::printf("%-28s BMxBN %3dx%-3d w%d %s grid %5d (%d/SM) tiles %6d: %8.3f ms  %6.2f TFLOP/s\n", name, E::BM, E::BN, E::NW,
+              DYN ? "dyn" : "sta", grid, per_sm, tiles, ms / reps, flops / (ms / reps * 1e-3) / 1e12);
+  if (getenv("DMMA_NO_CUBLAS")) return;
   // cuBLAS ceiling for the first segment
   cublasHandle_t hd;
   cublasCreate(&hd);
@@ -166,6 +230,7 @@ void run(const char* name, Prob p, int sms, bool check) {
   std::printf("%-28s cuBLAS ZGEMM (one segment)                   : %8.3f ms  %6.2f TFLOP/s\n", name, ms / reps,
               8.0 * p.batch * (double)p.M * p.N * p.K / (ms / reps * 1e-3) / 1e12);
   cublasDestroy(hd);
+  cudaFree(counter);
   cudaFree(A);
   cudaFree(B);
   cudaFree(A2);
@@ -178,6 +243,7 @@ void run(const char* name, Prob p, int sms, bool check) {
 using E64x64s4 = dmma::Engine<2, 4, 4, 2, 4>;
 using E64x64s2 = dmma::Engine<2, 4, 4, 2, 2>;
 using E64x64s6 = dmma::Engine<2, 4, 4, 2, 6>;
+using E4w = dmma::Engine<2, 2, 4, 4, 4>;
 
 int main() {
   int sms = 0;
@@ -185,7 +251,16 @@ int main() {
   std::printf("SMs %d\n", sms);
   const Prob trail{4, 3000, 3000, 64, 1, 0}, rgemm{4, 1535, 1535, 2045, 2, 1}, schur{4, 1535, 1535, 2045, 1, 0},
       small{64, 256, 256, 256, 1, 0}, trail_small{64, 200, 200, 32, 1, 0};
-  run<E64x64s4>("trail 4x3000^2 K64", trail, sms, true);
+  if (getenv("DMMA_ONLY")) {  // one launch shape for an ncu capture
+    run<E64x64s4, 1>("rgemm 4x1535^2 K2045x2", rgemm, sms, false);
+    return 0;
+  }
+  for (const Prob& q : {trail, rgemm, schur, small, trail_small}) {
+    const char* nm = q.K == 64 ? "trail K64" : q.nseg == 2 ? "rgemm" : q.K == 2045 ? "schur" : q.K == 256 ? "cfg1 K256" : "trail cfg1 K32";
+    run<E64x64s4, 0>(nm, q, sms, true);
+    run<E64x64s4, 1>(nm, q, sms, true);
+    run<E4w, 1>(nm, q, sms, false);
+  }
   run<E64x64s2>("trail 4x3000^2 K64", trail, sms, false);
   run<E64x64s6>("trail 4x3000^2 K64", trail, sms, false);
   run<E64x64s4>("rgemm 4x1535^2 K2045x2", rgemm, sms, true);
