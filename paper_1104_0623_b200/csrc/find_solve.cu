@@ -737,6 +737,42 @@ struct Tile {
       const double2* As = smem + (kc & 1) * STAGE;
       const double2* Bs = As + BM * kSK;
       const int kv = K - kc * kKC;
+      if (kv >= kKC && mtv == MT && ntv == NT) {
+        // whole chunk, every fragment valid: no predicates; the two DMMAs into one accumulator
+        // are MT*NT*2 instructions apart (each accumulator still sums ax*bx, -ay*by / ax*by, ay*bx
+        // in this order: bit-identical to the general path below)
+#pragma unroll
+        for (int kk = 0; kk < kKC; kk += 4) {
+          double2 a[MT], b[NT];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) a[mt] = As[(wm * MT * 8 + mt * 8 + fr) * kSK + kk + fc];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            b[nt] = Bs[(wn * NT * 8 + nt * 8 + fr) * kSK + kk + fc];
+            if (BT2) b[nt].y = -b[nt].y;
+          }
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const double ax = NEG ? -a[mt].x : a[mt].x;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              dmma(acc[mt][nt][0][0], acc[mt][nt][0][1], ax, b[nt].x);
+              dmma(acc[mt][nt][1][0], acc[mt][nt][1][1], ax, b[nt].y);
+            }
+          }
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const double ay = NEG ? -a[mt].y : a[mt].y, nai = -ay;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              dmma(acc[mt][nt][0][0], acc[mt][nt][0][1], nai, b[nt].y);
+              dmma(acc[mt][nt][1][0], acc[mt][nt][1][1], ay, b[nt].x);
+            }
+          }
+        }
+        __syncthreads();
+        continue;
+      }
 #pragma unroll
       for (int kk = 0; kk < kKC; kk += 4) {
         if (kk >= kv || mtv == 0 || ntv == 0) break;
@@ -1836,6 +1872,246 @@ __global__ void __launch_bounds__(T, 1) panel_cluster_reg_kernel(SolveParams P, 
       S.PERM[0] = s_nd;
       if (s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
     }
+  }
+}
+
+// ---- NB = 32 panel step of a TALL panel in ONE CTA (many concurrent panels: the contact-row
+// eliminations of the deep downward levels, s ~ 1000 with tiny b, hundreds per level).  The
+// cluster kernels above spread one panel over up to 8 SMs and leave each of them idle at the
+// per-column barriers; with more panels than SMs in flight the SM-time is what counts, so here a
+// panel stays on one SM: up to 512 threads x RPT rows each.  The 32 panel columns are processed as
+// four 8-column sub-panels held in registers (column steps: warp argmax, one barrier, pivot row
+// published, one barrier, rank-1 update); after a sub-panel its eight pivot rows' remaining
+// panel columns are solved in shared memory (8 x 24 block) and every other row applies the eight
+// multipliers to its remaining columns, which round-trip through its own row of M except the
+// next sub-panel's eight, which stay in registers (thread-per-row: every thread keeps its own
+// 128-byte row segments in flight; a cooperative lanes-along-columns variant with the
+// multipliers in shared memory measured slower, tools/tall_bench.cu).  Every element sees the
+// same updates in the same order as in panel1_kernel (bit-identical results); rows are staged
+// in MS and written once, to their final positions, at the end.
+constexpr int kTallSP = 8;
+constexpr int kTallMaxT = 512;
+constexpr int tall_threads(int rpt) { return rpt >= 3 ? 352 : kTallMaxT; }  // three rows a thread need > 128 registers
+constexpr int kTallMaxRows = 3 * tall_threads(3);
+template <int RPT>
+__global__ void __launch_bounds__(tall_threads(RPT), 1) panel_tall_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
+  constexpr int NB = 32, SP = kTallSP, MAXW = kTallMaxT / 32;
+  __shared__ double candv[2][MAXW];
+  __shared__ int candi[2][MAXW];
+  __shared__ double2 prow[2][SP + 1];  // pivot row's live sub-panel part + 1/u
+  __shared__ double2 Us[SP][NB - SP];  // the sub-panel's pivot rows, remaining panel columns
+  __shared__ double2 Lp[SP][SP];       // their multipliers inside the sub-panel
+  __shared__ int s_bad, s_nd;
+  __shared__ double s_scale[MAXW];
+  __shared__ double2 s_pval[NB];
+  __shared__ int s_piv[NB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = blockDim.x, NW = T >> 5;
+  const Task t = tasks[blockIdx.x];
+  const int e = blockIdx.y;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s, j = t.a;
+  const int j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
+  const Scr S = scratch_of(P, d, e, NB);
+  double2* M = S.M;
+  bool has[RPT];
+  int pos[RPT];
+  double2 a[RPT][SP];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int r = tid + i * T;
+    has[i] = r < R;
+    pos[i] = r;
+#pragma unroll
+    for (int c = 0; c < SP; ++c) a[i][c] = (has[i] && c < jb) ? M[(int64_t)(j0 + r) * n + j0 + c] : cz();
+  }
+  if (tid == 0) { s_bad = INT32_MAX; s_nd = 0; }
+  double scale;
+  if (j == 0) {
+    scale = 0.0;
+    for (int q = tid; q < (s + kRowChunk - 1) / kRowChunk; q += T) scale = fmax(scale, S.pmax[q]);
+    for (int o = 16; o; o >>= 1) scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
+    if (lane == 0) s_scale[warp] = scale;
+    __syncthreads();
+    scale = s_scale[0];
+    for (int w = 1; w < NW; ++w) scale = fmax(scale, s_scale[w]);
+    if (tid == 0) {
+      *S.scale = scale;
+      if (scale == 0.0) s_bad = 0;
+    }
+  } else {
+    scale = *reinterpret_cast<volatile double*>(S.scale);
+  }
+#pragma unroll 1
+  for (int c0 = 0; c0 < jb; c0 += SP) {
+    const int cw = min(SP, jb - c0);
+#pragma unroll
+    for (int k = 0; k < SP; ++k) {
+      if (k >= cw) break;
+      const int jj = c0 + k, buf = jj & 1;
+      PCLK(0);
+      // this thread's best active row (max |re|+|im|, lowest position), then the warp's
+      int vhi = -1, bpos = INT32_MAX;
+      unsigned vlo = 0;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const double v0 = cabs1(a[i][k]);
+        const double v = v0 >= 0.0 ? v0 : 0.0;  // NaN ranks lowest
+        const int hi = (has[i] && pos[i] >= jj) ? __double2hiint(v) : -1;
+        const unsigned lo = (unsigned)__double2loint(v);
+        if (hi > vhi || (hi == vhi && hi >= 0 && (lo > vlo || (lo == vlo && pos[i] < bpos)))) {
+          vhi = hi;
+          vlo = lo;
+          bpos = pos[i];
+        }
+      }
+      const int mhi = __reduce_max_sync(0xffffffffu, vhi);
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, vhi == mhi ? vlo : 0u);
+      const bool best = vhi >= 0 && vhi == mhi && vlo == mlo;
+      const int wpos = (int)__reduce_min_sync(0xffffffffu, (unsigned)(best ? bpos : INT32_MAX));
+      if (lane == 0) {
+        candv[buf][warp] = mhi < 0 ? -1.0 : __hiloint2double(mhi, (int)mlo);
+        candi[buf][warp] = wpos;
+      }
+      PCLK(1);
+      __syncthreads();
+      PCLK(2);
+      const double cvw = lane < NW ? candv[buf][lane] : -1.0;
+      const int ciw = lane < NW ? candi[buf][lane] : INT32_MAX;
+      const int whi = cvw < 0.0 ? -1 : __double2hiint(cvw);
+      const int bhi = __reduce_max_sync(0xffffffffu, whi);
+      const unsigned wlo = (unsigned)__double2loint(cvw);
+      const unsigned blo = __reduce_max_sync(0xffffffffu, whi == bhi ? wlo : 0u);
+      const int pr0 = (int)__reduce_min_sync(0xffffffffu, (unsigned)((whi == bhi && wlo == blo) ? ciw : INT32_MAX));
+      const int pr = pr0 >= jj && pr0 < R ? pr0 : jj;  // NaN / Inf entries: no interchange
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+        if (has[i] && pos[i] == pr) {
+          prow[buf][SP] = crcp(a[i][k]);
+#pragma unroll
+          for (int c = k; c < SP; ++c) prow[buf][c - k] = a[i][c];
+        }
+      PCLK(3);
+      __syncthreads();
+      PCLK(4);
+      const double2 rinv = prow[buf][SP];
+      if (tid == 0) {
+        s_piv[jj] = pr;
+        s_pval[jj] = prow[buf][0];
+      }
+      double2 pv[SP];
+#pragma unroll
+      for (int c = k + 1; c < SP; ++c) pv[c] = prow[buf][c - k];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        if (has[i] && pos[i] == pr) pos[i] = -1 - jj;  // pivot row of column jj (final position jj)
+        else if (has[i] && pos[i] == jj) pos[i] = pr;
+        if (has[i] && pos[i] > jj) {
+          const double2 l = cmul(a[i][k], rinv);
+          a[i][k] = l;
+#pragma unroll
+          for (int c = k + 1; c < SP; ++c) a[i][c] = cfms(a[i][c], l, pv[c]);
+        }
+      }
+    }
+    const int jj = c0 + SP - 1;  // (clock stamps of the rest phase: slots 5-7 of the sub-panel's last column)
+    (void)jj;
+    PCLK(5);
+    // the sub-panel's columns are final: stage them (L multipliers / U values) in MS
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+      if (has[i] && (pos[i] >= 0 || pos[i] <= -1 - c0)) {  // not earlier sub-panels' pivot rows (staged with their U values)
+        double2* Lst = S.MS + (int64_t)(tid + i * T) * NB + c0;
+#pragma unroll
+        for (int c = 0; c < SP; ++c)
+          if (c < cw) Lst[c] = a[i][c];
+      }
+    const int nrest = jb - (c0 + SP);  // panel columns right of the sub-panel
+    if (nrest <= 0) break;
+    // the sub-panel's pivot rows: raw remaining columns and their multipliers to shared memory
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int kk = -1 - pos[i] - c0;  // pivot index inside the sub-panel
+      if (has[i] && pos[i] < 0 && kk >= 0 && kk < SP) {
+        const double2* src = M + (int64_t)(j0 + tid + i * T) * n + j0 + c0 + SP;
+        for (int c = 0; c < nrest; ++c) Us[kk][c] = src[c];
+#pragma unroll
+        for (int c = 0; c < SP; ++c) Lp[kk][c] = a[i][c];
+      }
+    }
+    __syncthreads();
+    if (tid < nrest) {  // U rows of the sub-panel: row kk minus its multipliers times the rows above
+#pragma unroll
+      for (int kk = 1; kk < SP; ++kk) {
+        double2 u = Us[kk][tid];
+#pragma unroll
+        for (int q = 0; q < kk; ++q) u = cfms(u, Lp[kk][q], Us[q][tid]);
+        Us[kk][tid] = u;
+      }
+    }
+    __syncthreads();
+    PCLK(6);
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      if (!has[i]) continue;
+      const int r = tid + i * T;
+      const int kk = -1 - pos[i] - c0;
+      if (pos[i] < 0 && kk >= 0 && kk < SP) {  // a pivot row of this sub-panel: its U values are final
+        double2* Lst = S.MS + (int64_t)r * NB + c0 + SP;
+        for (int c = 0; c < nrest; ++c) Lst[c] = Us[kk][c];
+      } else if (pos[i] >= 0) {  // still active: apply the eight multipliers to the remaining columns
+        double2* mrow = M + (int64_t)(j0 + r) * n + j0 + c0 + SP;
+        double2 l[SP];
+#pragma unroll
+        for (int q = 0; q < SP; ++q) l[q] = a[i][q];
+#pragma unroll 1
+        for (int cc = 0; cc < nrest; cc += SP) {
+          double2 x[SP];
+#pragma unroll
+          for (int c = 0; c < SP; ++c) x[c] = cc + c < nrest ? mrow[cc + c] : cz();
+#pragma unroll 2
+          for (int q = 0; q < SP; ++q)
+#pragma unroll
+            for (int c = 0; c < SP; ++c) x[c] = cfms(x[c], l[q], Us[q][cc + c]);
+          if (cc == 0) {
+#pragma unroll
+            for (int c = 0; c < SP; ++c) a[i][c] = x[c];  // the next sub-panel stays in registers
+          } else {
+#pragma unroll
+            for (int c = 0; c < SP; ++c)
+              if (cc + c < nrest) mrow[cc + c] = x[c];
+          }
+        }
+      }
+    }
+    PCLK(7);
+    // (Us / Lp are next written after the next sub-panel's column barriers)
+  }
+  __syncthreads();
+  for (int k = tid; k < jb; k += T) {  // pivot rows and the pivot test of kernels.py:241 (abs < rtol * scale)
+    S.PIV[j0 + k] = j0 + s_piv[k];
+    if (cabs(s_pval[k]) < P.rtol * scale) atomicMin(&s_bad, j0 + k);
+  }
+#pragma unroll
+  for (int i = 0; i < RPT; ++i)
+    if (has[i]) {
+      const int r = tid + i * T;
+      const int fp = pos[i] < 0 ? -1 - pos[i] : pos[i];
+      const double2* Lst = S.MS + (int64_t)r * NB;
+      double2* dst = M + (int64_t)(j0 + fp) * n + j0;
+#pragma unroll 8
+      for (int c = 0; c < jb; ++c) dst[c] = Lst[c];
+      if (fp != r) {
+        const int k = atomicAdd(&s_nd, 1);
+        S.PERM[1 + k] = r;
+        S.PERM[1 + 2 * NB + k] = fp;
+      }
+    }
+  __syncthreads();
+  if (tid == 0) {
+    S.PERM[0] = s_nd;
+    if (s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
   }
 }
 
@@ -3234,12 +3510,19 @@ const int g_skip = [] {
 
 // persistent grid of the TMA tile kernels: one CTA per SM at most (a CTA holds ~132 KB of smem)
 int g_num_sms[kMaxDevices] = {};
+// FIND_B200_TMA_SMS: CTAs of a TMA tile launch (default: every SM); fewer leave SMs to the
+// latency-bound launches of the concurrent groups
+const int g_tma_sms = [] {
+  const char* f = std::getenv("FIND_B200_TMA_SMS");
+  return f ? std::atoi(f) : 0;
+}();
 dim3 tma_grid(unsigned cnt, int nE) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (g_num_sms[dev] == 0) cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
   const int64_t total = (int64_t)cnt * nE;
-  return dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(total, g_num_sms[dev])), 1);
+  const int sms = g_tma_sms > 0 ? std::min(g_tma_sms, g_num_sms[dev]) : g_num_sms[dev];
+  return dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(total, sms)), 1);
 }
 
 // NB = 32 panels of more than kRegPanelMaxS rows on register-row clusters (FIND_B200_CREG=0: the
@@ -3267,6 +3550,17 @@ const int g_tma_min_s = [] {
 const int g_tma_trail_min_n = [] {
   const char* f = std::getenv("FIND_B200_TMA_TRAIL_MIN_N");
   return f ? std::atoi(f) : 256;
+}();
+
+// One-CTA tall panels (panel_tall_kernel): for panel steps with more than g_tall_min_rows rows
+// when the launch holds at least g_tall_min_panels (elimination, energy) panels.
+const int g_tall_min_rows = [] {
+  const char* f = std::getenv("FIND_B200_TALL_MIN_ROWS");
+  return f ? std::atoi(f) : (int)kRegPanelMaxS;
+}();
+const int64_t g_tall_min_panels = [] {
+  const char* f = std::getenv("FIND_B200_TALL_MIN_PANELS");
+  return f ? std::atoll(f) : 48;
 }();
 
 const bool g_rsym_down = [] {
@@ -3329,7 +3623,14 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         case kLGatherS: launch_k(gather_kernel<true>, grid, kThreads, 0, stream, prm, tk); break;
         case kLPanel: {
           const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
-          if (L.nb == 32 && g_creg && rmax > (int)kRegPanelMaxS && rmax <= kClusterMax * kRegClusterRows) {
+          if (L.nb == 32 && rmax > g_tall_min_rows && rmax <= kTallMaxRows && (int64_t)cnt * nE >= g_tall_min_panels) {
+            // many tall panels in flight: one CTA per panel (SM-time, not latency, is what counts)
+            const int rpt = rmax <= kTallMaxT ? 1 : (rmax <= 2 * kTallMaxT ? 2 : 3);
+            const int T = 32 * (((rmax + rpt - 1) / rpt + 31) / 32);
+            if (rpt == 1) launch_k(panel_tall_kernel<1>, grid, T, 0, stream, prm, tk);
+            else if (rpt == 2) launch_k(panel_tall_kernel<2>, grid, T, 0, stream, prm, tk);
+            else launch_k(panel_tall_kernel<3>, grid, T, 0, stream, prm, tk);
+          } else if (L.nb == 32 && g_creg && rmax > (int)kRegPanelMaxS && rmax <= kClusterMax * kRegClusterRows) {
             // register rows over a thread-block cluster of cs CTAs
             const unsigned cs = (unsigned)((rmax + kRegClusterRows - 1) / kRegClusterRows);
             const int rows = (rmax + (int)cs - 1) / (int)cs;

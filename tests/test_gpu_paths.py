@@ -82,6 +82,34 @@ def test_structural_zero_skips_are_bit_identical(cuda):
     assert out[0] == out[1]
 
 
+TALL_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, {root!r})
+from paper_1104_0623_b200.configs import build_problem
+from paper_1104_0623_b200.plan import plan_for
+from paper_1104_0623_b200.solver import sigma_symmetry, solve_values
+p = build_problem({nx}, {ny}, [0.9, 2.7], seed=23, stencil=5)
+plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
+gr, gl, _, _ = solve_values(plan, p.a_vals_all(), p.s_vals, sigma_sym=sigma_symmetry(p.sigma_csr()))
+print("HASH", hashlib.sha1(gr.tobytes() + gl.tobytes()).hexdigest())
+"""
+
+
+@pytest.mark.parametrize("nx,ny", [(96, 40), (600, 12), (1030, 6)])
+def test_tall_panel_kernel_is_bit_identical(cuda, nx, ny):
+    """One-CTA tall panels (1, 2 and 3 rows per thread: dense contact rows of 96 / 600 / 1030 nodes) against
+    the register-row CTA / cluster panels: same pivots, same per-element update order, same bits."""
+    code = TALL_SCRIPT.format(root=str(ROOT), nx=nx, ny=ny)
+    out = []
+    for env in ({"FIND_B200_TALL_MIN_PANELS": "0", "FIND_B200_TALL_MIN_ROWS": "32"},
+                {"FIND_B200_TALL_MIN_PANELS": "1000000000"}):
+        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                           timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out.append([l for l in r.stdout.splitlines() if l.startswith("HASH")][-1])
+    assert out[0] == out[1]
+
+
 @pytest.mark.gpu
 def test_two_devices_in_one_process():
     """Kernel attributes and side streams are per device: a solve on cuda:0 then on cuda:1 (needs 2 GPUs)."""
