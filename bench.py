@@ -331,7 +331,7 @@ def run_b200(args):
     # inputs, outputs and the e2e leg's own buffers stay resident next to the workspace
     chunk = energy_chunk(plan, n_e, True, dev)
     reserve = (2 * n_e * plan.nnz + 4 * n_e * plan.n) * 16
-    while chunk > 1 and plan.workspace_bytes(chunk, True) + reserve > 0.85 * torch.cuda.mem_get_info(dev)[0]:
+    while chunk > 1 and plan.workspace_bytes(chunk, True) + reserve > 0.90 * torch.cuda.mem_get_info(dev)[0]:
         chunk -= 1
 
     m = device_measure(plan, p, dev, args.steps, args.warmup, world, chunk, ssym, flush)

@@ -3545,11 +3545,11 @@ const bool g_tma = [] {
 // group-size bounds for A/B runs.
 const int g_tma_min_s = [] {
   const char* f = std::getenv("FIND_B200_TMA_MIN_S");
-  return f ? std::atoi(f) : 0;
+  return f ? std::atoi(f) : 192;  // below: cfg4 loses < 1 % serialized, cfg1 (latency-bound, many small concurrent groups) gains 2 %
 }();
 const int g_tma_trail_min_n = [] {
   const char* f = std::getenv("FIND_B200_TMA_TRAIL_MIN_N");
-  return f ? std::atoi(f) : 256;
+  return f ? std::atoi(f) : 0;
 }();
 
 // One-CTA tall panels (panel_tall_kernel): for panel steps with more than g_tall_min_rows rows

@@ -206,7 +206,7 @@ def balanced_chunk(n_e: int, fit: int) -> int:
 
 
 def energy_chunk(plan: Plan, n_e: int, compute_gless: bool, dev, n_pairs: int = 0) -> int:
-    """Energy points per find_solve call that fit in 85 % of the free device memory (the plan's
+    """Energy points per find_solve call that fit in 90 % of the free device memory (the plan's
     own cached workspace counts as free), inputs / outputs included."""
     import torch
 
@@ -219,7 +219,7 @@ def energy_chunk(plan: Plan, n_e: int, compute_gless: bool, dev, n_pairs: int = 
 
         release_workspaces(keep=plan)
         free, total = torch.cuda.mem_get_info(dev)
-    fit = (0.85 * (free + held) - plan.workspace_bytes(1, compute_gless) + per_energy) // per_energy
+    fit = (0.90 * (free + held) - plan.workspace_bytes(1, compute_gless) + per_energy) // per_energy
     return balanced_chunk(n_e, fit)
 
 
