@@ -222,6 +222,30 @@ int find_schur_sigma_update(int32_t s, int32_t b, const void* ass, const void* a
                             const void* sbb, double pivot_rtol, void* u_out, void* r_out, void* l_out,
                             int32_t force_path, void* stream, find_status* st);
 
+/* ---- Dense batched primitives on the FIND kernels (the RGF comparison path,
+ * find_selinv/rgf.py:108-208: g_i = (D_i - F g E)^-1 and the G / Sigma sandwiches).
+ *
+ * find_dense: batched inverse of `batch` complex128 n x n matrices (row-major, contiguous,
+ * device).  Each matrix is one blocked elimination of [[A, I], [I, 0]] by the same panel /
+ * TRSM / DMMA kernels as find_solve (replaces numpy.linalg.inv at rgf.py:84-87); the handle owns
+ * the one-elimination plan and its workspace.  find_dense_inverse is asynchronous on `stream`;
+ * status_out (device, 8 bytes, may be NULL) receives the call's status word: all ones when
+ * every pivot was nonzero, else (energy << 16 | position) of the first zero pivot. */
+typedef struct find_dense find_dense;
+int find_dense_create(int32_t n, int32_t batch, find_dense** out, find_status* st);
+void find_dense_destroy(find_dense* h);
+int find_dense_inverse(find_dense* h, const void* a, void* inv_out, void* status_out, void* stream,
+                       find_status* st);
+
+/* Strided-batched complex128 GEMM on the DMMA tiles (replaces the `@` products of
+ * rgf.py:92-105, 121-136, 139-208): C[i] (mode 0: =, +1: +=, -1: -=) A[i] op(B[i]) for
+ * i < batch, A [m][k] row stride lda, B [k][n] row stride ldb (b_conj_trans = 0) or B [n][k]
+ * used as its conjugate transpose (b_conj_trans = 1), C [m][n] row stride ldc; sa / sb / sc are
+ * the batch strides in complex elements (0 broadcasts an operand). */
+int find_zgemm_batched(int32_t batch, int32_t m, int32_t n, int32_t k, const void* a, int64_t lda, int64_t sa,
+                       const void* b, int64_t ldb, int64_t sb, int32_t b_conj_trans, void* c, int64_t ldc,
+                       int64_t sc, int32_t mode, void* stream, find_status* st);
+
 #ifdef __cplusplus
 }
 #endif

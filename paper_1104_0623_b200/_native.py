@@ -26,7 +26,7 @@ EXPORTED = (
     "find_schur_sigma_update", "find_plan_exception_slots", "find_plan_specs", "find_solve_timing_enable",
     "find_solve_timing_read", "find_plan_group_phases", "find_solve_timing_read2", "find_plan_offdiag_pairs",
     "find_solve_offdiag", "find_solve_offdiag_groups", "find_plan_elim_splits", "find_plan_elim_out",
-    "find_plan_arena_elems",
+    "find_plan_arena_elems", "find_dense_create", "find_dense_destroy", "find_dense_inverse", "find_zgemm_batched",
 )
 
 
@@ -89,6 +89,10 @@ def lib():
         "find_solve_timing_enable": (None, [i32]),
         "find_solve_timing_read": (i64, [pi32, pi32, C.POINTER(C.c_float), i64]),
         "find_schur_sigma_update": (i32, [i32, i32, P, P, P, P, P, P, P, P, dbl, P, P, P, i32, P, st]),
+        "find_dense_create": (i32, [i32, i32, C.POINTER(P), st]),
+        "find_dense_destroy": (None, [P]),
+        "find_dense_inverse": (i32, [P, P, P, P, P, st]),
+        "find_zgemm_batched": (i32, [i32, i32, i32, i32, P, i64, i64, P, i64, i64, i32, P, i64, i64, i32, P, st]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -2792,6 +2792,66 @@ __global__ void __launch_bounds__(TmaEng::THREADS, 1) tile_tma_kernel(SolveParam
   }
 }
 
+// ================================================================== dense batched primitives
+// The block-tridiagonal RGF comparison path (find_selinv/rgf.py:108-208) runs on the same DMMA
+// tiles and elimination kernels as FIND: a strided-batched complex GEMM and a batched dense
+// inverse (the Schur complement of [[A, I], [I, 0]] is -A^-1: one blocked elimination per matrix).
+struct GemmArgs {
+  const double2* A;  // [m][k], row stride lda, batch stride sa
+  const double2* B;  // [k][n] (bt = 0) or [n][k], used as its conjugate transpose (bt = 1)
+  double2* C;        // [m][n]
+  int64_t lda, sa, ldb, sb, ldc, sc;
+  int m, n, k, bt, mode;  // mode 0: C = AB;  +1: C += AB;  -1: C -= AB
+};
+
+__global__ void __launch_bounds__(kThreads, 2) zgemm_kernel(GemmArgs g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  const int tn = (g.n + kTile - 1) / kTile;
+  const int i0 = (blockIdx.x / tn) * kTile, c0 = (blockIdx.x % tn) * kTile;
+  const int mv = min(kTile, g.m - i0), nv = min(kTile, g.n - c0);
+  const double2* A = g.A + (int64_t)blockIdx.y * g.sa + (int64_t)i0 * g.lda;
+  const double2* B = g.B + (int64_t)blockIdx.y * g.sb + (g.bt ? (int64_t)c0 * g.ldb : (int64_t)c0);
+  double2* C = g.C + (int64_t)blockIdx.y * g.sc + (int64_t)i0 * g.ldc + c0;
+  Tile64 T;
+  if (g.mode != 0) T.load_c(C, g.ldc, mv, nv);
+  else T.zero();
+  if (g.bt) {
+    if (g.mode < 0) T.mma<true, true>(A, g.lda, B, g.ldb, mv, nv, g.k, smem);
+    else T.mma<true, false>(A, g.lda, B, g.ldb, mv, nv, g.k, smem);
+  } else {
+    if (g.mode < 0) T.mma<false, true>(A, g.lda, B, g.ldb, mv, nv, g.k, smem);
+    else T.mma<false, false>(A, g.lda, B, g.ldb, mv, nv, g.k, smem);
+  }
+  T.for_each([&](int r, int c, double2 v) {
+    if (r < mv && c < nv) C[(int64_t)r * g.ldc + c] = v;
+  });
+}
+
+// merged block [[A, I], [I, 0]] (2n x 2n, row-major) of every matrix of the batch
+__global__ void __launch_bounds__(kThreads) dense_pack_kernel(const double2* a, double2* up, int64_t up_stride, int n) {
+  const int n2 = 2 * n;
+  double2* M = up + (int64_t)blockIdx.y * up_stride;
+  const double2* A = a + (int64_t)blockIdx.y * n * n;
+  for (int64_t q = blockIdx.x * (int64_t)kThreads + threadIdx.x; q < (int64_t)n2 * n2; q += (int64_t)gridDim.x * kThreads) {
+    const int i = (int)(q / n2), j = (int)(q % n2);
+    double2 v = cz();
+    if (i < n && j < n) v = A[(int64_t)i * n + j];
+    else if ((i < n && j == i + n) || (j < n && i == j + n)) v = make_double2(1.0, 0.0);
+    M[q] = v;
+  }
+}
+
+// A^-1 = -(Schur complement)
+__global__ void __launch_bounds__(kThreads) dense_unpack_kernel(const double2* u, int64_t u_stride, double2* out, int n) {
+  const double2* U = u + (int64_t)blockIdx.y * u_stride;
+  double2* O = out + (int64_t)blockIdx.y * n * n;
+  for (int64_t q = blockIdx.x * (int64_t)kThreads + threadIdx.x; q < (int64_t)n * n; q += (int64_t)gridDim.x * kThreads) {
+    const double2 v = U[q];
+    O[q] = make_double2(-v.x, -v.y);
+  }
+}
+
 // ---- final leaf step epilogue, warp per (leaf, energy)
 __device__ void final_body_warp(const SolveParams& P, const Task& t, int e, double2* uf, int cmax, int lane) {
   const ElimDesc d = P.elims[t.e];
@@ -3223,6 +3283,7 @@ int set_attrs(find_status* st) {
   if (g_attrs_done[dev]) return FIND_OK;
   const int mx = (int)kMaxSmem;
   CUDA_TRY(cudaFuncSetAttribute(small_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(mid_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(warp_panel_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -4265,6 +4326,126 @@ int find_schur_sigma_update(int32_t s, int32_t b, const void* ass, const void* a
   find_plan_free_device(&Q);
   if (ce != cudaSuccess) return fail_status(st, FIND_ECUDA, cudaGetErrorString(ce));
   return out;
+}
+
+// ---- dense batched primitives (include/find_b200.h)
+struct find_dense {
+  find_plan Q;
+  int32_t n = 0, batch = 0;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  int device = -1;
+};
+
+void find_dense_destroy(find_dense* H) {
+  if (!H) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (H->device >= 0 && H->device != cur) cudaSetDevice(H->device);
+  if (H->ws) cudaFree(H->ws);
+  find_plan_free_device(&H->Q);
+  if (H->device >= 0 && H->device != cur) cudaSetDevice(cur);
+  delete H;
+}
+
+int find_dense_create(int32_t n, int32_t batch, find_dense** out, find_status* st) {
+  status_ok(st);
+  if (!out || n < 1 || batch < 1 || batch > 0xffff) return fail_status(st, FIND_EINVAL, "invalid sizes");
+  find_dense* H = new find_dense;
+  H->n = n;
+  H->batch = batch;
+  const int n2 = 2 * n;
+  find_plan& Q = H->Q;
+  Q.n = n2;
+  Q.nnz = 0;
+  ElimDesc d;
+  std::memset(&d, 0, sizeof(d));
+  d.s = n; d.b = n; d.n = n2; d.p = n2; d.kind = kUpMerge; d.label = 1;
+  d.left_arena = kArenaUp; d.left_off = 0; d.right_arena = kArenaNone; d.right_off = -1;
+  d.out_arena = kArenaDown0; d.out_off = 0;
+  d.map_off = 0; d.rank_off = n2; d.sprow_off = n2 + n; d.sparse_off = 0; d.nsparse = 0; d.ws_off = 0;
+  Q.i32.resize((size_t)n2 + n + n2 + 1, 0);
+  for (int k = 0; k < n2; ++k) Q.i32[k] = k;
+  for (int k = 0; k < n; ++k) Q.i32[n2 + k] = k;
+  Q.elims.push_back(d);
+  Q.slabels.assign((size_t)n, 0);
+  for (int k = 0; k < n; ++k) Q.slabels[k] = k;
+  LaunchGroup G;
+  std::memset(&G, 0, sizeof(G));
+  const int path = n2 <= 32 ? 0 : (n2 <= kMidMaxN ? 2 : 1);
+  G.begin = 0; G.end = 1; G.path = path; G.max_n = n2; G.max_s = n; G.max_b = n;
+  G.nb = path == 1 ? pick_nb_host(n) : 0;
+  if (path == 1 && G.nb == 0) {
+    delete H;
+    return fail_status(st, FIND_EINVAL, "block too large");
+  }
+  G.ws_elems = path == 1 ? find_scratch_elems(n2, n, G.nb) : 0;
+  Q.groups.push_back(G);
+  Q.arena_elems[kArenaUp] = 2 * (int64_t)n2 * n2;
+  Q.arena_elems[kArenaDown0] = 2 * (int64_t)n * n + 2;
+  Q.arena_elems[kArenaDown1] = 0;
+  Q.arena_elems[kArenaDown2] = 0;
+  Q.ws_elems = G.ws_elems;
+  find_build_tasks(&Q);
+  int rc = find_plan_upload(&Q, st);
+  if (rc) { find_dense_destroy(H); return rc; }
+  cudaGetDevice(&H->device);
+  H->ws_bytes = find_solve_workspace_bytes(&Q, batch, 0);
+  cudaError_t ce = cudaMalloc(&H->ws, H->ws_bytes);
+  if (ce != cudaSuccess) {
+    find_dense_destroy(H);
+    return fail_status(st, FIND_ENOMEM, cudaGetErrorString(ce));
+  }
+  if ((ce = cudaMemset(H->ws, 0, H->ws_bytes)) != cudaSuccess) {
+    find_dense_destroy(H);
+    return fail_status(st, FIND_ECUDA, cudaGetErrorString(ce));
+  }
+  *out = H;
+  return FIND_OK;
+}
+
+int find_dense_inverse(find_dense* H, const void* a, void* inv_out, void* status_out, void* stream_, find_status* st) {
+  status_ok(st);
+  if (!H || !a || !inv_out) return fail_status(st, FIND_EINVAL, "invalid argument");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  SolveParams prm = make_params(&H->Q, H->ws, H->batch);
+  prm.compute_gless = 0;
+  prm.rtol = 1e-300;  // LAPACK getrf semantics: only an exactly zero pivot is singular
+  prm.a_vals = prm.arena[kArenaUp];  // unused: no sparse entries
+  prm.s_vals = prm.arena[kArenaUp];
+  prm.s_broadcast = 1;
+  const int n = H->n, n2 = 2 * n;
+  CUDA_TRY(cudaMemsetAsync(H->ws, 0xff, 8, stream));
+  const unsigned gx = (unsigned)std::min<int64_t>(((int64_t)n2 * n2 + kThreads - 1) / kThreads, 1184);
+  dense_pack_kernel<<<dim3(gx, (unsigned)H->batch), kThreads, 0, stream>>>((const double2*)a, prm.arena[kArenaUp],
+                                                                         H->Q.arena_elems[kArenaUp], n);
+  CUDA_TRY(cudaGetLastError());
+  int rc = run_groups(&H->Q, prm, 0, 1, H->batch, stream, st);
+  if (rc) return rc;
+  dense_unpack_kernel<<<dim3(gx, (unsigned)H->batch), kThreads, 0, stream>>>(prm.arena[kArenaDown0],
+                                                                           H->Q.arena_elems[kArenaDown0],
+                                                                           (double2*)inv_out, n);
+  CUDA_TRY(cudaGetLastError());
+  if (status_out) CUDA_TRY(cudaMemcpyAsync(status_out, H->ws, 8, cudaMemcpyDeviceToDevice, stream));
+  return FIND_OK;
+}
+
+int find_zgemm_batched(int32_t batch, int32_t m, int32_t n, int32_t k, const void* A, int64_t lda, int64_t sa,
+                       const void* B, int64_t ldb, int64_t sb, int32_t b_conj_trans, void* C, int64_t ldc, int64_t sc,
+                       int32_t mode, void* stream_, find_status* st) {
+  status_ok(st);
+  if (batch < 1 || m < 1 || n < 1 || k < 0 || !A || !B || !C || batch > 0xffff)
+    return fail_status(st, FIND_EINVAL, "invalid argument");
+  int rc = set_attrs(st);
+  if (rc) return rc;
+  GemmArgs g;
+  g.A = (const double2*)A; g.B = (const double2*)B; g.C = (double2*)C;
+  g.lda = lda; g.sa = sa; g.ldb = ldb; g.sb = sb; g.ldc = ldc; g.sc = sc;
+  g.m = m; g.n = n; g.k = k; g.bt = b_conj_trans ? 1 : 0; g.mode = mode;
+  const unsigned tiles = (unsigned)(((m + kTile - 1) / kTile) * ((n + kTile - 1) / kTile));
+  zgemm_kernel<<<dim3(tiles, (unsigned)batch), kThreads, Tile64::SMEM, (cudaStream_t)stream_>>>(g);
+  CUDA_TRY(cudaGetLastError());
+  return FIND_OK;
 }
 
 }  // extern "C"

@@ -10,11 +10,13 @@ F_i = A(line_{i+1}, line_i).  The recurrences are those of the reference:
     G^<: right-connected g^R, left/right-connected scattering blocks and
          G_ii R_i G_ii^H with R_i = S^L_i + S^R_i - S_ii                       (rgf.py:139-208)
 
-Every step is batched over all energy points: one cuSOLVER batched inverse and a few
-cuBLAS ZGEMMs per mesh line (library GEMM / inverse through torch on the device; this
-is the comparison path, the FIND path is the hand-written one).  The ledger follows the
-reference's charging rules (rgf.py:89-107: inverse c^3, products skipped when the
-coupling block is diagonal).
+Every step is batched over all energy points and runs on the library's own kernels
+through the C ABI (include/find_b200.h): the inverses are find_dense_inverse (one blocked
+elimination of [[A, I], [I, 0]] per matrix on the FIND panel / TRSM / DMMA kernels), the
+products find_zgemm_batched (DMMA tiles, the subtraction / addition of the recurrences
+folded into the accumulator); torch only holds the buffers and does the diagonal
+scalings and element-wise sums.  The ledger follows the reference's charging rules
+(rgf.py:89-107: inverse c^3, products skipped when the coupling block is diagonal).
 """
 
 from __future__ import annotations
@@ -110,14 +112,72 @@ def _is_diag_batch(X) -> bool:
     return not bool(torch.any(off != 0))
 
 
-def _inv(X, line: int, infos: list):
-    """Batched inverse; the singularity flags are collected and checked once per sweep
-    (no host synchronisation per line)."""
-    import torch
+class _Dense:
+    """The C-ABI dense primitives on torch buffers: batched inverse (one handle per (n, batch),
+    cached) and strided-batched GEMM, both asynchronous on torch's current stream."""
 
-    out, info = torch.linalg.inv_ex(X)
-    infos.append((line, info))
-    return out
+    _handles: dict = {}
+
+    def __init__(self, n: int, batch: int, dev):
+        import ctypes as C
+        import torch
+
+        from . import _native
+
+        self.L = _native.lib()
+        self.C = C
+        self.n, self.batch, self.dev = n, batch, dev
+        key = (n, batch, dev.index)
+        if key not in _Dense._handles:
+            if len(_Dense._handles) >= 4:  # a few (n, batch) shapes at most: free the oldest workspace
+                old = next(iter(_Dense._handles))
+                self.L.find_dense_destroy(_Dense._handles.pop(old))
+            h = C.c_void_p()
+            st = _native.FindStatus()
+            rc = self.L.find_dense_create(n, batch, C.byref(h), C.byref(st))
+            if rc != 0:
+                raise NativeLibraryError(f"find_dense_create failed: {st.text}")
+            _Dense._handles[key] = h
+        self.h = _Dense._handles[key]
+        self.stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        self._native = _native
+
+    def inv(self, X, line: int, infos: list):
+        """Batched inverse; the status words are collected and checked once per sweep
+        (no host synchronisation per line)."""
+        import torch
+
+        X = X.contiguous()
+        out = torch.empty_like(X)
+        word = torch.empty(1, dtype=torch.int64, device=self.dev)
+        st = self._native.FindStatus()
+        rc = self.L.find_dense_inverse(self.h, X.data_ptr(), out.data_ptr(), word.data_ptr(), self.stream,
+                                       self.C.byref(st))
+        if rc != 0:
+            raise NativeLibraryError(f"find_dense_inverse failed: {st.text}")
+        infos.append((line, word))
+        return out
+
+    def mm(self, A, B, acc=None, mode: int = 0, bh: bool = False):
+        """A @ B (mode 0), acc + A @ B (+1) or acc - A @ B (-1) per energy point; bh: B is used as its
+        conjugate transpose.  A / B / acc: [nE or 1, n, n] complex128 on the device (a leading 1 broadcasts)."""
+        import torch
+
+        A, B = A.contiguous(), B.contiguous()
+        n = self.n
+        ne = max(A.shape[0], B.shape[0], acc.shape[0] if acc is not None else 1)
+        out = torch.empty((ne, n, n), dtype=torch.complex128, device=self.dev)
+        if acc is not None:
+            out.copy_(acc)  # broadcasts a leading 1
+        st = self._native.FindStatus()
+        sa = 0 if A.shape[0] == 1 and ne > 1 else n * n
+        sb = 0 if B.shape[0] == 1 and ne > 1 else n * n
+        rc = self.L.find_zgemm_batched(ne, n, n, n, A.data_ptr(), n, sa, B.data_ptr(), n, sb, 1 if bh else 0,
+                                       out.data_ptr(), n, n * n, mode if acc is not None else 0, self.stream,
+                                       self.C.byref(st))
+        if rc != 0:
+            raise NativeLibraryError(f"find_zgemm_batched failed: {st.text}")
+        return out
 
 
 def _check_infos(infos: list):
@@ -125,18 +185,21 @@ def _check_infos(infos: list):
 
     if not infos:
         return
-    bad = torch.stack([i for _, i in infos]).ne(0).any(dim=1).nonzero()
+    bad = torch.cat([w for _, w in infos]).ne(-1).nonzero()
     if bad.numel():
         raise SingularPivotError(f"singular recurrence block at line {infos[int(bad[0, 0])][0]}")
     infos.clear()
 
 
-def _sandwich(L, Mid, R, ldiag: bool, rdiag: bool):
-    """L @ Mid @ R with diagonal factors applied as scalings (rgf.py:92-105)."""
+def _sandwich(dn, L, Mid, R, ldiag: bool, rdiag: bool, acc=None, mode: int = 0):
+    """L @ Mid @ R with diagonal factors applied as scalings (rgf.py:92-105); with acc / mode the
+    result is added to (+1) or subtracted from (-1) acc inside the last product."""
     t = Mid
-    t = t * L.diagonal(dim1=-2, dim2=-1).unsqueeze(-1) if ldiag else L @ t
-    t = t * R.diagonal(dim1=-2, dim2=-1).unsqueeze(-2) if rdiag else t @ R
-    return t
+    t = t * L.diagonal(dim1=-2, dim2=-1).unsqueeze(-1) if ldiag else dn.mm(L, t)
+    if rdiag:
+        t = t * R.diagonal(dim1=-2, dim2=-1).unsqueeze(-2)
+        return t if acc is None else (acc + t if mode > 0 else acc - t)
+    return dn.mm(t, R, acc, mode)
 
 
 def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
@@ -155,6 +218,7 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
         _check_tridiagonal(m, nx)
     led = FlopLedger()  # forward + backward: rgf_gr_diag's charges
     infos: list = []
+    dn = _Dense(nx, len(mats), dev)
     D, E, F = _blocks_device(mats, nx, ny, dev)
     ediag = [_is_diag_batch(E[:, i]) for i in range(ny - 1)]
     fdiag = [_is_diag_batch(F[:, i]) for i in range(ny - 1)]
@@ -168,11 +232,11 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
 
     # forward: left-connected g_i (rgf.py:108-115)
     gl_blk = [None] * ny
-    gl_blk[0] = _inv(D[:, 0], 0, infos)
+    gl_blk[0] = dn.inv(D[:, 0], 0, infos)
     led.add("rgf", c3)
     for i in range(1, ny):
-        gl_blk[i] = _inv(D[:, i] - _sandwich(F[:, i - 1], gl_blk[i - 1], E[:, i - 1], fdiag[i - 1], ediag[i - 1]), i,
-                         infos)
+        gl_blk[i] = dn.inv(_sandwich(dn, F[:, i - 1], gl_blk[i - 1], E[:, i - 1], fdiag[i - 1], ediag[i - 1],
+                                     D[:, i], -1), i, infos)
         charge_sandwich(fdiag[i - 1], ediag[i - 1])
         led.add("rgf", c3)
     led_forward = FlopLedger(led.multiplications, dict(led.by_kernel))
@@ -181,9 +245,9 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
     g_full = gl_blk[ny - 1]
     gr[:, (ny - 1) * nx:] = g_full.diagonal(dim1=-2, dim2=-1)
     for i in range(ny - 2, -1, -1):
-        t = _sandwich(E[:, i], g_full, F[:, i], ediag[i], fdiag[i])
+        t = _sandwich(dn, E[:, i], g_full, F[:, i], ediag[i], fdiag[i])
         charge_sandwich(ediag[i], fdiag[i])
-        g_full = gl_blk[i] + (gl_blk[i] @ t) @ gl_blk[i]
+        g_full = dn.mm(dn.mm(gl_blk[i], t), gl_blk[i], gl_blk[i], +1)
         led.add("rgf", 2 * c3)
         gr[:, i * nx:(i + 1) * nx] = g_full.diagonal(dim1=-2, dim2=-1)
     _check_infos(infos)
@@ -204,10 +268,10 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
     lo_nz[(sc.col // nx)[nzm & (sc.row // nx == sc.col // nx + 1)]] = True
     # right-connected g^R (rgf.py:164-168; its ledger repeats the forward one)
     gr_blk = [None] * ny
-    gr_blk[ny - 1] = _inv(D[:, ny - 1], ny - 1, infos)
+    gr_blk[ny - 1] = dn.inv(D[:, ny - 1], ny - 1, infos)
     led.add("rgf", c3)
     for i in range(ny - 2, -1, -1):
-        gr_blk[i] = _inv(D[:, i] - _sandwich(E[:, i], gr_blk[i + 1], F[:, i], ediag[i], fdiag[i]), i, infos)
+        gr_blk[i] = dn.inv(_sandwich(dn, E[:, i], gr_blk[i + 1], F[:, i], ediag[i], fdiag[i], D[:, i], -1), i, infos)
         charge_sandwich(ediag[i], fdiag[i])
         led.add("rgf", c3)
 
@@ -228,15 +292,14 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
                 if cdiag:
                     l_fac = coup.diagonal(dim1=-2, dim2=-1).unsqueeze(-1) * g_conn[prev]
                 else:
-                    l_fac = coup @ g_conn[prev]
+                    l_fac = dn.mm(coup, g_conn[prev])
                     led.add("rgf", c3)
-                lh = l_fac.conj().transpose(-2, -1)
-                term = SD[:, i] + (l_fac @ s_conn[prev]) @ lh
+                term = dn.mm(dn.mm(l_fac, s_conn[prev]), l_fac, SD[:, i], +1, bh=True)
                 led.add("rgf", 2 * c3)
                 if nz_sb:
-                    term = term - l_fac @ sig_sb
+                    term = dn.mm(l_fac, sig_sb, term, -1)
                 if nz_bs:
-                    term = term - sig_bs @ lh
+                    term = dn.mm(sig_bs, l_fac, term, -1, bh=True)
                 s_conn[i] = term
             prev = i
         return s_conn
@@ -245,17 +308,17 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
     s_right = connected(gr_blk, True)
     gless = torch.empty_like(gr)
     for i in range(ny):  # rgf.py:193-207
-        u = D[:, i].clone()
+        u = D[:, i]
         if i > 0:
-            u = u - _sandwich(F[:, i - 1], gl_blk[i - 1], E[:, i - 1], fdiag[i - 1], ediag[i - 1])
+            u = _sandwich(dn, F[:, i - 1], gl_blk[i - 1], E[:, i - 1], fdiag[i - 1], ediag[i - 1], u, -1)
             charge_sandwich(fdiag[i - 1], ediag[i - 1])
         if i + 1 < ny:
-            u = u - _sandwich(E[:, i], gr_blk[i + 1], F[:, i], ediag[i], fdiag[i])
+            u = _sandwich(dn, E[:, i], gr_blk[i + 1], F[:, i], ediag[i], fdiag[i], u, -1)
             charge_sandwich(ediag[i], fdiag[i])
         r_i = s_left[i] + s_right[i] - SD[:, i]
-        g_ii = _inv(u, i, infos)
+        g_ii = dn.inv(u, i, infos)
         led.add("rgf", c3)
-        gless[:, i * nx:(i + 1) * nx] = ((g_ii @ r_i) @ g_ii.conj().transpose(-2, -1)).diagonal(dim1=-2, dim2=-1)
+        gless[:, i * nx:(i + 1) * nx] = dn.mm(dn.mm(g_ii, r_i), g_ii, bh=True).diagonal(dim1=-2, dim2=-1)
         led.add("rgf", 2 * c3)
     _check_infos(infos)
     return gr.cpu().numpy(), gless.cpu().numpy(), {"gr": led_gr, "gless": led}

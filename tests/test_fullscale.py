@@ -86,3 +86,21 @@ def test_gpu_fullscale_parity(cuda, cfg):
     for k, (eg, el) in zip(ks, errs):
         assert eg <= TOL and el <= TOL, (cfg, k, eg, el)
     assert worst <= TOL
+
+
+@pytest.mark.gpu
+def test_gpu_rgf_fullscale_cfg3(cuda):
+    """The GPU RGF path (find_dense_inverse / find_zgemm_batched kernels) against the reference RGF
+    at full size: 256 x 1024, energies 0 and 31, every entry."""
+    from paper_1104_0623_b200 import Mesh, SparseOperator
+    from paper_1104_0623_b200.configs import config_problem
+    from paper_1104_0623_b200.rgf import rgf_batch
+
+    f = _fixture(3)
+    p = config_problem(3)
+    ks = [int(k) for k in f["energy_idx"]]
+    gr, gl, _ = rgf_batch(Mesh(p.nx, p.ny), [SparseOperator(p.a_csr(k)) for k in ks], SparseOperator(p.sigma_csr()))
+    for i, k in enumerate(ks):
+        eg, el = rel_err(gr[i], f["gr"][i]), rel_err(gl[i], f["gl"][i])
+        print(f"cfg3 RGF energy {k}: gr {eg:.2e} gl {el:.2e}")
+        assert eg <= TOL and el <= TOL, (k, eg, el)

@@ -1,5 +1,5 @@
 """FIND vs RGF on the B200 (the paper's crossover question): energy
-points/s of the GPU RGF path (paper_1104_0623_b200.rgf, cuBLAS/cuSOLVER through torch) next
+points/s of the GPU RGF path (paper_1104_0623_b200.rgf, find_dense_inverse / find_zgemm_batched) next
 to the FIND path (solve_values), per BASELINE config.  One JSON line per config.
 
     python tools/rgf_crossover.py [--configs 0,1,2,3] [--chunk 8]
