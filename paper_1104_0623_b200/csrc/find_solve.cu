@@ -996,143 +996,7 @@ __device__ void block_tri_inverse(const double2 (*D)[NB + 1], int jb, double2 (*
   block_tri_inverse_t<NB, LOWER, kThreads>(D, jb, X, W);
 }
 
-// ---- panel LU of the S rows [j0, s) x [j0, j1) with partial pivoting (kernels.py:237-252)
-// Thread t keeps physical row t of the panel in registers for the whole panel;
-// a pivot interchange only swaps the *logical positions* of two threads (no
-// data moves).  The current pivot column is always register 0: the rank-1
-// update writes its result shifted left, so the column loop is a compact loop.
-// Finished multipliers stream to a staging row in MS (unused until the Sigma
-// phase); every row is written once, to its final position, at the end.
-// Per column: one block argmax (shuffles + 1 barrier) + one broadcast barrier.
-template <int NB, int T>
-struct PanelShared {
-  double cand_v[2][T / 32];
-  int cand_i[2][T / 32];
-  double2 prow[2][NB + 1];
-  int s_bad, s_nd;
-  int lpiv[NB], dsrc[2 * NB], ddst[2 * NB];
-};
-
-template <int NB, int T>
-__device__ void panel_body(const SolveParams& P, int64_t eidx, const ElimDesc& d, int e, int j,
-                           PanelShared<NB, T>& sh) {
-  auto& cand_v = sh.cand_v;
-  auto& cand_i = sh.cand_i;
-  auto& prow = sh.prow;
-  auto& s_bad = sh.s_bad;
-  auto& s_nd = sh.s_nd;
-  auto& lpiv = sh.lpiv;
-  auto& dsrc = sh.dsrc;
-  auto& ddst = sh.ddst;
-  const int tid = threadIdx.x;
-  const struct { int64_t e; } t = {eidx};
-  const int n = d.n, s = d.s;
-  const int j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
-  const Scr S = scratch_of(P, d, e, NB);
-  double2* M = S.M;
-  double2* Lst = S.MS + (int64_t)tid * NB;  // this thread's finished multipliers
-  if (tid == 0) s_bad = INT32_MAX;
-  const bool has = tid < R;
-  int pos = tid;  // logical position of this thread's row
-  double2 row[NB];
-#pragma unroll
-  for (int c = 0; c < NB; ++c) row[c] = (has && c < jb) ? M[(int64_t)(j0 + tid) * n + j0 + c] : cz();
-  double scale;
-  if (j == 0) {
-    scale = 0.0;
-    for (int q = tid; q < (s + kRowChunk - 1) / kRowChunk; q += T) scale = fmax(scale, S.pmax[q]);
-    int dummy = 0;
-    block_argmax<T>(scale, dummy, cand_v[1], cand_i[1]);
-    if (tid == 0) {
-      *S.scale = scale;
-      if (scale == 0.0) s_bad = 0;
-    }
-  } else {
-    scale = *reinterpret_cast<volatile double*>(S.scale);
-  }
-#pragma unroll 1
-  for (int jj = 0; jj < jb; ++jj) {
-    const int buf = jj & 1;
-    double v = (has && pos >= jj) ? cabs1(row[0]) : -1.0;
-    int vi = (has && pos >= jj) ? pos : INT32_MAX;
-    block_argmax<T>(v, vi, cand_v[buf], cand_i[buf]);
-    const int pr = vi >= jj && vi < R ? vi : jj;  // NaN / Inf entries: no interchange
-    const bool winner = has && pos == pr;
-    if (winner) {
-#pragma unroll
-      for (int c = 0; c < NB; ++c) prow[buf][c] = row[c];
-      prow[buf][NB] = cinv(row[0]);
-      // final U row jj (columns jj..jb-1); its multipliers follow after the loop
-      double2* dst = M + (int64_t)(j0 + jj) * n + j0;
-#pragma unroll
-      for (int c = 0; c < NB; ++c)
-        if (jj + c < jb) dst[jj + c] = row[c];
-      if (cabs(row[0]) < P.rtol * scale) atomicMin(&s_bad, j0 + jj);
-    }
-    if (tid == 0) { lpiv[jj] = pr; S.PIV[j0 + jj] = j0 + pr; }
-    __syncthreads();
-    if (winner) pos = jj;
-    else if (has && pos == jj) pos = pr;
-    if (has && pos > jj) {
-      const double2 uinv = prow[buf][NB];
-      const double2 l = cmul(row[0], uinv);
-      Lst[jj] = l;
-#pragma unroll
-      for (int c = 1; c < NB; ++c) row[c - 1] = cfms(row[c], l, prow[buf][c]);
-      row[NB - 1] = cz();
-    }
-  }
-  // every row's multipliers (columns < min(pos, jb)) to its final position
-  if (has) {
-    double2* dst = M + (int64_t)(j0 + pos) * n + j0;
-    const int nl = min(pos, jb);
-#pragma unroll 8
-    for (int c = 0; c < nl; ++c) dst[c] = Lst[c];
-  }
-  // net row permutation of this panel's interchanges (rows that moved: <= 2 NB)
-  if (tid == 0) {
-    int key[2 * NB], val[2 * NB], cnt = 0;
-    for (int jj = 0; jj < jb; ++jj) {
-      if (lpiv[jj] == jj) continue;
-      int ia = -1, ib = -1;
-      for (int k = 0; k < cnt; ++k) {
-        if (key[k] == jj) ia = k;
-        if (key[k] == lpiv[jj]) ib = k;
-      }
-      if (ia < 0) { key[cnt] = jj; val[cnt] = jj; ia = cnt++; }
-      if (ib < 0) { key[cnt] = lpiv[jj]; val[cnt] = lpiv[jj]; ib = cnt++; }
-      const int tmp = val[ia];
-      val[ia] = val[ib];
-      val[ib] = tmp;
-    }
-    int nd = 0;
-    for (int k = 0; k < cnt; ++k)
-      if (key[k] != val[k]) { ddst[nd] = key[k]; dsrc[nd] = val[k]; ++nd; }
-    s_nd = nd;
-  }
-  __syncthreads();  // final panel rows are in M (global writes of this CTA are visible after the barrier)
-  {
-    const int nd = s_nd;
-    if (tid == 0) S.PERM[0] = nd;
-    for (int k = tid; k < nd; k += T) {
-      S.PERM[1 + k] = dsrc[k];
-      S.PERM[1 + 2 * NB + k] = ddst[k];
-    }
-  }
-  if (tid == 0 && s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
-  __syncthreads();
-}
-
-template <int NB, int T>
-__global__ void __launch_bounds__(T, 512 / T) panel_kernel(SolveParams P, const Task* tasks) {
-  pdl_entry();
-  __shared__ PanelShared<NB, T> sh;
-  const Task t = tasks[blockIdx.x];
-  const ElimDesc d = P.elims[t.e];
-  panel_body<NB, T>(P, t.e, d, blockIdx.y, t.a, sh);
-}
-
-#ifdef FIND_PANEL_CLOCKS  // tools/panel_bench.cu latency breakdown of one panel CTA
+#ifdef FIND_PANEL_CLOCKS  // tools/tall_bench.cu latency breakdown of one panel CTA
 __device__ long long g_pclk[64][8];
 #define PCLK(k) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && threadIdx.x / 32 == PCLK_WARP && jj < 64) g_pclk[jj][k] = clock64(); } while (0)
 #ifndef PCLK_WARP
@@ -1148,7 +1012,7 @@ __device__ long long g_pclk[64][8];
 // publishes its whole row and the pivot inverse in a per-warp slot (double
 // buffered); after the barrier every thread picks the winning slot and updates
 // its row from it.  Row interchanges are logical positions; rows are written to
-// their final positions at the end.  Same pivots and arithmetic as panel_body.
+// their final positions at the end (LAPACK zgetf2 pivots: max |re|+|im|, lowest row on ties).
 // two or three CTAs per SM up to 192 rows (the panel is latency-bound: throughput comes from
 // concurrent panels); above that the row registers leave room for one without spilling
 template <int NB, int T>
@@ -1295,128 +1159,6 @@ __global__ void __launch_bounds__(T, (T <= 96 ? 3 : (T <= 192 ? 2 : 1))) panel1_
   if (tid == 0) {
     S.PERM[0] = s_nd;
     if (s_bad != INT32_MAX) report_bad(P, t.e, e, s_bad);
-  }
-}
-
-// ---- panel step, one WARP per (elimination, energy): rows [j0, s) x columns
-// [j0, j0+jb) staged in shared memory (row stride NB+1: conflict-free), physical
-// row interchanges (LAPACK order), no CTA barriers; several panels per CTA.
-// Same pivots (max |re|+|im|, lowest row on ties), same pivot test and the same
-// multiplier / update arithmetic as panel_body.  RPL = rows per lane (R <= 32 RPL).
-__host__ __device__ constexpr size_t warp_panel_bytes(int rmax, int nb) {
-  return ((size_t)rmax * (nb + 1) * sizeof(double2) + (size_t)rmax * sizeof(int) + 15) & ~size_t(15);
-}
-
-template <int NB, int RPL>
-__global__ void __launch_bounds__(256) warp_panel_kernel(SolveParams P, const Task* tasks, int64_t count, int rmax) {
-  pdl_entry();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int LD = NB + 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t ti = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  if (ti >= count) return;  // warp-uniform; the kernel has no CTA barrier
-  const Task t = tasks[ti];
-  const int e = blockIdx.y;
-  const ElimDesc d = P.elims[t.e];
-  const int n = d.n, s = d.s, j = t.a;
-  const int j0 = j * NB, jb = min(NB, s - j0), R = s - j0;
-  const Scr S = scratch_of(P, d, e, NB);
-  unsigned char* base = smem_raw + (size_t)warp * warp_panel_bytes(rmax, NB);
-  double2* A = reinterpret_cast<double2*>(base);
-  int* rowof = reinterpret_cast<int*>(A + (size_t)rmax * LD);  // position -> original panel row
-  const double2* Mp = S.M + (int64_t)j0 * n + j0;
-#pragma unroll 4
-  for (int q = lane; q < R * NB; q += 32) {
-    const int r = q / NB, c = q % NB;
-    A[r * LD + c] = c < jb ? Mp[(int64_t)r * n + c] : cz();
-  }
-  for (int r = lane; r < R; r += 32) rowof[r] = r;
-  double scale;
-  if (j == 0) {
-    scale = 0.0;
-    for (int q = lane; q < (s + kRowChunk - 1) / kRowChunk; q += 32) scale = fmax(scale, S.pmax[q]);
-    for (int o = 16; o; o >>= 1) scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
-    if (lane == 0) *S.scale = scale;
-  } else {
-    scale = *reinterpret_cast<volatile double*>(S.scale);
-  }
-  int bad = (j == 0 && scale == 0.0) ? 0 : INT32_MAX;
-  __syncwarp();
-#pragma unroll 1
-  for (int jj = 0; jj < jb; ++jj) {
-    double v = -1.0;
-    int vi = INT32_MAX;
-    for (int r = jj + lane; r < R; r += 32) {
-      const double a = cabs1(A[r * LD + jj]);
-      if (a > v) { v = a; vi = r; }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, vi, o);
-      if (ov > v || (ov == v && oi < vi)) { v = ov; vi = oi; }
-    }
-    const int pr = vi >= jj && vi < R ? vi : jj;  // NaN / Inf entries: no interchange
-    if (pr != jj) {
-      for (int c = lane; c < NB; c += 32) {
-        const double2 x = A[jj * LD + c];
-        A[jj * LD + c] = A[pr * LD + c];
-        A[pr * LD + c] = x;
-      }
-      if (lane == 0) {
-        const int tmp = rowof[jj];
-        rowof[jj] = rowof[pr];
-        rowof[pr] = tmp;
-      }
-    }
-    __syncwarp();
-    const double2 pv = A[jj * LD + jj];
-    if (lane == 0) {
-      S.PIV[j0 + jj] = j0 + pr;
-      if (cabs(pv) < P.rtol * scale) bad = min(bad, j0 + jj);
-    }
-    const double2 uinv = cinv(pv);
-    double2 lv[RPL];
-#pragma unroll
-    for (int k = 0; k < RPL; ++k) {
-      const int r = jj + 1 + lane + 32 * k;
-      if (r < R) {
-        lv[k] = cmul(A[r * LD + jj], uinv);
-        A[r * LD + jj] = lv[k];
-      }
-    }
-    for (int c = jj + 1; c < jb; ++c) {
-      const double2 u = A[jj * LD + c];
-#pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int r = jj + 1 + lane + 32 * k;
-        if (r < R) A[r * LD + c] = cfms(A[r * LD + c], lv[k], u);
-      }
-    }
-    __syncwarp();
-  }
-  double2* Mw = S.M + (int64_t)j0 * n + j0;
-#pragma unroll 4
-  for (int q = lane; q < R * NB; q += 32) {
-    const int r = q / NB, c = q % NB;
-    if (c < jb) Mw[(int64_t)r * n + c] = A[r * LD + c];
-  }
-  // net row permutation of this panel (rows that moved: <= 2 NB)
-  int nd = 0;
-  for (int b0 = 0; b0 < R; b0 += 32) {
-    const int r = b0 + lane;
-    const bool mv = r < R && rowof[r] != r;
-    const unsigned m = __ballot_sync(0xffffffffu, mv);
-    if (mv) {
-      const int k = nd + __popc(m & ((1u << lane) - 1u));
-      S.PERM[1 + k] = rowof[r];
-      S.PERM[1 + 2 * NB + k] = r;
-    }
-    nd += __popc(m);
-  }
-  if (lane == 0) {
-    S.PERM[0] = nd;
-    if (bad != INT32_MAX) report_bad(P, t.e, e, bad);
   }
 }
 
@@ -1875,6 +1617,66 @@ __global__ void __launch_bounds__(T, 1) panel_cluster_reg_kernel(SolveParams P, 
   }
 }
 
+// ---- L_jj^-1 and U_jj^-1 of panel j, once per (elimination, energy), published to LINV / UINV.
+// Runs on the first kThreads threads of the CTA (every thread of the CTA must call it: the
+// CTA-wide barriers are __syncthreads); smem: 5 [NB][NB+1] blocks + 64 ints.
+template <int NB>
+__device__ void panel_inv_body(const SolveParams& P, const Task& t, int e, unsigned char* smem_raw) {
+  const int j = t.a;
+  const ElimDesc d = P.elims[t.e];
+  const int n = d.n, s = d.s;
+  const int j0 = j * NB, jb = min(NB, s - j0);
+  const Scr S = scratch_of(P, d, e, NB);
+  const bool on = threadIdx.x < kThreads;
+  typedef double2 Row[NB + 1];
+  Row* Dm = reinterpret_cast<Row*>(smem_raw);
+  Row* Xm = Dm + NB;
+  Row* Wm = Xm + NB;
+  // sigma (pivoted position -> merged position) kept up to date panel by panel: this panel's
+  // net row interchange PERM applied to SIG[j0:s) exactly as to the rows of M (identity
+  // before panel 0), so the last panel only inverts it -- no serial pass over PIV
+  int* stg = reinterpret_cast<int*>(Wm + 3 * NB);
+  const int nd = S.PERM[0];
+  if (on) {
+    if (j == 0)
+      for (int k = threadIdx.x; k < s; k += kThreads) S.SIG[k] = k;
+    for (int k = threadIdx.x; k < nd; k += kThreads) stg[k] = j == 0 ? S.PERM[1 + k] : S.SIG[j0 + S.PERM[1 + k]];
+    for (int q = threadIdx.x; q < NB * NB; q += kThreads) {
+      const int r = q / NB, c = q % NB;
+      Dm[r][c] = (r < jb && c < jb) ? S.M[(int64_t)(j0 + r) * n + j0 + c] : cz();
+    }
+  }
+  __syncthreads();
+  if (on) {
+    for (int k = threadIdx.x; k < nd; k += kThreads) S.SIG[j0 + S.PERM[1 + 2 * NB + k]] = stg[k];
+    // L_jj^-1 on threads [0, 128), U_jj^-1 on [128, 256), concurrently (named barriers 1 and 2)
+    constexpr int H = kThreads / 2;
+    const bool lower = threadIdx.x < H;
+    const int ht = lower ? threadIdx.x : threadIdx.x - H;
+    Row* Xh = lower ? Xm : Wm + NB;
+    Row* Wh = lower ? Wm : Wm + 2 * NB;
+    if (lower) block_tri_inverse_t<NB, true, H>(Dm, jb, Xh, Wh, ht, 1);
+    else block_tri_inverse_t<NB, false, H>(Dm, jb, Xh, Wh, ht, 2);
+    double2* out = (lower ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
+    for (int q = ht; q < NB * NB; q += H) {
+      const int r = q / NB, c = q % NB;
+      out[q] = (r < jb && c < jb) ? Xh[r][c] : cz();
+    }
+  }
+  if (j0 + jb == s) {  // last panel: sigma is final -> its inverse (the finish step)
+    __syncthreads();
+    if (on)
+      for (int k = threadIdx.x; k < s; k += kThreads) S.ISG[S.SIG[k]] = k;
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kThreads) panel_inv_kernel(SolveParams P, const Task* tasks) {
+  pdl_entry();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  panel_inv_body<NB>(P, tasks[blockIdx.x], blockIdx.y, smem_raw);
+}
+
 // ---- NB = 32 panel step of a TALL panel in ONE CTA (many concurrent panels: the contact-row
 // eliminations of the deep downward levels, s ~ 1000 with tiny b, hundreds per level).  The
 // cluster kernels above spread one panel over up to 8 SMs and leave each of them idle at the
@@ -2267,54 +2069,6 @@ __global__ void __launch_bounds__(kThreads) trsm_kernel(SolveParams P, const Tas
   trsm_body<NB>(P, tasks[blockIdx.x], blockIdx.y, j, reinterpret_cast<double2*>(smem_raw), inv_ready != 0);
 }
 
-// ---- L_jj^-1 and U_jj^-1 of panel j, once per (elimination, energy), published to LINV / UINV
-template <int NB>
-__global__ void __launch_bounds__(kThreads) panel_inv_kernel(SolveParams P, const Task* tasks) {
-  pdl_entry();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y, j = t.a;
-  const ElimDesc d = P.elims[t.e];
-  const int n = d.n, s = d.s;
-  const int j0 = j * NB, jb = min(NB, s - j0);
-  const Scr S = scratch_of(P, d, e, NB);
-  typedef double2 Row[NB + 1];
-  Row* Dm = reinterpret_cast<Row*>(smem_raw);
-  Row* Xm = Dm + NB;
-  Row* Wm = Xm + NB;
-  // sigma (pivoted position -> merged position) kept up to date panel by panel: this panel's
-  // net row interchange PERM applied to SIG[j0:s) exactly as to the rows of M (identity
-  // before panel 0), so the last panel only inverts it -- no serial pass over PIV
-  int* stg = reinterpret_cast<int*>(Wm + 3 * NB);
-  const int nd = S.PERM[0];
-  if (j == 0)
-    for (int k = threadIdx.x; k < s; k += kThreads) S.SIG[k] = k;
-  for (int k = threadIdx.x; k < nd; k += kThreads) stg[k] = j == 0 ? S.PERM[1 + k] : S.SIG[j0 + S.PERM[1 + k]];
-  for (int q = threadIdx.x; q < NB * NB; q += kThreads) {
-    const int r = q / NB, c = q % NB;
-    Dm[r][c] = (r < jb && c < jb) ? S.M[(int64_t)(j0 + r) * n + j0 + c] : cz();
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < nd; k += kThreads) S.SIG[j0 + S.PERM[1 + 2 * NB + k]] = stg[k];
-  // L_jj^-1 on threads [0, 128), U_jj^-1 on [128, 256), concurrently (named barriers 1 and 2)
-  constexpr int H = kThreads / 2;
-  const bool lower = threadIdx.x < H;
-  const int ht = lower ? threadIdx.x : threadIdx.x - H;
-  Row* Xh = lower ? Xm : Wm + NB;
-  Row* Wh = lower ? Wm : Wm + 2 * NB;
-  if (lower) block_tri_inverse_t<NB, true, H>(Dm, jb, Xh, Wh, ht, 1);
-  else block_tri_inverse_t<NB, false, H>(Dm, jb, Xh, Wh, ht, 2);
-  double2* out = (lower ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
-  for (int q = ht; q < NB * NB; q += H) {
-    const int r = q / NB, c = q % NB;
-    out[q] = (r < jb && c < jb) ? Xh[r][c] : cz();
-  }
-  if (j0 + jb == s) {  // last panel: sigma is final -> its inverse (the finish step)
-    __syncthreads();
-    for (int k = threadIdx.x; k < s; k += kThreads) S.ISG[S.SIG[k]] = k;
-  }
-}
-
 // ---- trailing update M[j1:, j1:] -= M[j1:, j0:j1] M[j0:j1, j1:]
 // t.c: 0 the full trailing update of panel j; 2 only the next panel's columns (the strip of
 // a wide block); 1 the wide block's update, K = both panels (j-1, j)
@@ -2450,118 +2204,6 @@ __global__ void __launch_bounds__(kThreads) finish_kernel(SolveParams P, const T
   const Task t = tasks[blockIdx.x];
   const ElimDesc d = P.elims[t.e];
   finish_body(P, t.e, d, blockIdx.y, nb, reinterpret_cast<int*>(smem_raw));
-}
-
-// ---- whole blocked LU of one elimination in one CTA (groups with many medium
-// eliminations): per 32-column panel the register panel step, the row
-// interchanges, the diagonal-block inverses, U12 / L21 DMMA tiles and the
-// trailing DMMA tiles (B x B block excluded); then X = Y L11^-1 and sigma.
-// Same arithmetic and data layout as the phase launches.
-constexpr int kFusedT = 256;
-__global__ void __launch_bounds__(kFusedT, 2) lu_fused_kernel(SolveParams P, const Task* tasks) {
-  pdl_entry();
-  constexpr int NB = 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* smem = reinterpret_cast<double2*>(smem_raw);
-  __shared__ PanelShared<NB, kFusedT> sh;
-  const int tid = threadIdx.x;
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y;
-  const ElimDesc d = P.elims[t.e];
-  const int n = d.n, s = d.s, b = d.b;
-  const Scr S = scratch_of(P, d, e, NB);
-  double2* M = S.M;
-  const int steps = (s + NB - 1) / NB;
-  for (int j = 0; j < steps; ++j) {
-    const int j0 = j * NB, jb = min(NB, s - j0), j1 = j0 + jb;
-    panel_body<NB, kFusedT>(P, t.e, d, e, j, sh);
-    // row interchanges on the columns outside the panel (staged through smem)
-    const int nd = S.PERM[0];
-    if (nd > 0) {
-      const int other = n - jb;
-      const int cap = 4096 / nd;
-      for (int cb = 0; cb < other; cb += cap) {
-        const int cn = min(cap, other - cb);
-        for (int q = tid; q < nd * cn; q += kFusedT) {
-          const int k = q / cn, x = cb + q % cn;
-          const int col = x < j0 ? x : x + jb;
-          smem[q] = M[(int64_t)(j0 + S.PERM[1 + k]) * n + col];
-        }
-        __syncthreads();
-        for (int q = tid; q < nd * cn; q += kFusedT) {
-          const int k = q / cn, x = cb + q % cn;
-          const int col = x < j0 ? x : x + jb;
-          M[(int64_t)(j0 + S.PERM[1 + 2 * NB + k]) * n + col] = smem[q];
-        }
-        __syncthreads();
-      }
-    }
-    // inverses of the diagonal block
-    {
-      typedef double2 Row[NB + 1];
-      Row* Dm = reinterpret_cast<Row*>(smem);
-      Row* Xm = Dm + NB;
-      Row* Wm = Xm + NB;
-      for (int q = tid; q < NB * NB; q += kFusedT) {
-        const int r = q / NB, c = q % NB;
-        Dm[r][c] = (r < jb && c < jb) ? M[(int64_t)(j0 + r) * n + j0 + c] : cz();
-      }
-      __syncthreads();
-      for (int pass = 0; pass < 2; ++pass) {
-        if (pass == 0) block_tri_inverse<NB, true>(Dm, jb, Xm, Wm);
-        else block_tri_inverse<NB, false>(Dm, jb, Xm, Wm);
-        double2* out = (pass == 0 ? S.LINV : S.UINV) + (int64_t)j * NB * NB;
-        for (int q = tid; q < NB * NB; q += kFusedT) {
-          const int r = q / NB, c = q % NB;
-          out[q] = (r < jb && c < jb) ? Xm[r][c] : cz();
-        }
-        __syncthreads();
-      }
-    }
-    // U12 = L_jj^-1 A12 and L21 = A21 U_jj^-1
-    for (int c0 = j1; c0 < n; c0 += kTile) {
-      using TT = TrsmTiles<NB>::U;
-      double2* B = M + (int64_t)j0 * n + c0;
-      TT T;
-      T.zero();
-      T.mma(S.LINV + (int64_t)j * NB * NB, NB, B, n, jb, min(kTile, n - c0), jb, smem);
-      T.for_each([&](int r, int c, double2 v) {
-        if (r < jb && c0 + c < n) B[(int64_t)r * n + c] = v;
-      });
-      __syncthreads();
-    }
-    for (int r0 = s; r0 < n; r0 += kTile) {
-      using TT = TrsmTiles<NB>::L;
-      double2* A = M + (int64_t)r0 * n + j0;
-      TT T;
-      T.zero();
-      T.mma(A, n, S.UINV + (int64_t)j * NB * NB, NB, min(kTile, n - r0), jb, jb, smem);
-      T.for_each([&](int r, int c, double2 v) {
-        if (r0 + r < n && c < jb) A[(int64_t)r * n + c] = v;
-      });
-      __syncthreads();
-    }
-    // trailing update (the B x B block is left to the Schur launch)
-    for (int r0 = j1; r0 < n; r0 += kTile)
-      for (int c0 = j1; c0 < n; c0 += kTile) {
-        if (r0 >= s && c0 >= s) continue;
-        Tile64 T;
-        T.zero();
-        T.mma(M + (int64_t)r0 * n + j0, n, M + (int64_t)j0 * n + c0, n, min(kTile, n - r0), min(kTile, n - c0), jb,
-              smem);
-        T.for_each([&](int r, int c, double2 v) {
-          if (r0 + r < n && c0 + c < n && (r0 + r < s || c0 + c < s)) {
-            double2* p = M + (int64_t)(r0 + r) * n + c0 + c;
-            *p = csub(*p, v);
-          }
-        });
-        __syncthreads();
-      }
-  }
-  // X = Y L11^-1, block columns right to left
-  for (int j = steps - 1; j >= 0; --j)
-    for (int r0 = 0; r0 < b; r0 += kTile) xsolve_tile<NB>(S, n, s, j, r0, smem);
-  finish_body(P, t.e, d, e, NB, reinterpret_cast<int*>(smem));
 }
 
 // ---- T_S = MS[s:, :s] - X MS[:s, :s]   (the S columns of T = Sigma'_B: - X Sigma'_S:)
@@ -3286,9 +2928,6 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(mid_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CUDA_TRY(cudaFuncSetAttribute(warp_panel_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CUDA_TRY(cudaFuncSetAttribute(warp_panel_kernel<32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CUDA_TRY(cudaFuncSetAttribute(warp_panel_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
 
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -3306,7 +2945,6 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(tgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(rgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(schur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
-  CUDA_TRY(cudaFuncSetAttribute(lu_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<32>()));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<16>()));
   CUDA_TRY(cudaFuncSetAttribute(xsolve_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsolve_smem<8>()));
@@ -3362,21 +3000,11 @@ int side_init(SideStreams& g_side, int dev, find_status* st) {
 
 int run_one_group(const find_plan* P, const SolveParams& prm, int64_t gi, int nE, cudaStream_t stream,
                   find_status* st);
-// NB = 32 panel steps: register rows with one barrier per column (default),
-// register rows with two barriers per column (FIND_B200_PANEL=reg), one warp per
-// panel in shared memory (FIND_B200_PANEL=warp) or CTA with shared-memory rows
-// (FIND_B200_SMEM_PANEL=1)
+// NB = 32 panel steps up to kRegPanelMaxS rows: register rows with one barrier per column, or the
+// CTA with shared-memory rows (FIND_B200_SMEM_PANEL=1)
 const bool g_reg_panel = [] {
   const char* f = std::getenv("FIND_B200_SMEM_PANEL");
   return !(f && f[0] == '1');
-}();
-const int g_panel_mode = [] {
-  const char* f = std::getenv("FIND_B200_PANEL");
-  if (f && std::string(f) == "reg") return 1;
-  if (f && std::string(f) == "warp") return 3;
-  const char* m = std::getenv("FIND_B200_SMEM_PANEL");
-  if (m && m[0] == '1') return 2;
-  return 0;
 }();
 
 // Diagonal-block inverses once per (elimination, panel) in their own launch (default), or
@@ -3391,20 +3019,6 @@ const bool g_zskip = [] {
   const char* f = std::getenv("FIND_B200_STRUCT");
   return !(f && f[0] == '0');
 }();
-
-// Fused-LU launches (one CTA per elimination and energy) instead of the
-// level-batched phase launches: opt-in (FIND_B200_FUSED=1, for groups that fill
-// the GPU); measured slower than the phase launches once the mid path takes the
-// small eliminations (profiles/r01_*).
-const int g_force_fused = [] {
-  const char* f = std::getenv("FIND_B200_FUSED");
-  return f ? std::atoi(f) : 0;
-}();
-bool use_fused(const LaunchGroup& G, int nE) {
-  if (G.fspec_end <= G.fspec_begin) return false;
-  if (g_force_fused == 2) return G.max_b <= 64;  // experiment: tall-S / small-B groups only
-  return g_force_fused == 1 && (G.end - G.begin) * (int64_t)nE >= 2 * 148;
-}
 
 // Opt-in per-launch timing (find_solve_timing_enable): one event pair per launch.
 struct LaunchTimer {
@@ -3624,6 +3238,17 @@ const int64_t g_tall_min_panels = [] {
   return f ? std::atoll(f) : 48;
 }();
 
+bool use_tall_panel(const LaunchGroup& G, const LaunchSpec& L, int nE) {
+  const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
+  return L.nb == 32 && rmax > g_tall_min_rows && rmax <= kTallMaxRows && L.task_count * nE >= g_tall_min_panels;
+}
+// rows per thread and CTA size of a tall panel launch
+void tall_shape(const LaunchGroup& G, const LaunchSpec& L, int& rpt, int& T) {
+  const int rmax = G.max_s - L.step * L.nb;
+  rpt = rmax <= kTallMaxT ? 1 : (rmax <= 2 * kTallMaxT ? 2 : 3);
+  T = 32 * (((rmax + rpt - 1) / rpt + 31) / 32);
+}
+
 const bool g_rsym_down = [] {
   const char* f = std::getenv("FIND_B200_RSYM_DOWN");
   return f && f[0] == '1';
@@ -3645,14 +3270,13 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
     SolveParams prm = prm_in;
     if (G.pass != 0 && !g_rsym_down) prm.rsym = 0;
     if (G.path == 1 && G.nb == 0) return fail_status(st, FIND_EINVAL, "elimination block too large for this build");
-    const bool fused = use_fused(G, nE);
-    for (int64_t si = fused ? G.fspec_begin : G.spec_begin; si < (fused ? G.fspec_end : G.spec_end); ++si) {
+    for (int64_t si = G.spec_begin; si < G.spec_end; ++si) {
       const LaunchSpec& L = P->specs[si];
       if (!prm.compute_gless && (L.kind == kLGatherS || L.kind == kLTGemm || L.kind == kLRGemm)) continue;
       if (L.kind == kLPanelInv && !g_inv_launch) continue;
       // sigma comes from the last panel's inverse launch; the finish launch remains for the
       // unit-test shim's L output (and when the inverse launches are off)
-      if (L.kind == kLFinish && g_inv_launch && !prm.dbg_l && !fused) continue;
+      if (L.kind == kLFinish && g_inv_launch && !prm.dbg_l) continue;
       const Task* tk = dtasks + L.task_off;
       const unsigned cnt = (unsigned)L.task_count;
       const dim3 grid(cnt, (unsigned)nE);
@@ -3684,10 +3308,12 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         case kLGatherS: launch_k(gather_kernel<true>, grid, kThreads, 0, stream, prm, tk); break;
         case kLPanel: {
           const int rmax = G.max_s - L.step * L.nb;  // rows of this step's largest panel
-          if (L.nb == 32 && rmax > g_tall_min_rows && rmax <= kTallMaxRows && (int64_t)cnt * nE >= g_tall_min_panels) {
-            // many tall panels in flight: one CTA per panel (SM-time, not latency, is what counts)
-            const int rpt = rmax <= kTallMaxT ? 1 : (rmax <= 2 * kTallMaxT ? 2 : 3);
-            const int T = 32 * (((rmax + rpt - 1) / rpt + 31) / 32);
+          if (use_tall_panel(G, L, nE)) {
+            // many tall panels in flight: one CTA per panel (SM-time, not latency, is what counts).
+            // (Running the diagonal-block inverses in the same launch measured neutral: the panel CTA
+            // holds its SM that much longer.)
+            int rpt, T;
+            tall_shape(G, L, rpt, T);
             if (rpt == 1) launch_k(panel_tall_kernel<1>, grid, T, 0, stream, prm, tk);
             else if (rpt == 2) launch_k(panel_tall_kernel<2>, grid, T, 0, stream, prm, tk);
             else launch_k(panel_tall_kernel<3>, grid, T, 0, stream, prm, tk);
@@ -3713,7 +3339,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
                            prm, tk);
           } else if (L.nb == 32 && rmax > (int)kRegPanelMaxS) {  // more rows than the register panel holds
             launch_k(panel_smem_kernel<32>, grid, kThreads, (size_t)rmax * 33 * sizeof(double2), stream, prm, tk);
-          } else if (L.nb == 32 && g_panel_mode == 0) {
+          } else if (L.nb == 32 && g_reg_panel) {
             switch ((std::max(rmax, 1) + 31) / 32) {
               case 1: launch_k(panel1_kernel<32, 32>, grid, 32, 0, stream, prm, tk); break;
               case 2: launch_k(panel1_kernel<32, 64>, grid, 64, 0, stream, prm, tk); break;
@@ -3725,19 +3351,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
               case 8: launch_k(panel1_kernel<32, 256>, grid, 256, 0, stream, prm, tk); break;
               default: launch_k(panel1_kernel<32, 288>, grid, 288, 0, stream, prm, tk); break;
             }
-          } else if (L.nb == 32 && rmax > 256) {  // other NB = 32 variants hold <= 256 rows
-            launch_k(panel_smem_kernel<32>, grid, kThreads, (size_t)rmax * 33 * sizeof(double2), stream, prm, tk);
-          } else if (L.nb == 32 && g_panel_mode == 3) {
-            const size_t pb = warp_panel_bytes(std::max(rmax, 1), 32);
-            const int w = (int)std::max<size_t>(1, std::min<size_t>(8, kMaxSmem / pb));
-            const dim3 wg((unsigned)((L.task_count + w - 1) / w), (unsigned)nE);
-            if (rmax <= 64) launch_k(warp_panel_kernel<32, 2>, wg, 32 * w, pb * w, stream, prm, tk, L.task_count, rmax);
-            else if (rmax <= 128) launch_k(warp_panel_kernel<32, 4>, wg, 32 * w, pb * w, stream, prm, tk, L.task_count, rmax);
-            else launch_k(warp_panel_kernel<32, 8>, wg, 32 * w, pb * w, stream, prm, tk, L.task_count, rmax);
-          } else if (L.nb == 32 && g_reg_panel && rmax <= 64) launch_k(panel_kernel<32, 64>, grid, 64, 0, stream, prm, tk);
-          else if (L.nb == 32 && g_reg_panel && rmax <= 128) launch_k(panel_kernel<32, 128>, grid, 128, 0, stream, prm, tk);
-          else if (L.nb == 32 && g_reg_panel) launch_k(panel_kernel<32, 256>, grid, 256, 0, stream, prm, tk);
-          else if (L.nb == 32)
+          } else if (L.nb == 32)
             launch_k(panel_smem_kernel<32>, grid, kThreads, (size_t)std::max(rmax, 1) * 33 * sizeof(double2), stream, prm, tk);
           else if (L.nb == 16)
             launch_k(panel_smem_kernel<16>, grid, kThreads, (size_t)G.max_s * 17 * sizeof(double2), stream, prm, tk);
@@ -3801,7 +3415,6 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           else
             launch_k(schur_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk);
           break;
-        case kLLuFused: launch_k(lu_fused_kernel, grid, kFusedT, Tile64::SMEM, stream, prm, tk); break;
         case kLFinal: {
           const int cmax = std::max(1, G.max_b);
           const size_t smem = (size_t)kSmallWarps * 2 * cmax * (cmax + 1) * sizeof(double2);
@@ -3820,7 +3433,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
       const unsigned ne = (unsigned)nE;
       if (G.path == 1) {
         const LaunchSpec* fl = nullptr;
-        for (int64_t si = fused ? G.fspec_begin : G.spec_begin; si < (fused ? G.fspec_end : G.spec_end); ++si)
+        for (int64_t si = G.spec_begin; si < G.spec_end; ++si)
           if (P->specs[si].kind == kLFinal) fl = &P->specs[si];
         if (!fl) return fail_status(st, FIND_EINVAL, "final group without a final launch");
         const bool gl = prm.off_gl != nullptr, gen = gl && prm.off_sym == 0;
@@ -3848,10 +3461,9 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
 template <class F>
 void for_each_launch(const find_plan* P, int nE, F f) {
   for (const LaunchGroup& G : P->groups) {
-    const bool fu = use_fused(G, nE);
-    for (int64_t si = fu ? G.fspec_begin : G.spec_begin; si < (fu ? G.fspec_end : G.spec_end); ++si) {
+    for (int64_t si = G.spec_begin; si < G.spec_end; ++si) {
       if (P->specs[si].kind == kLPanelInv && !g_inv_launch) continue;
-      if (P->specs[si].kind == kLFinish && g_inv_launch && !fu) continue;  // folded into the last inverse launch
+      if (P->specs[si].kind == kLFinish && g_inv_launch) continue;  // folded into the last inverse launch
       f(P->specs[si].kind, P->specs[si].step, P->specs[si].group, P->specs[si].task_count);
     }
   }

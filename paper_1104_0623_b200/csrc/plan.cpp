@@ -136,7 +136,6 @@ void find_build_tasks(find_plan* P) {
   for (int32_t gi = 0; gi < (int32_t)P->groups.size(); ++gi) {
     LaunchGroup& G = P->groups[gi];
     G.spec_begin = (int64_t)P->specs.size();
-    G.fspec_begin = G.fspec_end = 0;
     if (G.path == 0 || G.path == 2) {
       LaunchSpec L;
       L.kind = G.path == 0 ? kLSmall : kLMid; L.step = 0; L.nb = 0; L.group = gi;
@@ -269,27 +268,6 @@ void find_build_tasks(find_plan* P) {
       if (P->elims[e].kind == kFinal) push((int32_t)e, 0, 0, 0);
     spec(kLFinal, 0, nb, gi, off);
     G.spec_end = (int64_t)P->specs.size();
-    // fused alternative: gatherA, fused LU (+X, sigma), then the same tail launches
-    G.fspec_begin = G.fspec_end = (int64_t)P->specs.size();
-    if (nb == 32 && G.max_s <= 256) {
-      std::vector<LaunchSpec> tail;
-      LaunchSpec ga{};
-      for (int64_t si = G.spec_begin; si < G.spec_end; ++si) {
-        const LaunchSpec& L = P->specs[si];
-        if (L.kind == kLGatherA) ga = L;
-        if (L.kind == kLSchur || L.kind == kLGatherS || L.kind == kLTGemm || L.kind == kLRGemm || L.kind == kLFinal)
-          tail.push_back(L);
-      }
-      off = (int64_t)P->tasks.size();
-      for (int64_t e = G.begin; e < G.end; ++e) push((int32_t)e, 0, 0, 0);
-      LaunchSpec lu{};
-      lu.kind = kLLuFused; lu.step = 0; lu.nb = nb; lu.group = gi;
-      lu.task_off = off; lu.task_count = (int64_t)P->tasks.size() - off;
-      P->specs.push_back(ga);
-      P->specs.push_back(lu);
-      for (const LaunchSpec& L : tail) P->specs.push_back(L);
-      G.fspec_end = (int64_t)P->specs.size();
-    }
   }
 }
 

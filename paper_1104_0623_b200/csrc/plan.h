@@ -55,7 +55,7 @@ enum LaunchKind : int32_t {
   kLRGemm = 9,     // R = S_BB - X S_SB - T_S X^H (+ store)     tasks {e, tm, tn, sym-skip}
   kLFinal = 10,    // leaf inverse + G^< sandwich               tasks {e}
   kLSchur = 11,    // U = A_BB - Y U12 (K = s), stored sorted  tasks {e, tm, tn}
-  kLLuFused = 12,  // whole blocked LU + X + sigma in one CTA    tasks {e}
+  kLLuFused = 12,  // (retired: whole blocked LU in one CTA; the value stays reserved)
   kLMid = 13,      // CTA-per-elimination smem kernel (32 < s+b <= 64)
   kLOffdiag = 14,  // off-diagonal G^r / G^< of a final group (after its final launch)
   kLPanelInv = 15, // diagonal-block inverses L_jj^-1, U_jj^-1 of panel j  tasks {e, j}
@@ -101,7 +101,6 @@ struct LaunchGroup {
   int32_t nb;          // panel width of the CTA path (0: unsupported size)
   int32_t phase;       // groups of one phase are independent and run concurrently
   int64_t spec_begin, spec_end;    // launches of this group (level-batched phase launches)
-  int64_t fspec_begin, fspec_end;  // alternative with one fused-LU CTA per elimination (empty if n/a)
 };
 
 struct SparseEntry {  // merged (row, col) <- csr value slot

@@ -1,5 +1,5 @@
-"""CTA-path variants (level-batched phase launches, the fused per-elimination LU, panel
-widths and kinds, dependency scheduling, wide blocks, per-tile inverses) against the
+"""CTA-path variants (panel widths and kinds, tile engines, one-CTA tall panels, dependency
+scheduling, wide blocks, per-tile inverses) against the
 reference's golden outputs, each selected through its environment switch in a fresh
 process (the choices are read once per process / plan)."""
 
@@ -37,11 +37,9 @@ print("RESULT", json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("env", [{"FIND_B200_FUSED": "1"}, {"FIND_B200_FUSED": "0"},
-                                 {"FIND_B200_FUSED": "0", "FIND_B200_NB": "16"},
-                                 {"FIND_B200_FUSED": "0", "FIND_B200_NB": "8"},
-                                 {"FIND_B200_FUSED": "0", "FIND_B200_SMEM_PANEL": "1"},
-                                 {"FIND_B200_PANEL": "reg"}, {"FIND_B200_PANEL": "warp"},
+@pytest.mark.parametrize("env", [{}, {"FIND_B200_NB": "16"}, {"FIND_B200_NB": "8"}, {"FIND_B200_SMEM_PANEL": "1"},
+                                 {"FIND_B200_TMA": "0"}, {"FIND_B200_TMA_MIN_S": "0"},
+                                 {"FIND_B200_TALL_MIN_PANELS": "0", "FIND_B200_TALL_MIN_ROWS": "32"},
                                  {"FIND_B200_DAG_MAX_N": "100000"}, {"FIND_B200_WIDE_MIN_S": "0"},
                                  {"FIND_B200_INV_LAUNCH": "0"}, {"FIND_B200_STRUCT": "0"},
                                  {"FIND_B200_SPLIT_K": "1"}, {"FIND_B200_SPLIT_K": "3"}])
