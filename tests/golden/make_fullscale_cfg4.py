@@ -9,7 +9,8 @@ Why the port and not the reference: at 1024x1024 the reference FIND cannot build
 oracle/find_oracle.py restates the reference path with the same LAPACK calls per elimination; it
 is pinned to the reference's own outputs on every full-size fixture the reference can produce
 (tests/test_oracle_golden.py: cfg0-cfg2 FIND, cfg3 RGF), so its cfg4 output stands in for the
-reference there.  The test tests/test_fullscale.py compares the GPU path against every entry.
+reference there.  tests/test_fullscale.py compares the GPU path against every 8th node (the committed
+subset).
 """
 
 import sys
@@ -25,6 +26,9 @@ from oracle.find_oracle import FindOracle  # noqa: E402
 from paper_1104_0623_b200.configs import config_problem  # noqa: E402
 
 
+STRIDE = 8
+
+
 def main(ks):
     p = config_problem(4)
     t0 = time.time()
@@ -38,8 +42,15 @@ def main(ks):
         gr.append(r.gr_diag)
         gl.append(r.gless_diag)
         print("energy", k, round(secs[-1], 1), "s", flush=True)
-    np.savez(HERE / "full_cfg4.npz", config=4, energy_idx=np.array(ks), gr=np.array(gr), gl=np.array(gl),
-             seconds=np.array(secs), source="oracle port (oracle/find_oracle.py FindOracle.solve, naive, compute_gless)")
+    gr, gl = np.array(gr), np.array(gl)
+    # the committed fixture keeps every STRIDE-th node (1 048 576 nodes x 2 vectors x 16 B = 32 MB per energy
+    # otherwise) plus the vectors' maxima; the full vectors go to /tmp for the generating session
+    np.savez("/tmp/full_cfg4_all.npz", energy_idx=np.array(ks), gr=gr, gl=gl)
+    idx = np.arange(0, gr.shape[1], STRIDE)
+    np.savez_compressed(HERE / "full_cfg4.npz", config=4, energy_idx=np.array(ks), node_idx=idx, gr=gr[:, idx],
+                        gl=gl[:, idx], gr_max=np.abs(gr).max(axis=1), gl_max=np.abs(gl).max(axis=1),
+                        seconds=np.array(secs),
+                        source="oracle port (oracle/find_oracle.py FindOracle.solve, naive, compute_gless)")
     print("wrote full_cfg4.npz", flush=True)
 
 

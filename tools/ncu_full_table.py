@@ -31,7 +31,7 @@ for r in rows[2:]:
             vals.append(v)
             continue
         if name == "dur_us":
-            x = x * {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(u, 1)
+            x = x * {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6}.get(u, 1)
         elif name in ("dramR_MB", "dramW_MB"):
             x = x * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1, "Gbyte": 1e3}.get(u, 1)
         vals.append(f"{x:.4g}")
