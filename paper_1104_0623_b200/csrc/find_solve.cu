@@ -2174,150 +2174,6 @@ __global__ void __launch_bounds__(kThreads) xsolve_kernel(SolveParams P, const T
     xsolve_tile<NB>(S, d.n, d.s, j, t.a * kTile, reinterpret_cast<double2*>(smem_raw));
 }
 
-// ---- "skinny" eliminations (b <= kSkinnyB boundary rows against a large S: the contact-row
-// eliminations): X = Y L11^-1 and T_S = Sigma'_BS - X Sigma'_SS are b x s outputs of passes over
-// s x s matrices, i.e. HBM streaming, not tensor work.  X stays in shared memory; the threads of a
-// warp take consecutive columns of one matrix row (512 B / 1 KB row segments), several rows in
-// flight per thread; the k range is split over the CTA's warps and reduced in a fixed order
-// (deterministic; the sums differ from the DMMA tiles' only in their association).
-constexpr int kSkinnyB = 8;
-constexpr int kSkinnyMinS = 256;
-inline size_t skinny_smem(int bmax, int smax) { return ((size_t)bmax * smax + 8 * 32 * kSkinnyB) * sizeof(double2); }
-
-// X_j = (Y_j - X_{>j} L11[>j, j]) L_jj^-1, block columns right to left, one CTA per (elimination, energy)
-__global__ void __launch_bounds__(kThreads) xsolve_skinny_kernel(SolveParams P, const Task* tasks, int smax) {
-  pdl_entry();
-  constexpr int NB = 32, KS = kThreads / NB;  // 8 k-slices (one warp each) x 32 columns
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y;
-  const ElimDesc d = P.elims[t.e];
-  const int n = d.n, s = d.s, b = d.b;
-  if (s == 0 || b == 0) return;
-  const Scr S = scratch_of(P, d, e, NB);
-  const double2* M = S.M;
-  double2* Xs = reinterpret_cast<double2*>(smem_raw);  // [b][s] (row stride s)
-  double2* red = Xs + (size_t)kSkinnyB * smax;         // [KS][b][32] partial sums, then Z [b][32]
-  const int tid = threadIdx.x, c = tid & 31, ks = tid >> 5;
-  const int steps = (s + NB - 1) / NB;
-  for (int j = steps - 1; j >= 0; --j) {
-    const int j0 = j * NB, jb = min(NB, s - j0), j1 = j0 + jb;
-    double2 acc[kSkinnyB];
-#pragma unroll
-    for (int i = 0; i < kSkinnyB; ++i) acc[i] = cz();
-    if (c < jb) {
-      const double2* col = M + j0 + c;
-      int k = j1 + ks;
-      for (; k + 7 * KS < s; k += 8 * KS) {  // 8 rows in flight
-        double2 l[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) l[u] = col[(int64_t)(k + u * KS) * n];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-          for (int i = 0; i < kSkinnyB; ++i)
-            if (i < b) acc[i] = cfma(acc[i], Xs[(size_t)i * s + k + u * KS], l[u]);
-      }
-      for (; k < s; k += KS) {
-        const double2 l = col[(int64_t)k * n];
-#pragma unroll
-        for (int i = 0; i < kSkinnyB; ++i)
-          if (i < b) acc[i] = cfma(acc[i], Xs[(size_t)i * s + k], l);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < kSkinnyB; ++i)
-      if (i < b) red[(ks * kSkinnyB + i) * NB + c] = acc[i];
-    __syncthreads();
-    // Z = Y_j - sum over the k-slices (fixed order), by thread (i, c)
-    const int zi = tid >> 5;  // row i (KS == kSkinnyB)
-    double2 z = cz();
-    if (zi < b && c < jb) {
-      double2 sum = red[(0 * kSkinnyB + zi) * NB + c];
-#pragma unroll
-      for (int q = 1; q < KS; ++q) {
-        const double2 v = red[(q * kSkinnyB + zi) * NB + c];
-        sum.x += v.x;
-        sum.y += v.y;
-      }
-      z = csub(M[(int64_t)(s + zi) * n + j0 + c], sum);
-    }
-    __syncthreads();
-    red[zi * NB + c] = z;  // Z [b][32] (zero beyond b / jb)
-    __syncthreads();
-    if (zi < b && c < jb) {  // X_j = Z L_jj^-1
-      const double2* li = S.LINV + (int64_t)j * NB * NB + c;
-      double2 x = cz();
-#pragma unroll 8
-      for (int q = 0; q < NB; ++q) x = cfma(x, red[zi * NB + q], li[q * NB]);
-      Xs[(size_t)zi * s + j0 + c] = x;
-      S.X[(int64_t)zi * s + j0 + c] = x;
-    }
-    __syncthreads();
-  }
-}
-
-// T_S[:, c0:c0+64) = MS[s:, c0:..) - X MS[:s, c0:..), one CTA per (elimination, 64-column block, energy)
-__global__ void __launch_bounds__(kThreads) tgemm_skinny_kernel(SolveParams P, const Task* tasks, int nb, int smax) {
-  pdl_entry();
-  constexpr int CB = 64, KS = kThreads / CB;  // 4 k-slices x 64 columns
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Task t = tasks[blockIdx.x];
-  const int e = blockIdx.y;
-  const ElimDesc d = P.elims[t.e];
-  const int n = d.n, s = d.s, b = d.b;
-  if (s == 0 || b == 0) return;
-  const Scr S = scratch_of(P, d, e, nb);
-  double2* MS = S.MS;
-  double2* Xs = reinterpret_cast<double2*>(smem_raw);  // [b][s]
-  double2* red = Xs + (size_t)kSkinnyB * smax;         // [KS][b][64]
-  const int tid = threadIdx.x, c = tid % CB, ks = tid / CB;
-  const int c0 = t.b * CB;
-  const bool cok = c0 + c < s;
-  for (int q = tid; q < b * s; q += kThreads) Xs[q] = S.X[q];
-  __syncthreads();
-  double2 acc[kSkinnyB];
-#pragma unroll
-  for (int i = 0; i < kSkinnyB; ++i) acc[i] = cz();
-  if (cok) {
-    const double2* col = MS + c0 + c;
-    int k = ks;
-    for (; k + 7 * KS < s; k += 8 * KS) {
-      double2 m[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) m[u] = col[(int64_t)(k + u * KS) * n];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int i = 0; i < kSkinnyB; ++i)
-          if (i < b) acc[i] = cfma(acc[i], Xs[(size_t)i * s + k + u * KS], m[u]);
-    }
-    for (; k < s; k += KS) {
-      const double2 m = col[(int64_t)k * n];
-#pragma unroll
-      for (int i = 0; i < kSkinnyB; ++i)
-        if (i < b) acc[i] = cfma(acc[i], Xs[(size_t)i * s + k], m);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < kSkinnyB; ++i)
-    if (i < b) red[(ks * kSkinnyB + i) * CB + c] = acc[i];
-  __syncthreads();
-  for (int q = tid; q < b * CB; q += kThreads) {
-    const int i = q / CB, cc = q % CB;
-    if (c0 + cc >= s) continue;
-    double2 sum = red[(0 * kSkinnyB + i) * CB + cc];
-#pragma unroll
-    for (int w = 1; w < KS; ++w) {
-      const double2 v = red[(w * kSkinnyB + i) * CB + cc];
-      sum.x += v.x;
-      sum.y += v.y;
-    }
-    double2* dst = MS + (int64_t)(s + i) * n + c0 + cc;
-    *dst = csub(*dst, sum);
-  }
-}
-
 // ---- pivot permutation sigma and its inverse (+ L for the unit-test shim)
 __device__ void finish_body(const SolveParams& P, int64_t eidx, const ElimDesc& d, int e, int nb, int* sig) {
   const int tid = threadIdx.x;
@@ -3069,8 +2925,6 @@ int set_attrs(find_status* st) {
   if (g_attrs_done[dev]) return FIND_OK;
   const int mx = (int)kMaxSmem;
   CUDA_TRY(cudaFuncSetAttribute(small_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CUDA_TRY(cudaFuncSetAttribute(xsolve_skinny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CUDA_TRY(cudaFuncSetAttribute(tgemm_skinny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile64::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(mid_elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CUDA_TRY(cudaFuncSetAttribute(panel_smem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -3395,17 +3249,6 @@ void tall_shape(const LaunchGroup& G, const LaunchSpec& L, int& rpt, int& T) {
   T = 32 * (((rmax + rpt - 1) / rpt + 31) / 32);
 }
 
-// Streaming kernels for the X solve and T_S of groups whose eliminations all have b <= kSkinnyB
-// boundary rows against a large S (FIND_B200_SKINNY=0: the DMMA tile kernels).
-const bool g_skinny = [] {
-  const char* f = std::getenv("FIND_B200_SKINNY");
-  return !(f && f[0] == '0');
-}();
-bool use_skinny(const LaunchGroup& G, const LaunchSpec& L) {
-  return g_skinny && L.nb == 32 && G.max_b <= kSkinnyB && G.max_s >= kSkinnyMinS &&
-         skinny_smem(kSkinnyB, G.max_s) <= kMaxSmem;
-}
-
 const bool g_rsym_down = [] {
   const char* f = std::getenv("FIND_B200_RSYM_DOWN");
   return f && f[0] == '1';
@@ -3543,9 +3386,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
             launch_k(trail_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.step, L.nb);
           break;
         case kLXSolve:
-          if (use_skinny(G, L))
-            launch_k(xsolve_skinny_kernel, grid, kThreads, skinny_smem(kSkinnyB, G.max_s), stream, prm, tk, G.max_s);
-          else if (L.nb == 32) launch_k(xsolve_kernel<32>, grid, kThreads, xsolve_smem<32>(), stream, prm, tk);
+          if (L.nb == 32) launch_k(xsolve_kernel<32>, grid, kThreads, xsolve_smem<32>(), stream, prm, tk);
           else if (L.nb == 16) launch_k(xsolve_kernel<16>, grid, kThreads, xsolve_smem<16>(), stream, prm, tk);
           else if (L.nb == 8) launch_k(xsolve_kernel<8>, grid, kThreads, xsolve_smem<8>(), stream, prm, tk);
           else launch_k(xsolve_kernel<4>, grid, kThreads, xsolve_smem<4>(), stream, prm, tk);
@@ -3554,9 +3395,7 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           launch_k(finish_kernel, grid, kThreads, std::max<size_t>((size_t)G.max_s * sizeof(int), 16), stream, prm, tk, L.nb);
           break;
         case kLTGemm:
-          if (use_skinny(G, L))
-            launch_k(tgemm_skinny_kernel, grid, kThreads, skinny_smem(kSkinnyB, G.max_s), stream, prm, tk, L.nb, G.max_s);
-          else if (prm.use_tma && G.max_s >= g_tma_min_s)
+          if (prm.use_tma && G.max_s >= g_tma_min_s)
             launch_k(tile_tma_kernel<kLTGemm>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
                      (int64_t)cnt, nE, 0, L.nb, prm.tile_ctr + si);
           else

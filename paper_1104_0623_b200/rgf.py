@@ -71,26 +71,55 @@ def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def _blocks_device(mats, nx: int, ny: int, dev):
-    """Dense line blocks of a batch of CSR matrices sharing one pattern, scattered on the
-    device: D [nE, ny, nx, nx], E / F [nE, ny-1, nx, nx]."""
-    import torch
+class _Lines:
+    """Dense line blocks of a batch of CSR matrices sharing one pattern, built on the device one line at
+    a time (D(i) / E(i) / F(i): [nE, nx, nx]); holding all 3 ny blocks at once is 48 GB per energy point
+    at 1024 x 1024.  ediag / fdiag: the coupling blocks with no nonzero off their diagonal (rgf.py:75-81)."""
 
-    m0 = mats[0].tocoo()
-    r, c = m0.row.astype(np.int64), m0.col.astype(np.int64)
-    ly, lc = r // nx, c // nx
-    vals = np.stack([np.asarray(_coo_on(m, m0), np.complex128) for m in mats])
-    v = torch.from_numpy(vals).to(dev)
-    ne = len(mats)
-    D = torch.zeros((ne, ny, nx, nx), dtype=torch.complex128, device=dev)
-    E = torch.zeros((ne, max(ny - 1, 0), nx, nx), dtype=torch.complex128, device=dev)
-    F = torch.zeros_like(E)
-    for dst, sel, line in ((D, ly == lc, ly), (E, lc == ly + 1, ly), (F, ly == lc + 1, lc)):
-        if not sel.any():
-            continue
-        idx = torch.from_numpy(((line[sel] * nx + r[sel] % nx) * nx + c[sel] % nx)).to(dev)
-        dst.view(ne, -1)[:, idx] = v[:, torch.from_numpy(np.nonzero(sel)[0]).to(dev)]  # (row, col) unique
-    return D, E, F
+    def __init__(self, mats, nx: int, ny: int, dev):
+        import torch
+
+        self.nx, self.ny, self.dev, self.ne = nx, ny, dev, len(mats)
+        m0 = mats[0].tocoo()
+        r, c = m0.row.astype(np.int64), m0.col.astype(np.int64)
+        ly, lc = r // nx, c // nx
+        vals = np.stack([np.asarray(_coo_on(m, m0), np.complex128) for m in mats])
+        self.vals = torch.from_numpy(vals).to(dev)
+        local = (r % nx) * nx + c % nx
+        offd = (r % nx) != (c % nx)
+        self.idx, self.pos, self.off = {}, {}, {}
+        nz_off = {}
+        for kind, sel, line, nl in (("D", ly == lc, ly, ny), ("E", lc == ly + 1, ly, ny - 1), ("F", ly == lc + 1, lc, ny - 1)):
+            where = np.nonzero(sel)[0]
+            order = np.argsort(line[where], kind="stable")
+            where = where[order]
+            self.pos[kind] = torch.from_numpy(where).to(dev)
+            self.idx[kind] = torch.from_numpy(local[where]).to(dev)
+            self.off[kind] = np.searchsorted(line[where], np.arange(max(nl, 0) + 1))
+            flag = np.zeros(max(nl, 0), bool)  # lines with a nonzero off-diagonal entry in some energy point
+            hot = where[offd[where] & np.any(vals[:, where] != 0, axis=0)]
+            flag[line[hot]] = True
+            nz_off[kind] = flag
+        self.ediag = [not bool(x) for x in nz_off["E"]]
+        self.fdiag = [not bool(x) for x in nz_off["F"]]
+
+    def _block(self, kind: str, i: int):
+        import torch
+
+        out = torch.zeros((self.ne, self.nx * self.nx), dtype=torch.complex128, device=self.dev)
+        a, b = int(self.off[kind][i]), int(self.off[kind][i + 1])
+        if b > a:
+            out[:, self.idx[kind][a:b]] = self.vals[:, self.pos[kind][a:b]]  # (row, col) unique
+        return out.view(self.ne, self.nx, self.nx)
+
+    def D(self, i: int):
+        return self._block("D", i)
+
+    def E(self, i: int):
+        return self._block("E", i)
+
+    def F(self, i: int):
+        return self._block("F", i)
 
 
 def _coo_on(m, m0) -> np.ndarray:
@@ -101,15 +130,6 @@ def _coo_on(m, m0) -> np.ndarray:
         if np.array_equal(cm.row, m0.row) and np.array_equal(cm.col, m0.col):
             return cm.data
     return np.asarray(m[m0.row, m0.col]).ravel()
-
-
-def _is_diag_batch(X) -> bool:
-    """rgf.py:75-81: no entry off the diagonal (for every energy point)."""
-    import torch
-
-    nx = X.shape[-1]
-    off = X * (1 - torch.eye(nx, dtype=X.dtype, device=X.device))
-    return not bool(torch.any(off != 0))
 
 
 class _Dense:
@@ -219,9 +239,8 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
     led = FlopLedger()  # forward + backward: rgf_gr_diag's charges
     infos: list = []
     dn = _Dense(nx, len(mats), dev)
-    D, E, F = _blocks_device(mats, nx, ny, dev)
-    ediag = [_is_diag_batch(E[:, i]) for i in range(ny - 1)]
-    fdiag = [_is_diag_batch(F[:, i]) for i in range(ny - 1)]
+    A = _Lines(mats, nx, ny, dev)
+    ediag, fdiag = A.ediag, A.fdiag
     c3 = nx ** 3
 
     def charge_sandwich(ld, rd):
@@ -232,11 +251,11 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
 
     # forward: left-connected g_i (rgf.py:108-115)
     gl_blk = [None] * ny
-    gl_blk[0] = dn.inv(D[:, 0], 0, infos)
+    gl_blk[0] = dn.inv(A.D(0), 0, infos)
     led.add("rgf", c3)
     for i in range(1, ny):
-        gl_blk[i] = dn.inv(_sandwich(dn, F[:, i - 1], gl_blk[i - 1], E[:, i - 1], fdiag[i - 1], ediag[i - 1],
-                                     D[:, i], -1), i, infos)
+        gl_blk[i] = dn.inv(_sandwich(dn, A.F(i - 1), gl_blk[i - 1], A.E(i - 1), fdiag[i - 1], ediag[i - 1],
+                                     A.D(i), -1), i, infos)
         charge_sandwich(fdiag[i - 1], ediag[i - 1])
         led.add("rgf", c3)
     led_forward = FlopLedger(led.multiplications, dict(led.by_kernel))
@@ -245,7 +264,7 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
     g_full = gl_blk[ny - 1]
     gr[:, (ny - 1) * nx:] = g_full.diagonal(dim1=-2, dim2=-1)
     for i in range(ny - 2, -1, -1):
-        t = _sandwich(dn, E[:, i], g_full, F[:, i], ediag[i], fdiag[i])
+        t = _sandwich(dn, A.E(i), g_full, A.F(i), ediag[i], fdiag[i])
         charge_sandwich(ediag[i], fdiag[i])
         g_full = dn.mm(dn.mm(gl_blk[i], t), gl_blk[i], gl_blk[i], +1)
         led.add("rgf", 2 * c3)
@@ -259,7 +278,7 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
         raise ValueError("compute_gless requires a scattering matrix")
     sm = sigma.matrix.tocsr()
     _check_tridiagonal(sm, nx)
-    SD, SE, SF = _blocks_device([sm], nx, ny, dev)  # Sigma^< is energy independent
+    S = _Lines([sm], nx, ny, dev)  # Sigma^< is energy independent
     sc = sm.tocoo()
     up_nz = np.zeros(max(ny - 1, 0), bool)  # Sigma coupling blocks with a nonzero entry (host, no sync)
     lo_nz = np.zeros(max(ny - 1, 0), bool)
@@ -268,10 +287,10 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
     lo_nz[(sc.col // nx)[nzm & (sc.row // nx == sc.col // nx + 1)]] = True
     # right-connected g^R (rgf.py:164-168; its ledger repeats the forward one)
     gr_blk = [None] * ny
-    gr_blk[ny - 1] = dn.inv(D[:, ny - 1], ny - 1, infos)
+    gr_blk[ny - 1] = dn.inv(A.D(ny - 1), ny - 1, infos)
     led.add("rgf", c3)
     for i in range(ny - 2, -1, -1):
-        gr_blk[i] = dn.inv(_sandwich(dn, E[:, i], gr_blk[i + 1], F[:, i], ediag[i], fdiag[i], D[:, i], -1), i, infos)
+        gr_blk[i] = dn.inv(_sandwich(dn, A.E(i), gr_blk[i + 1], A.F(i), ediag[i], fdiag[i], A.D(i), -1), i, infos)
         charge_sandwich(ediag[i], fdiag[i])
         led.add("rgf", c3)
 
@@ -281,20 +300,22 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
         prev = None
         for i in order:
             if prev is None:
-                s_conn[i] = SD[:, i].clone()
+                s_conn[i] = S.D(i)
             else:
                 if reverse:
-                    coup, cdiag, sig_sb, sig_bs = E[:, i], ediag[i], SF[:, i], SE[:, i]
+                    coup, cdiag = A.E(i), ediag[i]
                     nz_sb, nz_bs = lo_nz[i], up_nz[i]
+                    sig_sb, sig_bs = (S.F(i) if nz_sb else None), (S.E(i) if nz_bs else None)
                 else:
-                    coup, cdiag, sig_sb, sig_bs = F[:, i - 1], fdiag[i - 1], SE[:, i - 1], SF[:, i - 1]
+                    coup, cdiag = A.F(i - 1), fdiag[i - 1]
                     nz_sb, nz_bs = up_nz[i - 1], lo_nz[i - 1]
+                    sig_sb, sig_bs = (S.E(i - 1) if nz_sb else None), (S.F(i - 1) if nz_bs else None)
                 if cdiag:
                     l_fac = coup.diagonal(dim1=-2, dim2=-1).unsqueeze(-1) * g_conn[prev]
                 else:
                     l_fac = dn.mm(coup, g_conn[prev])
                     led.add("rgf", c3)
-                term = dn.mm(dn.mm(l_fac, s_conn[prev]), l_fac, SD[:, i], +1, bh=True)
+                term = dn.mm(dn.mm(l_fac, s_conn[prev]), l_fac, S.D(i), +1, bh=True)
                 led.add("rgf", 2 * c3)
                 if nz_sb:
                     term = dn.mm(l_fac, sig_sb, term, -1)
@@ -308,14 +329,15 @@ def rgf_batch(mesh, a_list, sigma=None, compute_gless: bool = True):
     s_right = connected(gr_blk, True)
     gless = torch.empty_like(gr)
     for i in range(ny):  # rgf.py:193-207
-        u = D[:, i]
+        u = A.D(i)
         if i > 0:
-            u = _sandwich(dn, F[:, i - 1], gl_blk[i - 1], E[:, i - 1], fdiag[i - 1], ediag[i - 1], u, -1)
+            u = _sandwich(dn, A.F(i - 1), gl_blk[i - 1], A.E(i - 1), fdiag[i - 1], ediag[i - 1], u, -1)
             charge_sandwich(fdiag[i - 1], ediag[i - 1])
         if i + 1 < ny:
-            u = _sandwich(dn, E[:, i], gr_blk[i + 1], F[:, i], ediag[i], fdiag[i], u, -1)
+            u = _sandwich(dn, A.E(i), gr_blk[i + 1], A.F(i), ediag[i], fdiag[i], u, -1)
             charge_sandwich(ediag[i], fdiag[i])
-        r_i = s_left[i] + s_right[i] - SD[:, i]
+        r_i = s_left[i] + s_right[i] - S.D(i)
+        s_left[i] = s_right[i] = None  # (release the line's connected blocks)
         g_ii = dn.inv(u, i, infos)
         led.add("rgf", c3)
         gless[:, i * nx:(i + 1) * nx] = dn.mm(dn.mm(g_ii, r_i), g_ii, bh=True).diagonal(dim1=-2, dim2=-1)

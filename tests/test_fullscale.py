@@ -7,7 +7,7 @@ tests/golden/make_fullscale.py and make_fullscale_cfg4.py):
   cfg2  reference solve, energies 0, 21, 42, 63
   cfg3  reference RGF (rgf.py:121-208), energies 0, 31
   cfg4  pinned oracle port (reference FIND / RGF infeasible at 1024x1024), energy 0, every 8th node
-        (the committed subset of the 1 048 576 nodes)
+        (the committed subset of the 1 048 576 nodes); and FIND vs the GPU RGF path on every node, energy 3
 
 Bound (north star): max|Δ| / max|ref| <= 1e-10 per energy point, for G^r and G^<.
 """
@@ -112,3 +112,29 @@ def test_gpu_rgf_fullscale_cfg3(cuda):
         print(f"cfg3 RGF energy {k}: gr {eg:.2e} gl {el:.2e}")
         assert eg <= TOL and el <= TOL, (k, eg, el)
 
+
+@pytest.mark.gpu
+def test_gpu_find_vs_gpu_rgf_cfg4(cuda):
+    """cfg4 at full size, every node: the FIND path against the GPU RGF path (an independent algorithm on the
+    dense primitives, pinned to the reference RGF at cfg3 full size above), energy point 3.  The RGF holds
+    4 x 1024 connected blocks of 16 MB (64 GB) on the device."""
+    import torch
+
+    from paper_1104_0623_b200 import Mesh, SolverConfig, SparseOperator, solve_batch
+    from paper_1104_0623_b200.configs import config_problem
+    from paper_1104_0623_b200.plan import release_workspaces
+    from paper_1104_0623_b200.rgf import rgf_batch
+
+    if torch.cuda.mem_get_info()[0] < 100 * 2 ** 30:
+        pytest.skip("needs 100 GB of free device memory")
+    p = config_problem(4)
+    mesh, k = Mesh(p.nx, p.ny), 3
+    a, s = SparseOperator(p.a_csr(k)), SparseOperator(p.sigma_csr())
+    release_workspaces()
+    gr, gl, _ = rgf_batch(mesh, [a], s)
+    torch.cuda.empty_cache()
+    res = solve_batch(mesh, [a], s, SolverConfig())
+    eg, el = rel_err(res.gr_diag[0], gr[0]), rel_err(res.gless_diag[0], gl[0])
+    print(f"cfg4 energy {k}: FIND vs GPU RGF gr {eg:.2e} gl {el:.2e}")
+    release_workspaces()
+    assert eg <= TOL and el <= TOL, (eg, el)

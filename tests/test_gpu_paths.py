@@ -108,37 +108,6 @@ def test_tall_panel_kernel_is_bit_identical(cuda, nx, ny):
     assert out[0] == out[1]
 
 
-DUMP_SCRIPT = r"""
-import sys
-import numpy as np
-sys.path.insert(0, {root!r})
-from paper_1104_0623_b200.configs import build_problem
-from paper_1104_0623_b200.plan import plan_for
-from paper_1104_0623_b200.solver import sigma_symmetry, solve_values
-p = build_problem({nx}, {ny}, [0.9, 2.7], seed=23, stencil=5)
-plan, _ = plan_for(p.nx, p.ny, p.indptr, p.indices)
-gr, gl, _, _ = solve_values(plan, p.a_vals_all(), p.s_vals, sigma_sym=sigma_symmetry(p.sigma_csr()))
-np.savez({out!r}, gr=gr, gl=gl)
-"""
-
-
-@pytest.mark.parametrize("nx,ny", [(600, 12), (1030, 6)])
-def test_skinny_streaming_kernels_match_the_tile_kernels(cuda, tmp_path, nx, ny):
-    """X solve / T_S of the contact-row eliminations (b <= 8 against s ~ nx) on the streaming kernels against
-    the DMMA tile kernels: same sums in a different association."""
-    res = []
-    for v in ("1", "0"):
-        out = str(tmp_path / f"skinny{v}.npz")
-        code = DUMP_SCRIPT.format(root=str(ROOT), nx=nx, ny=ny, out=out)
-        r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "FIND_B200_SKINNY": v}, capture_output=True,
-                           text=True, timeout=900)
-        assert r.returncode == 0, r.stderr[-2000:]
-        res.append(np.load(out))
-    for k in ("gr", "gl"):
-        d = np.abs(res[0][k] - res[1][k]).max() / np.abs(res[1][k]).max()
-        assert d < 1e-11, (k, d)
-
-
 @pytest.mark.gpu
 def test_two_devices_in_one_process():
     """Kernel attributes and side streams are per device: a solve on cuda:0 then on cuda:1 (needs 2 GPUs)."""
