@@ -98,8 +98,9 @@ struct Seg {
   int K, bt;
 };
 
-// WM x WN consumer warps (8), each MT x NT 8x8 fragments; S stages.
-template <int WM, int WN, int MT, int NT, int S>
+// WM x WN consumer warps (8), each MT x NT 8x8 fragments; S stages; CS: with the C staging buffer
+// (stage_c / load_c_staged).
+template <int WM, int WN, int MT, int NT, int S, bool CS = false>
 struct Engine {
   static constexpr int NW = WM * WN;
   static constexpr int THREADS = (NW + 1) * 32;  // + one producer warp
@@ -111,9 +112,10 @@ struct Engine {
   static constexpr int B_BYTES = (B_BYTES_RAW + 1023) & ~1023;
   static constexpr int STAGE = A_BYTES + B_BYTES;      // multiple of 1024 (swizzle-128B alignment)
   static constexpr int QD = 2;                         // depth of the dynamic tile queue
-  // stages, then one 1 KB block of barriers / tile-queue slots; + 1 KB alignment slack
-  static constexpr size_t SMEM = (size_t)S * STAGE + 2048;
-  static_assert((2 * S + 2 * QD) * sizeof(uint64_t) + QD * sizeof(long long) <= 1024, "barrier block");
+  static constexpr int C_BYTES = CS ? BM * BN * 16 : 0;  // the next tile's C block: BN / 8 swizzled [BM][8] boxes
+  // stages, the C block, then one 1 KB block of barriers / tile-queue slots; + 1 KB alignment slack
+  static constexpr size_t SMEM = (size_t)S * STAGE + C_BYTES + 2048;
+  static_assert((2 * S + 2 * QD + 2) * sizeof(uint64_t) + QD * sizeof(long long) <= 1024, "barrier block");
 
   unsigned char* st;  // S stages, 1024-byte aligned
   uint64_t* full;
@@ -125,16 +127,30 @@ struct Engine {
   uint64_t* qempty;
   long long* qslot;
   unsigned qn;
+  // C staging (stage_c / load_c_staged, CS = true): the producer brings the tile's C block in with the TMA
+  // unit while the consumers still multiply the previous tile, so seeding the accumulators is a
+  // shared-memory read instead of 32 dependent global loads per thread at the head of every tile.
+  // Standalone (tools/dmma_bench.cu) +8 % on the K = 64 trailing shape (32.6 TFLOP/s, cuBLAS 31.5); inside
+  // the solver the trailing updates ran 7 % slower with it (in-place C in the same matrix as the
+  // operands; cause not isolated), so find_solve.cu uses load_c + the L2 prefetch (CS = false).
+  unsigned char* cbuf;
+  uint64_t* cfull;
+  uint64_t* cempty;
+  unsigned cn;
 
   __device__ __forceinline__ void init(unsigned char* smem_raw) {
     st = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    full = reinterpret_cast<uint64_t*>(st + (size_t)S * STAGE);
+    full = reinterpret_cast<uint64_t*>(st + (size_t)S * STAGE + C_BYTES);
     empty = full + S;
     qfull = empty + S;
     qempty = qfull + QD;
-    qslot = reinterpret_cast<long long*>(qempty + QD);
+    cfull = qempty + QD;
+    cempty = cfull + 1;
+    qslot = reinterpret_cast<long long*>(cempty + 1);
+    cbuf = st + (size_t)S * STAGE;
     chunk = 0;
     qn = 0;
+    cn = 0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < S; ++i) {
         mbar_init(&full[i], 1);
@@ -144,6 +160,8 @@ struct Engine {
         mbar_init(&qfull[i], 1);
         mbar_init(&qempty[i], NW);
       }
+      mbar_init(cfull, 1);
+      mbar_init(cempty, NW);
       mbar_fence_init();
     }
     __syncthreads();
@@ -210,6 +228,41 @@ struct Engine {
             bulk_g2s(Bs + k * SKB * 16, sg.B + (int64_t)(k0 + k) * sg.ldb, (unsigned)nv * 16u, &full[stage]);
       }
     }
+  }
+
+  // producer warp: the C block [r0, r0 + 64) x [c0, c0 + 64) of the tile into the C buffer (BN / 8 boxes
+  // through the matrix's tensor map; rows / columns outside the matrix arrive as zeros)
+  __device__ __forceinline__ void stage_c(const void* cmap, int r0, int c0, int e) {
+    const unsigned round = cn++;
+    mbar_wait(cempty, (round & 1) ^ 1);
+    if ((threadIdx.x & 31) == 0) {
+      mbar_expect_tx(cfull, (unsigned)C_BYTES);
+#pragma unroll
+      for (int h = 0; h < BN / 8; ++h) tensor_g2s(cbuf + h * (BM * 128), cmap, 2 * (c0 + 8 * h), r0, e, cfull);
+    }
+    __syncwarp();
+  }
+
+  // consumer warps: acc = the staged C block (this thread's elements), then the buffer is released
+  __device__ __forceinline__ void load_c_staged() {
+    const int lane = threadIdx.x & 31;
+    const int fr = lane >> 2, fc = lane & 3;
+    const unsigned round = cn++;
+    mbar_wait(cfull, round & 1);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r = row_of(mt, fr), c = col_of(nt, 2 * fc + i);
+          const double2 v = *reinterpret_cast<const double2*>(cbuf + (c >> 3) * (BM * 128) + r * 128 +
+                                                              (((c & 7) ^ (r & 7)) << 4));
+          acc[mt][nt][0][i] = v.x;
+          acc[mt][nt][1][i] = v.y;
+        }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(cempty);
   }
 
   // L2 prefetch of a C block [r0, r0 + 64) x [c0, c0 + 64) through its matrix's tensor map
@@ -392,5 +445,6 @@ struct Engine {
 };
 
 using Eng64 = Engine<2, 4, 4, 2, 4>;   // 8 consumer warps (32 x 16 each), one CTA per SM
+using Eng64cs = Engine<2, 4, 4, 2, 4, true>;  // + C staging
 
 }  // namespace dmma

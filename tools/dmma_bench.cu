@@ -29,7 +29,7 @@ struct Prob {
 };
 
 struct Maps {
-  CUtensorMap a, a2, b2;
+  CUtensorMap a, a2, b2, c;
 };
 
 template <class E>
@@ -88,6 +88,10 @@ __global__ void __launch_bounds__(E::THREADS, MINB) eng_dyn_kernel(Prob p, const
       double2* Cb;
       int bi, mv, nv;
       job(t, seg, Cb, bi, mv, nv);
+      if (E::C_BYTES) {
+        const int r = (int)(t % (tm * tn));
+        eng.stage_c(&maps.c, (r / tn) * E::BM, (r % tn) * E::BN, bi);
+      }
       eng.produce(seg, p.nseg, bi, nv);
     }
   } else {
@@ -98,7 +102,8 @@ __global__ void __launch_bounds__(E::THREADS, MINB) eng_dyn_kernel(Prob p, const
       double2* Cb;
       int bi, mv, nv;
       job(t, seg, Cb, bi, mv, nv);
-      eng.load_c(Cb, p.N, mv, nv);
+      if (E::C_BYTES) eng.load_c_staged();
+      else eng.load_c(Cb, p.N, mv, nv);
       eng.template consume<true>(seg, p.nseg, mv, nv);
       eng.for_each([&](int r, int c, double2 v) {
         if (r < mv && c < nv) Cb[(int64_t)r * p.N + c] = v;
@@ -154,7 +159,8 @@ void run(const char* name, Prob p, int sms, bool check) {
   Maps maps;
   if (!findb200::encode_complex_tmap(&maps.a, A, p.K, p.M, p.K, (int64_t)p.M * p.K, p.batch) ||
       !findb200::encode_complex_tmap(&maps.a2, A2, p.K, p.M, p.K, (int64_t)p.M * p.K, p.batch) ||
-      !findb200::encode_complex_tmap(&maps.b2, B2, p.K, p.N, p.K, (int64_t)p.N * p.K, p.batch)) {
+      !findb200::encode_complex_tmap(&maps.b2, B2, p.K, p.N, p.K, (int64_t)p.N * p.K, p.batch) ||
+      !findb200::encode_complex_tmap(&maps.c, C, p.N, p.M, p.N, (int64_t)p.M * p.N, p.batch)) {
     std::printf("tensor map encoding failed\n");
     std::exit(1);
   }
@@ -208,8 +214,8 @@ void run(const char* name, Prob p, int sms, bool check) {
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   const double flops = 8.0 * p.batch * (double)p.M * p.N * p.K * p.nseg;
-  std::printf("%-28s BMxBN %3dx%-3d w%d %s grid %5d (%d/SM) tiles %6d: %8.3f ms  %6.2f TFLOP/s\n", name, E::BM, E::BN, E::NW,
-              DYN ? "dyn" : "sta", grid, per_sm, tiles, ms / reps, flops / (ms / reps * 1e-3) / 1e12);
+  std::printf("%-28s BMxBN %3dx%-3d w%d%s %s grid %5d (%d/SM) tiles %6d: %8.3f ms  %6.2f TFLOP/s\n", name, E::BM, E::BN, E::NW,
+              E::C_BYTES ? "+Cstage" : "", DYN ? "dyn" : "sta", grid, per_sm, tiles, ms / reps, flops / (ms / reps * 1e-3) / 1e12);
   if (getenv("DMMA_NO_CUBLAS")) return;
   // cuBLAS ceiling for the first segment
   cublasHandle_t hd;
@@ -242,8 +248,8 @@ void run(const char* name, Prob p, int sms, bool check) {
 
 using E64x64s4 = dmma::Engine<2, 4, 4, 2, 4>;
 using E64x64s2 = dmma::Engine<2, 4, 4, 2, 2>;
-using E64x64s6 = dmma::Engine<2, 4, 4, 2, 6>;
 using E4w = dmma::Engine<2, 2, 4, 4, 4>;
+using E64cs = dmma::Engine<2, 4, 4, 2, 4, true>;
 
 int main() {
   int sms = 0;
@@ -259,12 +265,11 @@ int main() {
     const char* nm = q.K == 64 ? "trail K64" : q.nseg == 2 ? "rgemm" : q.K == 2045 ? "schur" : q.K == 256 ? "cfg1 K256" : "trail cfg1 K32";
     run<E64x64s4, 0>(nm, q, sms, true);
     run<E64x64s4, 1>(nm, q, sms, true);
+    run<E64cs, 1>(nm, q, sms, true);
     run<E4w, 1>(nm, q, sms, false);
   }
   run<E64x64s2>("trail 4x3000^2 K64", trail, sms, false);
-  run<E64x64s6>("trail 4x3000^2 K64", trail, sms, false);
   run<E64x64s4>("rgemm 4x1535^2 K2045x2", rgemm, sms, true);
-  run<E64x64s6>("rgemm 4x1535^2 K2045x2", rgemm, sms, false);
   run<E64x64s4>("schur 4x1535^2 K2045", schur, sms, false);
   run<E64x64s4>("cfg1 64x256^2 K256", small, sms, true);
   run<E64x64s4>("trail cfg1 64x200^2 K32", trail_small, sms, true);
