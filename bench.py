@@ -359,6 +359,8 @@ def run_b200(args):
     if NCU_KERNELS.exists():
         rec = json.loads(NCU_KERNELS.read_text()).get(f"{dom}_kernel", {})
         traffic = rec.get("dram_bytes_per_launch")
+        if traffic is not None and rec.get("energies_in_capture"):  # the capture ran fewer energy points per launch
+            traffic = int(traffic * c0 / rec["energies_in_capture"])
     roofline = {
         "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
@@ -367,7 +369,8 @@ def run_b200(args):
         "work": (f"executed complex MACs x 8 of those launches (paper_1104_0623_b200/workmodel.py) / their CUDA-event "
                  f"durations, every launch group run alone on the solve stream (one serialized find_solve call of "
                  f"{c0} energy points); dominant = the FP64 tensor-core (DMMA) kind with the largest serialized "
-                 f"time; traffic = ncu --set full dram bytes per launch of that kernel ({NCU_KERNELS.name})"),
+                 f"time; traffic = ncu dram__bytes_read + dram__bytes_write per launch of that kernel, averaged over "
+                 f"every such launch of one call and scaled to this call's energy points ({NCU_KERNELS.name})"),
     }
     g = plan.groups
     ngroups = len(g["count"])

@@ -26,7 +26,7 @@ for r in rows[hi + 1:]:
     if len(r) < len(h):
         continue
     nm = re.sub(r"\(anonymous namespace\)::|<unnamed>::|^void ", "", r[idx["Kernel Name"]]).split("(")[0]
-    m = re.match(r"tile_tma_kernel<\(?(?:int\)?)?(\d+)>", nm)
+    m = re.match(r"tile_tma_kernel<\(?(?:int\)?)?(\d+)>", nm) or re.search(r"tile_tma_kernelILi(\d+)E", nm)
     if m:  # the TMA tile engine's four launch kinds (LaunchKind, plan.h): named like the cp.async kernels they replace
         nm = {4: "trail_kernel", 8: "tgemm_kernel", 9: "rgemm_kernel", 11: "schur_kernel"}.get(int(m.group(1)), nm) + "[tma]"
     nm = re.sub(r"<.*", "", nm)
