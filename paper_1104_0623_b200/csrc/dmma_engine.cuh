@@ -131,9 +131,9 @@ struct Engine {
   // unit while the consumers still multiply the previous tile, so seeding the accumulators is a
   // shared-memory read instead of 32 dependent global loads per thread at the head of every tile.
   // Standalone (tools/dmma_bench.cu) +8 % on the K = 64 trailing shape (32.6 TFLOP/s, cuBLAS 31.5); inside
-  // the solver the trailing updates ran 7 % slower with it (probably the 16-byte-only alignment of the
-  // scratch rows: n * 16 B is not a multiple of 128 B there), so find_solve.cu uses load_c + the L2
-  // prefetch (CS = false).
+  // the solver the trailing updates ran 7 % slower with it (ncu: same DRAM traffic, the consumer warps
+  // run in lockstep and contend for the FP64 pipe instead of overlapping one warp's epilogue with
+  // another's MMAs), so find_solve.cu uses load_c + the L2 prefetch unless FIND_B200_CSTAGE=1.
   unsigned char* cbuf;
   uint64_t* cfull;
   uint64_t* cempty;

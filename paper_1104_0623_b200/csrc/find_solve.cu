@@ -25,6 +25,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -2346,9 +2347,9 @@ __device__ __forceinline__ bool tile_job(const SolveParams& P, const Task& t, in
   return true;
 }
 
-template <int KIND>
+template <int KIND, class Eng>
 __device__ __forceinline__ void tile_store(const SolveParams& P, const Task& t, int e, int j, int nb, const TileJob& J,
-                                           const TmaEng& eng) {
+                                           const Eng& eng) {
   const ElimDesc d = P.elims[t.e];
   const int n = d.n, s = d.s, b = d.b;
   if (KIND == kLTrail) {
@@ -2397,18 +2398,19 @@ __device__ __forceinline__ void tile_store(const SolveParams& P, const Task& t, 
   }
 }
 
-template <int KIND>
+template <int KIND, bool CS = false>
 __global__ void __launch_bounds__(TmaEng::THREADS, 1) tile_tma_kernel(SolveParams P, const Task* tasks, int64_t cnt,
                                                                      int nE, int j, int nb,
                                                                      unsigned long long* counter) {
+  using Eng = typename std::conditional<CS, dmma::Eng64cs, TmaEng>::type;
   pdl_entry();
   extern __shared__ __align__(16) unsigned char smem_raw[];  // Engine::init aligns to 1024
-  TmaEng eng;
+  Eng eng;
   eng.init(smem_raw);
   const int64_t total = cnt * nE;
   // tiles are drawn in order from the launch's counter (zeroed by the solve call): the tiles of
   // one launch differ in K, in skipped work and in their epilogues
-  if (TmaEng::producer()) {
+  if (Eng::producer()) {
     for (;;) {
       const int64_t q = eng.next_tile_p(counter, total);
       if (q < 0) break;
@@ -2416,7 +2418,8 @@ __global__ void __launch_bounds__(TmaEng::THREADS, 1) tile_tma_kernel(SolveParam
       const Task t = tasks[q % cnt];
       TileJob J;
       if (!tile_job<KIND>(P, t, e, j, nb, J)) continue;
-      TmaEng::prefetch_c(J.cmap, J.cr, J.cc, e);
+      if (CS) eng.stage_c(J.cmap, J.cr, J.cc, e);
+      else Eng::prefetch_c(J.cmap, J.cr, J.cc, e);
       eng.produce(J.seg, J.nseg, e, J.nv);
     }
   } else {
@@ -2427,7 +2430,8 @@ __global__ void __launch_bounds__(TmaEng::THREADS, 1) tile_tma_kernel(SolveParam
       const Task t = tasks[q % cnt];
       TileJob J;
       if (!tile_job<KIND>(P, t, e, j, nb, J)) continue;
-      eng.load_c(J.C, P.elims[t.e].n, J.mv, J.nv);
+      if (CS) eng.load_c_staged();
+      else eng.load_c(J.C, P.elims[t.e].n, J.mv, J.nv);
       eng.template consume<true>(J.seg, J.nseg, J.mv, J.nv);
       tile_store<KIND>(P, t, e, j, nb, J, eng);
     }
@@ -2958,6 +2962,8 @@ int set_attrs(find_status* st) {
   CUDA_TRY(cudaFuncSetAttribute(offdiag_small_kernel<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)offdiag_small_smem<64>()));
   CUDA_TRY(cudaFuncSetAttribute(tile_tma_kernel<kLTrail>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaEng::SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(tile_tma_kernel<kLTrail, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)dmma::Eng64cs::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(tile_tma_kernel<kLSchur>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaEng::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(tile_tma_kernel<kLTGemm>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaEng::SMEM));
   CUDA_TRY(cudaFuncSetAttribute(tile_tma_kernel<kLRGemm>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TmaEng::SMEM));
@@ -3249,6 +3255,13 @@ void tall_shape(const LaunchGroup& G, const LaunchSpec& L, int& rpt, int& T) {
   T = 32 * (((rmax + rpt - 1) / rpt + 31) / 32);
 }
 
+// Trailing updates with the C block staged through the TMA unit (FIND_B200_CSTAGE=1; dmma_engine.cuh:
+// faster standalone, slower inside the solver)
+const bool g_cstage = [] {
+  const char* f = std::getenv("FIND_B200_CSTAGE");
+  return f && f[0] == '1';
+}();
+
 const bool g_rsym_down = [] {
   const char* f = std::getenv("FIND_B200_RSYM_DOWN");
   return f && f[0] == '1';
@@ -3380,8 +3393,12 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
         }
         case kLTrail:
           if (prm.use_tma && G.max_n >= g_tma_trail_min_n)
-            launch_k(tile_tma_kernel<kLTrail>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
-                     (int64_t)cnt, nE, L.step, L.nb, prm.tile_ctr + si);
+            if (g_cstage)
+              launch_k(tile_tma_kernel<kLTrail, true>, tma_grid(cnt, nE), TmaEng::THREADS, dmma::Eng64cs::SMEM, stream, prm,
+                       tk, (int64_t)cnt, nE, L.step, L.nb, prm.tile_ctr + si);
+            else
+              launch_k(tile_tma_kernel<kLTrail>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
+                       (int64_t)cnt, nE, L.step, L.nb, prm.tile_ctr + si);
           else
             launch_k(trail_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.step, L.nb);
           break;
