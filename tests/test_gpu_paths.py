@@ -38,7 +38,7 @@ print("RESULT", json.dumps(out))
 
 
 @pytest.mark.parametrize("env", [{}, {"FIND_B200_NB": "16"}, {"FIND_B200_NB": "8"}, {"FIND_B200_SMEM_PANEL": "1"},
-                                 {"FIND_B200_TMA": "0"}, {"FIND_B200_TMA_MIN_S": "0"},
+                                 {"FIND_B200_TMA": "0"}, {"FIND_B200_TMA_MIN_S": "0"}, {"FIND_B200_CSTAGE": "1"},
                                  {"FIND_B200_TALL_MIN_PANELS": "0", "FIND_B200_TALL_MIN_ROWS": "32"},
                                  {"FIND_B200_DAG_MAX_N": "100000"}, {"FIND_B200_WIDE_MIN_S": "0"},
                                  {"FIND_B200_INV_LAUNCH": "0"}, {"FIND_B200_STRUCT": "0"},
