@@ -8,6 +8,4 @@ FIND_B200_NB=16 timeout 300 python tools/err_probe.py 1 2 >> $O 2>&1
 FIND_B200_NB=8 timeout 300 python tools/err_probe.py 1 2 >> $O 2>&1
 FIND_B200_STRUCT=0 timeout 300 python tools/err_probe.py 1 2 >> $O 2>&1
 FIND_B200_WIDE_MIN_S=100000 timeout 300 python tools/err_probe.py 1 2 >> $O 2>&1
-FIND_B200_PANEL=reg timeout 300 python tools/err_probe.py 1 >> $O 2>&1
 FIND_B200_SMEM_PANEL=1 timeout 300 python tools/err_probe.py 1 >> $O 2>&1
-FIND_B200_FUSED=1 timeout 300 python tools/err_probe.py 1 >> $O 2>&1
