@@ -3228,6 +3228,12 @@ const int g_tma_min_s = [] {
   const char* f = std::getenv("FIND_B200_TMA_MIN_S");
   return f ? std::atoi(f) : 192;  // below: cfg4 loses < 1 % serialized, cfg1 (latency-bound, many small concurrent groups) gains 2 %
 }();
+// ... or launches of at least this many tiles whatever their s (cfg4's boundary-carrying eliminations: tens of
+// thousands of tiles per launch, where the engine wins; cfg1's stay below)
+const int64_t g_tma_min_tiles = [] {
+  const char* f = std::getenv("FIND_B200_TMA_MIN_TILES");
+  return f ? std::atoll(f) : 16384;
+}();
 const int g_tma_trail_min_n = [] {
   const char* f = std::getenv("FIND_B200_TMA_TRAIL_MIN_N");
   return f ? std::atoi(f) : 0;
@@ -3412,21 +3418,21 @@ int run_one_group(const find_plan* P, const SolveParams& prm_in, int64_t gi, int
           launch_k(finish_kernel, grid, kThreads, std::max<size_t>((size_t)G.max_s * sizeof(int), 16), stream, prm, tk, L.nb);
           break;
         case kLTGemm:
-          if (prm.use_tma && G.max_s >= g_tma_min_s)
+          if (prm.use_tma && (G.max_s >= g_tma_min_s || (int64_t)cnt * nE >= g_tma_min_tiles))
             launch_k(tile_tma_kernel<kLTGemm>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
                      (int64_t)cnt, nE, 0, L.nb, prm.tile_ctr + si);
           else
             launch_k(tgemm_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.nb);
           break;
         case kLRGemm:
-          if (prm.use_tma && G.max_s >= g_tma_min_s)
+          if (prm.use_tma && (G.max_s >= g_tma_min_s || (int64_t)cnt * nE >= g_tma_min_tiles))
             launch_k(tile_tma_kernel<kLRGemm>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
                      (int64_t)cnt, nE, 0, L.nb, prm.tile_ctr + si);
           else
             launch_k(rgemm_kernel, grid, kThreads, Tile64::SMEM, stream, prm, tk, L.nb);
           break;
         case kLSchur:
-          if (prm.use_tma && G.max_s >= g_tma_min_s)
+          if (prm.use_tma && (G.max_s >= g_tma_min_s || (int64_t)cnt * nE >= g_tma_min_tiles))
             launch_k(tile_tma_kernel<kLSchur>, tma_grid(cnt, nE), TmaEng::THREADS, TmaEng::SMEM, stream, prm, tk,
                      (int64_t)cnt, nE, 0, L.nb, prm.tile_ctr + si);
           else
