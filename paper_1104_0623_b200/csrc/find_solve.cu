@@ -713,8 +713,9 @@ struct Tile {
     cp_async_commit();
   }
 
-  // acc += A op(B), or acc -= A op(B) with NEG (acc seeded by load_c: C - A op(B) tiles)
-  template <bool BT2 = BT, bool NEG = false>
+  // acc += A op(B), or acc -= A op(B) with NEG (acc seeded by load_c: C - A op(B) tiles).
+  // NS shared-memory stages (NS - 1 K chunks in flight; smem must hold NS * STAGE elements).
+  template <bool BT2 = BT, bool NEG = false, int NS = 2>
   __device__ __forceinline__ void mma(const double2* A, int64_t lda, const double2* B, int64_t ldb, int Mv, int Nv,
                                       int K, double2* smem) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -726,16 +727,18 @@ struct Tile {
     // zero padding of partial tiles is not multiplied
     const int mtv = min(MT, max(0, (Mv - wm * MT * 8 + 7) / 8));
     const int ntv = min(NT, max(0, (Nv - wn * NT * 8 + 7) / 8));
-    load<BT2>(A, lda, B, ldb, Mv, Nv, K, 0, smem);
+#pragma unroll
+    for (int p = 0; p < NS - 1; ++p) {
+      if (p < nk) load<BT2>(A, lda, B, ldb, Mv, Nv, K, p, smem + p * STAGE);
+      else cp_async_commit();
+    }
     for (int kc = 0; kc < nk; ++kc) {
-      if (kc + 1 < nk) {
-        load<BT2>(A, lda, B, ldb, Mv, Nv, K, kc + 1, smem + ((kc + 1) & 1) * STAGE);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
+      // one commit group per iteration (empty past the end), so wait<NS - 1> always means "chunk kc landed"
+      if (kc + NS - 1 < nk) load<BT2>(A, lda, B, ldb, Mv, Nv, K, kc + NS - 1, smem + ((kc + NS - 1) % NS) * STAGE);
+      else cp_async_commit();
+      cp_async_wait<NS - 1>();
       __syncthreads();
-      const double2* As = smem + (kc & 1) * STAGE;
+      const double2* As = smem + (kc % NS) * STAGE;
       const double2* Bs = As + BM * kSK;
       const int kv = K - kc * kKC;
       if (kv >= kKC && mtv == MT && ntv == NT) {
@@ -2132,7 +2135,7 @@ __global__ void __launch_bounds__(kThreads, 2) schur_kernel(SolveParams P, const
 // ---- X_j = (Y_j - X_{>j} L11[>j, j]) L_jj^-1 for 64 B rows: Z = Y_j - X_{>j} L11[>j, j]
 // (one DMMA tile, K = s - j1) is written to X_j, then X_j = Z L_jj^-1 (second DMMA
 // tile, K = jb) with the inverse published by the panel / TRSM launch of step j.
-template <int NB, class TT = typename XTileSel<NB>::T>
+template <int NB, class TT = typename XTileSel<NB>::T, int NS = 2>
 __device__ void xsolve_tile(const Scr& S, int n, int s, int j, int r0, double2* smem, int rows = kTile) {
   double2* M = S.M;
   const int b = n - s;
@@ -2142,7 +2145,7 @@ __device__ void xsolve_tile(const Scr& S, int n, int s, int j, int r0, double2* 
     TT T;
     T.load_c(M + (int64_t)(s + r0) * n + j0, n, nr, jb);
     if (s > j1)
-      T.template mma<false, true>(S.X + (int64_t)r0 * s + j1, s, M + (int64_t)j1 * n + j0, n, nr, jb, s - j1, smem);
+      T.template mma<false, true, NS>(S.X + (int64_t)r0 * s + j1, s, M + (int64_t)j1 * n + j0, n, nr, jb, s - j1, smem);
     T.for_each([&](int r, int c, double2 v) {
       if (r < nr && c < jb) S.X[(int64_t)(r0 + r) * s + j0 + c] = v;
     });
@@ -2150,7 +2153,7 @@ __device__ void xsolve_tile(const Scr& S, int n, int s, int j, int r0, double2* 
   __syncthreads();
   TT T;
   T.zero();
-  T.mma(S.X + (int64_t)r0 * s + j0, s, S.LINV + (int64_t)j * NB * NB, NB, nr, jb, jb, smem);
+  T.template mma<false, false, NS>(S.X + (int64_t)r0 * s + j0, s, S.LINV + (int64_t)j * NB * NB, NB, nr, jb, jb, smem);
   T.for_each([&](int r, int c, double2 v) {
     if (r < nr && c < jb) S.X[(int64_t)(r0 + r) * s + j0 + c] = v;
   });
@@ -2168,7 +2171,7 @@ __global__ void __launch_bounds__(kThreads) xsolve_kernel(SolveParams P, const T
   const Scr S = scratch_of(P, d, e, NB);
   if (NB == 32 && t.b == 16) {  // 16-row tiles: 4x the CTAs for groups with few row tiles
     for (int j = (d.s + NB - 1) / NB - 1; j >= 0; --j)
-      xsolve_tile<NB, Tile<2, 4, 1, 1, false>>(S, d.n, d.s, j, t.a * 16, reinterpret_cast<double2*>(smem_raw), 16);
+      xsolve_tile<NB, Tile<2, 4, 1, 1, false>, 4>(S, d.n, d.s, j, t.a * 16, reinterpret_cast<double2*>(smem_raw), 16);
     return;
   }
   for (int j = (d.s + NB - 1) / NB - 1; j >= 0; --j)
