@@ -46,3 +46,17 @@ def test_solve_rejects_bad_arguments_without_gpu():
     st = _native.FindStatus()
     rc = lib.find_solve(None, None, None, 1, 1, 1, 1e-12, None, None, None, 0, None, C.byref(st))
     assert rc == _native.FIND_EINVAL
+
+
+def test_dense_primitives_reject_bad_arguments_without_gpu():
+    from paper_1104_0623_b200 import _native
+
+    lib = _native.lib()
+    st = _native.FindStatus()
+    h = C.c_void_p()
+    assert lib.find_dense_create(0, 1, C.byref(h), C.byref(st)) == _native.FIND_EINVAL
+    assert lib.find_dense_create(8, 0, C.byref(h), C.byref(st)) == _native.FIND_EINVAL
+    assert lib.find_dense_inverse(None, None, None, None, None, C.byref(st)) == _native.FIND_EINVAL
+    rc = lib.find_zgemm_batched(1, 4, 4, 4, None, 4, 16, None, 4, 16, 0, None, 4, 16, 0, None, C.byref(st))
+    assert rc == _native.FIND_EINVAL
+    lib.find_dense_destroy(None)  # no-op
